@@ -1,0 +1,221 @@
+/*
+ * hqmq_b200 — C ABI of the B200-native HQMQ KV-cache codec.
+ *
+ * Drop-in boundary for the reference package's codec path
+ * (/root/reference/pkg/src/hqmq/).  Every entry point takes plain device
+ * pointers and sizes (caller-allocated, e.g. by torch), is asynchronous on the
+ * caller's CUDA stream (`stream` is a cudaStream_t passed as void*; NULL = the
+ * legacy default stream), holds no global mutable state, and returns an
+ * hqmq_status.  Data-dependent failures that the reference raises as Python
+ * exceptions are reported through a device-resident error word (HQMQ_DEVERR_*)
+ * that the host maps to the reference's exception types after it synchronises.
+ *
+ * Reference interfaces replaced (file:line under /root/reference/pkg/src/hqmq):
+ *   hqmq_nearest_scan        <- _kernels.nearest_scan        (_kernels.pyx:16-46,
+ *                               dispatched by kernels.nearest_scan, kernels.py:54-63)
+ *   hqmq_encode              <- codec.encode_tensor          (codec.py:232-287),
+ *                               including outliers.lower_median (outliers.py:50-55),
+ *                               radius.quantize_radii (radius.py:35-47) and the
+ *                               kvpack section bit streams (kvpack.py:66-76,134-146)
+ *   hqmq_decode              <- codec.decode_token_range     (codec.py:290-328)
+ *                               and codec.decode_tensor       (codec.py:331-336)
+ *   hqmq_unpack              <- kvpack._unpack_uint_stream   (kvpack.py:79-87) and the
+ *                               flag/index/quanta scatter of kvpack.from_bytes
+ *                               (kvpack.py:264-287)
+ *   hqmq_token_offsets       <- the cumsum(flags) payload addressing of
+ *                               codec.decode_token_range     (codec.py:322-325)
+ *   hqmq_validate_indices    <- the index range checks of kvpack.from_bytes
+ *                               (kvpack.py:279-280) / decode_token_range (codec.py:305-309)
+ *   hqmq_attention_decode    <- attention.fused_attend       (attention.py:137-199)
+ */
+#ifndef HQMQ_B200_H
+#define HQMQ_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ------------------------------------------------------------- statuses */
+typedef enum {
+  HQMQ_OK = 0,
+  HQMQ_ERR_INVALID_ARGUMENT = 1, /* maps to errors.InvalidArgument (errors.py:4) */
+  HQMQ_ERR_CUDA = 2,             /* a CUDA launch/runtime call failed            */
+  HQMQ_ERR_WORKSPACE = 3,        /* workspace smaller than *_workspace_bytes()   */
+  HQMQ_ERR_UNSUPPORTED = 4       /* shape outside what the kernels implement     */
+} hqmq_status;
+
+/* Device error word bits (uint32 written with atomicOr). */
+#define HQMQ_DEVERR_SIGMA_NONPOSITIVE 0x1u /* radius.py:42-43 -> InvalidArgument  */
+#define HQMQ_DEVERR_INDEX_RANGE 0x2u       /* codec.py:305-309 -> CorruptData      */
+
+/* Element types of dense tensors. */
+typedef enum {
+  HQMQ_F16 = 0,
+  HQMQ_BF16 = 1,
+  HQMQ_F32 = 2,
+  HQMQ_F64 = 3
+} hqmq_dtype;
+
+/* Version / diagnostics. */
+const char* hqmq_version(void);
+const char* hqmq_status_string(int status);
+/* Last CUDA error string recorded by a failing call on this thread. */
+const char* hqmq_last_error(void);
+
+/* --------------------------------------------------------- nearest scan */
+/* Exact twin of _kernels.nearest_scan (_kernels.pyx:16-46): for each of the n
+ * directions (n x 4 fp64) the argmax over the m codewords (m x 4 fp64) of
+ * ((u0*c0 + u1*c1) + u2*c2) + u3*c3 in fp64 without FMA, ties to the lowest
+ * index, best initialised to -2.0.  idx: n int64, cos: n fp64 (device). */
+int hqmq_nearest_scan(const double* dirs, int64_t n, const double* codewords, int64_t m,
+                      int64_t* idx, double* cos, void* stream);
+
+/* --------------------------------------------------------------- encode */
+/* One (layer, role) call of codec.encode_tensor (codec.py:232-287) over a
+ * dense (batch, heads, tokens, head_dim) tensor.  Outputs are the kvpack
+ * sections (kvpack.py:134-146) in HBM:
+ *   scales        fp16 bits, one per (batch, head, token)
+ *   index_words   LSB-first stream of index_bits-wide codes of the UNFLAGGED
+ *                 chunks in scan order (32-bit little-endian words)
+ *   radius_words  same at radius_bits
+ *   flag_words    1 bit per chunk (all chunks), present iff multiplier > 0
+ *   payloads      fp16 4-tuples of flagged chunks in scan order
+ *   token_offsets coded-stream position of each token's first chunk (u32),
+ *                 written iff multiplier > 0 (decode addressing)
+ * Capacities: index_words >= ceil(n_chunks*index_bits/32)+1 words, radius_words
+ * >= ceil(n_chunks*radius_bits/32)+1, flag_words >= ceil(n_chunks/32)+1,
+ * payloads >= n_chunks rows (or the caller's bound), all zero-filled by
+ * hqmq_encode itself.  counters[0] = n_coded, counters[1] = n_payload rows
+ * (int64, device).  Tables are prepared by the host from the numpy codebooks
+ * (codebook.py:53-81):
+ *   rot_f32   [heads][S][16] fp32: the conj(secondary) rotation as 8 float2
+ *             pairs (see csrc/encode.cu)
+ *   joint_f64 [heads][24*S][4] fp64: the reference joint table, flat p*S+s */
+typedef struct {
+  int64_t batch, heads, tokens, head_dim;
+  int32_t codebook_size; /* S */
+  int32_t radius_bits;   /* b_r, 1..8 */
+  int32_t index_bits;    /* ceil(log2(24*S)) (codec.py:110-113) */
+  int32_t input_dtype;   /* hqmq_dtype */
+  double outlier_multiplier; /* <= 0 disables extraction (codec.py:212) */
+  int32_t per_head_pooling;  /* 0 = "batch", 1 = "per_head" (codec.py:214-219) */
+  int32_t _pad0;
+  const void* data;
+  const float* rot_f32;
+  const double* joint_f64;
+  uint16_t* scales;
+  uint32_t* index_words;
+  uint32_t* radius_words;
+  uint32_t* flag_words;
+  uint16_t* payloads;
+  uint32_t* token_offsets;
+  int64_t payload_capacity; /* rows available in `payloads` */
+  int64_t* counters;        /* [0] n_coded, [1] n_payload, [2] n_fixup (diagnostic) */
+  uint32_t* error_word;
+  void* workspace;
+  size_t workspace_bytes;
+  size_t index_capacity_words;
+  size_t radius_capacity_words;
+  size_t flag_capacity_words;
+} hqmq_encode_args;
+
+size_t hqmq_encode_workspace_bytes(const hqmq_encode_args* args);
+int hqmq_encode(const hqmq_encode_args* args, void* stream);
+
+/* --------------------------------------------------------------- decode */
+/* codec.decode_token_range (codec.py:290-328) for tokens [token_start,
+ * token_stop) of every (batch, head) row, written densely as
+ * (batch, heads, token_stop-token_start, head_dim) in out_dtype.  HQMQ_F64
+ * output is bit-identical to the reference; HQMQ_F32 is within 1e-6 relative.
+ * joint_f32 / joint_f64: [heads][24*S][4] (only the one matching out_dtype's
+ * precision is read: F64 -> joint_f64, others -> joint_f32). */
+typedef struct {
+  int64_t batch, heads, tokens, head_dim;
+  int32_t codebook_size;
+  int32_t radius_bits;
+  int32_t index_bits;
+  int32_t out_dtype;
+  int64_t token_start, token_stop;
+  const uint16_t* scales;
+  const uint32_t* index_words;
+  const uint32_t* radius_words;
+  const uint32_t* flag_words;    /* NULL when extraction is disabled */
+  const uint16_t* payloads;      /* NULL when extraction is disabled */
+  const uint32_t* token_offsets; /* NULL when extraction is disabled */
+  const float* joint_f32;
+  const double* joint_f64;
+  void* out;
+  uint32_t* error_word;
+} hqmq_decode_args;
+
+int hqmq_decode(const hqmq_decode_args* args, void* stream);
+
+/* Unpack the sections into the reference's dense QuantizedTensor arrays
+ * (codec.py:124-147): indices int32, quanta uint8, flags uint8 (0/1), each
+ * (batch, heads, tokens, chunks); entries at flagged positions are zero. */
+int hqmq_unpack(const hqmq_decode_args* args, int32_t* indices, uint8_t* quanta,
+                uint8_t* flags, void* stream);
+
+/* Pack dense arrays (indices int32, quanta uint8, flags uint8 or NULL) into
+ * the section streams (the inverse of hqmq_unpack; kvpack.py:134-146).
+ * index/radius/flag word buffers must be zero-filled by the caller. */
+int hqmq_pack(int64_t n_chunks, int32_t chunks_per_token, int32_t index_bits,
+              int32_t radius_bits, const int32_t* indices, const uint8_t* quanta,
+              const uint8_t* flags, uint32_t* index_words, uint32_t* radius_words,
+              uint32_t* flag_words, uint32_t* token_offsets, void* workspace,
+              size_t workspace_bytes, void* stream);
+size_t hqmq_pack_workspace_bytes(int64_t n_chunks);
+
+/* Coded-stream offset of each token (exclusive prefix count of unflagged
+ * chunks), from a flag bitmap; n_tokens = batch*heads*tokens. */
+int hqmq_token_offsets(int64_t n_tokens, int32_t chunks_per_token, const uint32_t* flag_words,
+                       uint32_t* token_offsets, void* workspace, size_t workspace_bytes,
+                       void* stream);
+size_t hqmq_token_offsets_workspace_bytes(int64_t n_tokens);
+
+/* Set HQMQ_DEVERR_INDEX_RANGE if any of the n_codes index codes >= limit. */
+int hqmq_validate_indices(const uint32_t* index_words, int64_t n_codes, int32_t index_bits,
+                          int64_t limit, uint32_t* error_word, void* stream);
+
+/* ------------------------------------------------------------ attention */
+/* attention.fused_attend (attention.py:137-199) with the K/V decode fused into
+ * the kernel (the dense K/V never exist in HBM).  q: (batch, q_heads,
+ * q_tokens, head_dim) fp32; out: same shape fp32.  K and V are two encoded
+ * tensors (role K / role V) of shape (batch, kv_heads, kv_tokens, head_dim)
+ * sharing codebook_size / radius_bits / index_bits.  Grouped queries: query
+ * head h reads kv head h / (q_heads/kv_heads); causal: key j visible to query
+ * i iff j <= i + (kv_tokens - q_tokens) (attention.py:29-69). */
+typedef struct {
+  const uint16_t* scales;
+  const uint32_t* index_words;
+  const uint32_t* radius_words;
+  const uint32_t* flag_words;
+  const uint16_t* payloads;
+  const uint32_t* token_offsets;
+  const float* joint_f32; /* [kv_heads][24*S][4] */
+} hqmq_packed_view;
+
+typedef struct {
+  int64_t batch, q_heads, kv_heads, q_tokens, kv_tokens, head_dim;
+  int32_t codebook_size, radius_bits, index_bits, causal;
+  double scale;
+  const float* q;
+  hqmq_packed_view k, v;
+  float* out;
+  int32_t num_splits; /* 0 = choose automatically */
+  int32_t _pad0;
+  void* workspace;
+  size_t workspace_bytes;
+} hqmq_attention_args;
+
+size_t hqmq_attention_workspace_bytes(const hqmq_attention_args* args);
+int hqmq_attention_decode(const hqmq_attention_args* args, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HQMQ_B200_H */

@@ -1,0 +1,218 @@
+"""Seeded codebooks (host side, numpy) and their device tables.
+
+Host restatement of the reference's codebook construction so the tables are
+bit-identical to the reference's:
+
+* keyed streams: SplitMix64 hash chain -> Philox4x64 key, counter 0
+  (rng.py:39-106), Box-Muller on 53-bit uniforms (rng.py:84-101);
+* Haar secondaries: normalised 4-d Gaussians with prefix-stable resampling of
+  zero draws (quat.py:76-91), keyed (0x5345434F, seed, layer, head, role tag)
+  (rng.py:31,104-106; codebook.py:53-71);
+* the 24-element primary group 2T in canonical order (hurwitz.py:10-36);
+* the joint table codewords[p*S + s] = P[p] (x) Sec[s] (codebook.py:74-81).
+
+The generation must stay in numpy on the host: numpy's SIMD log/cos/sin are
+part of the reference's definition of the codebook bits (SURVEY.md §7 hard
+part 3).  What is new here is the device side: CodebookBank uploads, once per
+(layer, head, role), the three tables the sm_100a kernels consume and keeps
+them resident in HBM:
+
+* rot_f32   (S, 16) fp32 — conj(secondary) as 8 float2 pairs for the FFMA2
+  rotation v = u (x) conj(q_s) of the encode search;
+* joint_f64 (24S, 4) fp64 — the reference table, for exact fixup / fp64 decode;
+* joint_f32 (24S, 4) fp32 — the same rounded to fp32, for decode / attention.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .errors import InvalidArgument
+
+_MASK64 = (1 << 64) - 1
+
+ROLE_TAGS = {"K": 0x4B, "V": 0x56}
+TAG_SECONDARY = 0x5345434F
+TAG_SYNTH = 0x53594E54
+GROUP_ORDER = 24
+UNIT_TOL = 1e-6
+
+
+def splitmix64(z: int) -> int:
+    z = (z + 0x9E3779B97F4A7C15) & _MASK64
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & _MASK64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & _MASK64
+    return z ^ (z >> 31)
+
+
+def mix64(*words: int) -> int:
+    h = 0
+    for w in words:
+        h = splitmix64(h ^ (int(w) & _MASK64))
+    return h
+
+
+class RandomStream:
+    """Forward-only keyed stream (rng.py:59-101)."""
+
+    def __init__(self, *key_words: int):
+        self.key_words = tuple(int(w) for w in key_words)
+        key = np.array([mix64(*key_words), mix64(*key_words, 1)], dtype=np.uint64)
+        self._bitgen = np.random.Philox(key=key)
+
+    def raw(self, n: int) -> np.ndarray:
+        if n <= 0:
+            return np.empty(0, dtype=np.uint64)
+        return np.atleast_1d(np.asarray(self._bitgen.random_raw(n), dtype=np.uint64))
+
+    def uniform(self, n: int) -> np.ndarray:
+        return (self.raw(n) >> np.uint64(11)).astype(np.float64) * 2.0**-53
+
+    def gaussian(self, n: int) -> np.ndarray:
+        m = (n + 1) // 2
+        r = self.raw(2 * m)
+        u1 = ((r[0::2] >> np.uint64(11)).astype(np.float64) + 1.0) * 2.0**-53
+        u2 = (r[1::2] >> np.uint64(11)).astype(np.float64) * 2.0**-53
+        radial = np.sqrt(-2.0 * np.log(u1))
+        theta = 2.0 * np.pi * u2
+        out = np.empty(2 * m, dtype=np.float64)
+        out[0::2] = radial * np.cos(theta)
+        out[1::2] = radial * np.sin(theta)
+        return out[:n]
+
+
+def hamilton(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    w1, x1, y1, z1 = np.moveaxis(np.asarray(a, np.float64), -1, 0)
+    w2, x2, y2, z2 = np.moveaxis(np.asarray(b, np.float64), -1, 0)
+    return np.stack(
+        [
+            w1 * w2 - x1 * x2 - y1 * y2 - z1 * z2,
+            w1 * x2 + x1 * w2 + y1 * z2 - z1 * y2,
+            w1 * y2 - x1 * z2 + y1 * w2 + z1 * x2,
+            w1 * z2 + x1 * y2 - y1 * x2 + z1 * w2,
+        ],
+        axis=-1,
+    )
+
+
+def primary_entries() -> np.ndarray:
+    """The 24 unit Hurwitz quaternions in canonical order (hurwitz.py:28-36)."""
+    e = np.zeros((GROUP_ORDER, 4), dtype=np.float64)
+    for axis in range(4):
+        e[2 * axis, axis] = 1.0
+        e[2 * axis + 1, axis] = -1.0
+    for bits in range(16):
+        signs = [1.0 if not (bits >> (3 - k)) & 1 else -1.0 for k in range(4)]
+        e[8 + bits] = np.array(signs) * 0.5
+    return e
+
+
+def haar_quaternions(stream: RandomStream, n: int) -> np.ndarray:
+    g = stream.gaussian(4 * n).reshape(n, 4)
+    norms = np.sqrt((g * g).sum(axis=1))
+    while True:
+        bad = np.flatnonzero(norms == 0.0)
+        if bad.size == 0:
+            break
+        g[bad] = stream.gaussian(4 * bad.size).reshape(-1, 4)
+        norms[bad] = np.sqrt((g[bad] * g[bad]).sum(axis=1))
+    return g / norms[:, None]
+
+
+@dataclass(frozen=True)
+class SecondaryCodebook:
+    entries: np.ndarray
+    seed: int
+    layer: int
+    head: int
+    role: str
+
+    @property
+    def size(self) -> int:
+        return self.entries.shape[0]
+
+
+@dataclass(frozen=True)
+class JointCodebook:
+    secondary: SecondaryCodebook
+    codewords: np.ndarray
+
+    @property
+    def size(self) -> int:
+        return self.secondary.size
+
+
+def build_secondary(seed: int, layer: int, head: int, role: str, size: int) -> SecondaryCodebook:
+    if size < 1:
+        raise InvalidArgument(f"codebook size must be >= 1, got {size}")
+    if role not in ROLE_TAGS:
+        raise InvalidArgument(f"role must be one of {sorted(ROLE_TAGS)}, got {role!r}")
+    if layer < 0 or head < 0:
+        raise InvalidArgument("layer and head must be nonnegative")
+    stream = RandomStream(TAG_SECONDARY, seed, layer, head, ROLE_TAGS[role])
+    return SecondaryCodebook(haar_quaternions(stream, size), seed, layer, head, role)
+
+
+_PRIMARY = primary_entries()
+
+
+def build_joint(secondary: SecondaryCodebook) -> JointCodebook:
+    cw = hamilton(_PRIMARY[:, None, :], secondary.entries[None, :, :]).reshape(-1, 4)
+    return JointCodebook(secondary, cw)
+
+
+def effective_size(size: int) -> int:
+    return GROUP_ORDER * size
+
+
+def rotation_table(secondary: np.ndarray) -> np.ndarray:
+    """(S, 16) fp32 pairs for v = u (x) conj(s) as two float2 FMA chains.
+
+    With s = (e, f, g, h) and u = (a, b, c, d):
+      (w, x) = a(e,-f) + b(f,e) + c(g,-h) + d(h,g)
+      (y, z) = a(-g,-h) + b(h,-g) + c(e,f) + d(-f,e)
+    """
+    s = np.asarray(secondary, dtype=np.float64).astype(np.float32)
+    e, f, g, h = s[:, 0], s[:, 1], s[:, 2], s[:, 3]
+    return np.stack([e, -f, f, e, g, -h, h, g, -g, -h, h, -g, e, f, -f, e], axis=1).astype(
+        np.float32
+    )
+
+
+@dataclass
+class CodebookBank:
+    """Lazily built joint codebooks for one (seed, size) (codebook.py:98-118),
+    plus their HBM-resident device tables for the sm_100a kernels."""
+
+    seed: int
+    size: int
+    _cache: dict = field(default_factory=dict, repr=False)
+    _dev: dict = field(default_factory=dict, repr=False)
+
+    def joint(self, layer: int, head: int, role: str) -> JointCodebook:
+        key = (layer, head, role)
+        found = self._cache.get(key)
+        if found is None:
+            found = build_joint(build_secondary(self.seed, layer, head, role, self.size))
+            self._cache[key] = found
+        return found
+
+    def device_tables(self, layer: int, head_base: int, heads: int, role: str, device) -> dict:
+        """Stacked (heads, ...) device tables for heads head_base..head_base+heads-1."""
+        import torch
+
+        key = (layer, head_base, heads, role, str(device))
+        found = self._dev.get(key)
+        if found is None:
+            joints = [self.joint(layer, head_base + h, role) for h in range(heads)]
+            rot = np.stack([rotation_table(j.secondary.entries) for j in joints])
+            j64 = np.stack([j.codewords for j in joints])
+            found = {
+                "rot_f32": torch.from_numpy(np.ascontiguousarray(rot)).to(device),
+                "joint_f64": torch.from_numpy(np.ascontiguousarray(j64)).to(device),
+                "joint_f32": torch.from_numpy(np.ascontiguousarray(j64.astype(np.float32))).to(device),
+            }
+            self._dev[key] = found
+        return found

@@ -1,0 +1,465 @@
+"""HQMQ codec API on B200: encode/decode of KV tensors through the sm_100a kernels.
+
+Mirrors the reference quantizer API (codec.py:49-349): TensorShape,
+CodecConfig, QuantizedTensor, encode_tensor, decode_tensor,
+decode_token_range and quantize_dequantize keep their names, argument
+meaning, validation and exception types.  What changes is where the data
+lives: inputs may be torch tensors (any device) or numpy arrays, and the
+QuantizedTensor holds the compressed cache in HBM in its packed form — the
+five kvpack sections (kvpack.py:134-146) plus per-token coded offsets — which
+is what the decode and fused-attention kernels read.  The reference's dense
+views (indices / quanta / flags / payloads, codec.py:124-147) are produced on
+demand by the unpack kernel and are read-only snapshots.
+
+No CPU fallback exists: without the C-ABI library or a CUDA device every
+entry point raises NativeLibraryMissing.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native as nat
+from .codebook import ROLE_TAGS, CodebookBank, effective_size
+from .errors import CorruptData, InvalidArgument
+
+CHUNK_DIM = 4
+MEDIAN_POOLING_MODES = ("batch", "per_head")
+MIN_BITS = 1
+MAX_BITS = 8
+
+
+@dataclass(frozen=True)
+class TensorShape:
+    """codec.py:49-72."""
+
+    batch: int
+    heads: int
+    tokens: int
+    head_dim: int
+
+    def __post_init__(self):
+        if self.batch < 1 or self.heads < 1 or self.head_dim < 1:
+            raise InvalidArgument(f"degenerate tensor shape {self}")
+        if self.tokens < 0:
+            raise InvalidArgument("token count must be nonnegative")
+
+    @property
+    def chunks_per_vector(self) -> int:
+        return -(-self.head_dim // CHUNK_DIM)
+
+    @property
+    def padded_dim(self) -> int:
+        return self.chunks_per_vector * CHUNK_DIM
+
+    @property
+    def elements(self) -> int:
+        return self.batch * self.heads * self.tokens * self.head_dim
+
+    @property
+    def n_chunks(self) -> int:
+        return self.batch * self.heads * self.tokens * self.chunks_per_vector
+
+
+@dataclass(frozen=True)
+class CodecConfig:
+    """codec.py:75-113 (same fields, defaults and validation)."""
+
+    codebook_size: int
+    radius_bits: int
+    seed: int = 0
+    outlier_multiplier: float | None = None
+    median_pooling: str = "batch"
+
+    def __post_init__(self):
+        if self.codebook_size < 1:
+            raise InvalidArgument("codebook size must be >= 1")
+        if not 0 <= self.seed < 2**64:
+            raise InvalidArgument("seed must fit in an unsigned 64-bit word")
+        if not MIN_BITS <= self.radius_bits <= MAX_BITS:
+            raise InvalidArgument(f"radius bits must be in [{MIN_BITS}, {MAX_BITS}]")
+        if self.outlier_multiplier is not None and not self.outlier_multiplier > 0:
+            raise InvalidArgument("outlier multiplier must be positive")
+        if self.median_pooling not in MEDIAN_POOLING_MODES:
+            raise InvalidArgument(f"median pooling must be one of {MEDIAN_POOLING_MODES}")
+
+    @property
+    def index_count(self) -> int:
+        return effective_size(self.codebook_size)
+
+    @property
+    def index_bits(self) -> int:
+        return (self.index_count - 1).bit_length()
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _dtype_code(dt) -> int:
+    torch = _torch()
+    return {torch.float16: nat.F16, torch.bfloat16: nat.BF16, torch.float32: nat.F32,
+            torch.float64: nat.F64}[dt]
+
+
+def _words(bits: int) -> int:
+    # +2 padding words: the bit reader always loads the word after the target.
+    return (bits + 31) // 32 + 2
+
+
+class QuantizedTensor:
+    """Quantized form of one (layer, role) tensor across its heads (codec.py:124-151).
+
+    Device-resident sections: scales (B,H,T) fp16; index/radius bit streams
+    (int32 words, LSB-first); flag bitmap (iff extraction); fp16 payload rows;
+    per-token coded offsets (iff extraction).
+    """
+
+    def __init__(self, shape, config, layer, role, head_base, scales, index_words,
+                 radius_words, flag_words, payload_buf, token_offsets, meta, device,
+                 n_coded=None, n_payload=None):
+        self.shape = shape
+        self.config = config
+        self.layer = layer
+        self.role = role
+        self.head_base = head_base
+        self.scales = scales
+        self.index_words = index_words
+        self.radius_words = radius_words
+        self.flag_words = flag_words
+        self._payload_buf = payload_buf
+        self.token_offsets = token_offsets
+        self._meta = meta  # int64[4]: n_coded, n_payload, n_fixup, error word
+        self.device = device
+        self._n_coded = n_coded
+        self._n_payload = n_payload
+        self._n_fixup = None
+        self._dense = None
+
+    # ------------------------------------------------------------ sync
+    def synchronize(self) -> "QuantizedTensor":
+        """Wait for the encode, read its counters and raise its errors."""
+        if self._n_coded is None:
+            meta = self._meta.cpu().tolist()
+            self._n_coded, self._n_payload, self._n_fixup = int(meta[0]), int(meta[1]), int(meta[2])
+            err = int(meta[3]) & 0xFFFFFFFF
+            if err & nat.DEVERR_SIGMA:
+                raise InvalidArgument("sigma must be positive")
+            if err & nat.DEVERR_INDEX:
+                raise CorruptData("codeword index out of range")
+        return self
+
+    @property
+    def n_coded(self) -> int:
+        return self.synchronize()._n_coded
+
+    @property
+    def n_payload(self) -> int:
+        return self.synchronize()._n_payload
+
+    @property
+    def n_fixup(self) -> int:
+        """Chunks the exact fp64 fixup re-scored (diagnostic)."""
+        self.synchronize()
+        return self._n_fixup or 0
+
+    @property
+    def payloads(self):
+        return self._payload_buf[: self.n_payload]
+
+    @property
+    def outlier_fraction(self) -> float:
+        n = self.shape.n_chunks
+        return self.n_payload / n if n else 0.0
+
+    # ------------------------------------------------------- dense views
+    def _unpack(self):
+        if self._dense is None:
+            torch = _torch()
+            s = self.shape
+            grid = (s.batch, s.heads, s.tokens, s.chunks_per_vector)
+            idx = torch.zeros(grid, dtype=torch.int32, device=self.device)
+            q = torch.zeros(grid, dtype=torch.uint8, device=self.device)
+            fl = torch.zeros(grid, dtype=torch.uint8, device=self.device)
+            if s.n_chunks:
+                args = self._decode_args(0, s.tokens, nat.F32, None, None, None, None)
+                nat.check(nat.lib().hqmq_unpack(ctypes.byref(args), idx.data_ptr(), q.data_ptr(),
+                                                fl.data_ptr(), nat.stream_handle(self.device)),
+                          "hqmq_unpack")
+            self._dense = (idx, q, fl.bool())
+        return self._dense
+
+    @property
+    def indices(self):
+        return self._unpack()[0].clone()
+
+    @property
+    def quanta(self):
+        return self._unpack()[1].clone()
+
+    @property
+    def flags(self):
+        return self._unpack()[2].clone()
+
+    # ----------------------------------------------------------- kernels
+    def _decode_args(self, start, stop, out_dtype, out, err, j32, j64):
+        s, c = self.shape, self.config
+        a = nat.DecodeArgs()
+        a.batch, a.heads, a.tokens, a.head_dim = s.batch, s.heads, s.tokens, s.head_dim
+        a.codebook_size, a.radius_bits, a.index_bits = c.codebook_size, c.radius_bits, c.index_bits
+        a.out_dtype = out_dtype
+        a.token_start, a.token_stop = start, stop
+        a.scales = self.scales.data_ptr()
+        a.index_words = self.index_words.data_ptr()
+        a.radius_words = self.radius_words.data_ptr()
+        a.flag_words = self.flag_words.data_ptr() if self.flag_words is not None else None
+        a.payloads = self._payload_buf.data_ptr() if self.flag_words is not None else None
+        a.token_offsets = self.token_offsets.data_ptr() if self.token_offsets is not None else None
+        a.joint_f32 = j32.data_ptr() if j32 is not None else None
+        a.joint_f64 = j64.data_ptr() if j64 is not None else None
+        a.out = out.data_ptr() if out is not None else None
+        a.error_word = err.data_ptr() if err is not None else None
+        return a
+
+    def packed_view(self, bank: CodebookBank) -> nat.PackedView:
+        tabs = bank.device_tables(self.layer, self.head_base, self.shape.heads, self.role,
+                                  self.device)
+        v = nat.PackedView()
+        v.scales = self.scales.data_ptr()
+        v.index_words = self.index_words.data_ptr()
+        v.radius_words = self.radius_words.data_ptr()
+        v.flag_words = self.flag_words.data_ptr() if self.flag_words is not None else None
+        v.payloads = self._payload_buf.data_ptr() if self.flag_words is not None else None
+        v.token_offsets = self.token_offsets.data_ptr() if self.token_offsets is not None else None
+        v.joint_f32 = tabs["joint_f32"].data_ptr()
+        return v
+
+    # ---------------------------------------------------------- sections
+    def section_bytes(self) -> list:
+        """The five kvpack sections (kvpack.py:134-146) as bytes."""
+        s, c = self.shape, self.config
+        n_coded = self.n_coded
+        scales = self.scales.contiguous().cpu().numpy().astype("<f2").tobytes()
+
+        def stream(words, width):
+            nbytes = (n_coded * width + 7) // 8
+            raw = words.cpu().numpy().astype("<u4").tobytes()
+            return raw[:nbytes]
+
+        idx = stream(self.index_words, c.index_bits)
+        rad = stream(self.radius_words, c.radius_bits)
+        if c.outlier_multiplier is not None:
+            fl = self.flag_words.cpu().numpy().astype("<u4").tobytes()[: (s.n_chunks + 7) // 8]
+        else:
+            fl = b""
+        pay = self.payloads.contiguous().cpu().numpy().astype("<f2").tobytes()
+        return [scales, idx, rad, fl, pay]
+
+    # -------------------------------------------------------- construct
+    @classmethod
+    def from_arrays(cls, shape: TensorShape, config: CodecConfig, layer: int, role: str,
+                    scales, indices, quanta, flags, payloads, head_base: int = 0,
+                    device="cuda") -> "QuantizedTensor":
+        """Pack dense arrays (the reference's QuantizedTensor fields) into sections."""
+        torch = _torch()
+        nat.require_cuda(device)
+        device = torch.device(device)
+        s, c = shape, config
+        n = s.n_chunks
+        grid = (s.batch, s.heads, s.tokens, s.chunks_per_vector)
+        to = lambda a, dt: torch.as_tensor(np.asarray(a) if not torch.is_tensor(a) else a).to(
+            device=device, dtype=dt).contiguous()
+        idx = to(indices, torch.int32).reshape(grid)
+        q = to(quanta, torch.uint8).reshape(grid)
+        ext = c.outlier_multiplier is not None
+        fl = to(flags, torch.uint8).reshape(grid) if ext else None
+        if idx.numel() and (int(idx.min()) < 0 or int(idx.max()) >= c.index_count):
+            raise CorruptData("codeword index out of range")
+        n_flag = int(fl.sum()) if ext else 0
+        iw = torch.zeros(_words(n * c.index_bits), dtype=torch.int32, device=device)
+        rw = torch.zeros(_words(n * c.radius_bits), dtype=torch.int32, device=device)
+        fw = torch.zeros(_words(n), dtype=torch.int32, device=device) if ext else None
+        tok = torch.zeros(max(1, s.batch * s.heads * s.tokens), dtype=torch.int32,
+                          device=device) if ext else None
+        ws = torch.empty(int(nat.lib().hqmq_pack_workspace_bytes(n)), dtype=torch.uint8,
+                         device=device)
+        nat.check(nat.lib().hqmq_pack(
+            n, s.chunks_per_vector, c.index_bits, c.radius_bits, idx.data_ptr(), q.data_ptr(),
+            fl.data_ptr() if ext else None, iw.data_ptr(), rw.data_ptr(),
+            fw.data_ptr() if ext else None, tok.data_ptr() if ext else None,
+            ws.data_ptr(), ws.numel(), nat.stream_handle(device)), "hqmq_pack")
+        sc = torch.as_tensor(np.asarray(scales, dtype=np.float16) if not torch.is_tensor(scales)
+                             else scales).to(device=device, dtype=torch.float16).reshape(
+                                 s.batch, s.heads, s.tokens).contiguous()
+        pay = torch.as_tensor(np.asarray(payloads, dtype=np.float16) if not torch.is_tensor(payloads)
+                              else payloads).to(device=device, dtype=torch.float16).reshape(-1, 4)
+        if pay.shape[0] != n_flag:
+            raise CorruptData("payload count does not match the flags")
+        pay_buf = torch.zeros((max(1, n_flag), 4), dtype=torch.float16, device=device)
+        pay_buf[:n_flag] = pay
+        meta = torch.tensor([n - n_flag, n_flag, 0, 0], dtype=torch.int64, device=device)
+        return cls(s, c, layer, role, head_base, sc, iw, rw, fw, pay_buf, tok, meta, device,
+                   n_coded=n - n_flag, n_payload=n_flag)
+
+    @classmethod
+    def from_reference(cls, packed, device="cuda") -> "QuantizedTensor":
+        """Wrap a reference (numpy) QuantizedTensor, e.g. hqmq.codec.QuantizedTensor."""
+        rs, rc = packed.shape, packed.config
+        shape = TensorShape(rs.batch, rs.heads, rs.tokens, rs.head_dim)
+        config = CodecConfig(rc.codebook_size, rc.radius_bits, rc.seed, rc.outlier_multiplier,
+                             rc.median_pooling)
+        return cls.from_arrays(shape, config, packed.layer, packed.role, packed.scales,
+                               packed.indices, packed.quanta, packed.flags, packed.payloads,
+                               packed.head_base, device)
+
+
+# --------------------------------------------------------------- helpers
+def _bank_for(config: CodecConfig, bank: CodebookBank | None) -> CodebookBank:
+    """codec.py:222-229."""
+    if bank is None:
+        return CodebookBank(seed=config.seed, size=config.codebook_size)
+    if bank.seed != config.seed or bank.size != config.codebook_size:
+        raise InvalidArgument("codebook bank does not match the codec config (seed or size)")
+    return bank
+
+
+def _as_device_4d(data, device):
+    torch = _torch()
+    if not torch.is_tensor(data):
+        arr = np.asarray(data)
+        if arr.dtype not in (np.float16, np.float32, np.float64):
+            arr = arr.astype(np.float64)
+        data = torch.from_numpy(np.ascontiguousarray(arr))
+    if data.dtype not in (torch.float16, torch.bfloat16, torch.float32, torch.float64):
+        data = data.to(torch.float64)
+    if data.dim() != 4:
+        raise InvalidArgument(f"expected (batch, heads, tokens, head_dim) data, got ndim={data.dim()}")
+    nat.require_cuda(device)
+    if device is None:
+        device = data.device if data.is_cuda else torch.device("cuda", torch.cuda.current_device())
+    data = data.to(device=device, non_blocking=True).contiguous()
+    return data, TensorShape(*data.shape), torch.device(device)
+
+
+def encode_tensor(data, config: CodecConfig, layer: int = 0, role: str = "K",
+                  bank: CodebookBank | None = None, head_base: int = 0, *,
+                  device=None, sync: bool = True) -> QuantizedTensor:
+    """Quantize a (batch, heads, tokens, head_dim) tensor (codec.py:232-287).
+
+    Runs Med3x, the fused encode kernel and the section packing on the GPU.
+    sync=True (reference semantics) waits for the kernels and raises
+    InvalidArgument on a non-positive scale; sync=False returns immediately and
+    defers that check to QuantizedTensor.synchronize().
+    """
+    torch = _torch()
+    if role not in ROLE_TAGS:
+        raise InvalidArgument(f"role must be one of {sorted(ROLE_TAGS)}")
+    if head_base < 0:
+        raise InvalidArgument("head_base must be nonnegative")
+    data, shape, device = _as_device_4d(data, device)
+    bank = _bank_for(config, bank)
+    c = config
+    n = shape.n_chunks
+    ext = c.outlier_multiplier is not None
+    rows_t = shape.batch * shape.heads * shape.tokens
+    scales = torch.empty((shape.batch, shape.heads, shape.tokens), dtype=torch.float16,
+                         device=device)
+    iw = torch.empty(_words(n * c.index_bits), dtype=torch.int32, device=device)
+    rw = torch.empty(_words(n * c.radius_bits), dtype=torch.int32, device=device)
+    fw = torch.empty(_words(n), dtype=torch.int32, device=device) if ext else None
+    tok = torch.empty(max(1, rows_t), dtype=torch.int32, device=device) if ext else None
+    if ext:
+        groups = shape.heads if c.median_pooling == "per_head" else 1
+        cap = n // 2 + groups + 1 if c.outlier_multiplier >= 1.0 else n + 1
+    else:
+        cap = 1
+    pay = torch.empty((cap, 4), dtype=torch.float16, device=device)
+    meta = torch.zeros(4, dtype=torch.int64, device=device)
+    tabs = bank.device_tables(layer, head_base, shape.heads, role, device)
+    a = nat.EncodeArgs()
+    a.batch, a.heads, a.tokens, a.head_dim = shape.batch, shape.heads, shape.tokens, shape.head_dim
+    a.codebook_size, a.radius_bits, a.index_bits = c.codebook_size, c.radius_bits, c.index_bits
+    a.input_dtype = _dtype_code(data.dtype)
+    a.outlier_multiplier = float(c.outlier_multiplier) if ext else 0.0
+    a.per_head_pooling = 1 if c.median_pooling == "per_head" else 0
+    a.data = data.data_ptr()
+    a.rot_f32 = tabs["rot_f32"].data_ptr()
+    a.joint_f64 = tabs["joint_f64"].data_ptr()
+    a.scales = scales.data_ptr()
+    a.index_words, a.radius_words = iw.data_ptr(), rw.data_ptr()
+    a.flag_words = fw.data_ptr() if ext else None
+    a.payloads = pay.data_ptr()
+    a.token_offsets = tok.data_ptr() if ext else None
+    a.payload_capacity = cap if ext else 0
+    a.counters = meta.data_ptr()
+    a.error_word = meta.data_ptr() + 24
+    a.index_capacity_words, a.radius_capacity_words = iw.numel(), rw.numel()
+    a.flag_capacity_words = fw.numel() if ext else 0
+    L = nat.lib()
+    ws_bytes = int(L.hqmq_encode_workspace_bytes(ctypes.byref(a)))
+    ws = torch.empty(max(1, ws_bytes), dtype=torch.uint8, device=device)
+    a.workspace, a.workspace_bytes = ws.data_ptr(), ws_bytes
+    nat.check(L.hqmq_encode(ctypes.byref(a), nat.stream_handle(device)), "hqmq_encode")
+    qt = QuantizedTensor(shape, config, layer, role, head_base, scales, iw, rw, fw, pay, tok,
+                         meta, device)
+    qt._keepalive = (data, ws)
+    if sync:
+        qt.synchronize()
+    return qt
+
+
+_OUT_CODES = None
+
+
+def _out_code(dtype):
+    torch = _torch()
+    table = {torch.float32: nat.F32, torch.float16: nat.F16, torch.bfloat16: nat.BF16,
+             torch.float64: nat.F64}
+    if dtype not in table:
+        raise InvalidArgument("decode dtype must be float16, bfloat16, float32 or float64")
+    return table[dtype]
+
+
+def decode_token_range(packed: QuantizedTensor, bank: CodebookBank, start: int, stop: int,
+                       dtype=None, *, out=None, check: bool = True):
+    """Decode tokens [start, stop) to a dense (B, H, stop-start, head_dim) tensor
+    (codec.py:290-328).  dtype float64 is bit-identical to the reference;
+    float32 (default) is within 1e-6 relative; float16/bfloat16 for serving."""
+    torch = _torch()
+    dtype = torch.float32 if dtype is None else dtype
+    s = packed.shape
+    if not 0 <= start <= stop <= s.tokens:
+        raise InvalidArgument(f"token range [{start}, {stop}) out of bounds")
+    code = _out_code(dtype)
+    dev = packed.device
+    if out is None:
+        out = torch.empty((s.batch, s.heads, stop - start, s.head_dim), dtype=dtype, device=dev)
+    if stop == start:
+        return out
+    tabs = bank.device_tables(packed.layer, packed.head_base, s.heads, packed.role, dev)
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    args = packed._decode_args(start, stop, code, out, err,
+                               tabs["joint_f32"], tabs["joint_f64"])
+    nat.check(nat.lib().hqmq_decode(ctypes.byref(args), nat.stream_handle(dev)), "hqmq_decode")
+    if check and int(err.item()) & nat.DEVERR_INDEX:
+        raise CorruptData("codeword index out of range")
+    return out
+
+
+def decode_tensor(packed: QuantizedTensor, bank: CodebookBank | None = None, dtype=None, *,
+                  out=None, check: bool = True):
+    """Reconstruct the full (batch, heads, tokens, head_dim) tensor (codec.py:331-336)."""
+    bank = _bank_for(packed.config, bank)
+    return decode_token_range(packed, bank, 0, packed.shape.tokens, dtype, out=out, check=check)
+
+
+def quantize_dequantize(data, config: CodecConfig, layer: int = 0, role: str = "K",
+                        bank: CodebookBank | None = None, head_base: int = 0, dtype=None):
+    """Fake-quant round trip (codec.py:339-349)."""
+    bank = _bank_for(config, bank)
+    return decode_tensor(encode_tensor(data, config, layer, role, bank, head_base), bank, dtype)

@@ -1,0 +1,83 @@
+// C-ABI odds and ends: version / status strings / last-error, and the exact
+// device twin of the reference's only native kernel.
+//
+// hqmq_nearest_scan replaces _kernels.nearest_scan (_kernels.pyx:16-46): one
+// warp per direction, lanes stride over the codewords in ascending order with
+// the reference's fp64 association order and strict '>' update, then a warp
+// argmax that prefers the lower index on equal scores — so idx AND cos are
+// bit-identical to the Cython kernel.
+#include <algorithm>
+#include <cstdio>
+
+#include "common.cuh"
+
+namespace hqmq {
+
+namespace {
+thread_local char g_last_error[256] = "";
+}
+
+int record_cuda_error(cudaError_t e) {
+  snprintf(g_last_error, sizeof(g_last_error), "%s", cudaGetErrorString(e));
+  return HQMQ_ERR_CUDA;
+}
+
+__global__ void nearest_scan_kernel(const double* __restrict__ dirs, int64_t n,
+                                    const double* __restrict__ cw, int64_t m,
+                                    int64_t* __restrict__ idx, double* __restrict__ cos) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n;
+       i += warps) {
+    const double u[4] = {dirs[4 * i], dirs[4 * i + 1], dirs[4 * i + 2], dirs[4 * i + 3]};
+    double best = -2.0;
+    long long bj = 0x7fffffffffffffffLL;
+    for (int64_t j = lane; j < m; j += 32) {
+      const double s = exact_dot(u, cw + 4 * j);
+      if (s > best) {
+        best = s;
+        bj = j;
+      }
+    }
+    warp_argmax_lowest(best, bj);
+    if (lane == 0) {
+      // m == 0 (or every score <= -2.0, impossible for finite unit inputs):
+      // the reference leaves best_j = 0, cos = -2.0 (_kernels.pyx:32-33).
+      idx[i] = bj == 0x7fffffffffffffffLL ? 0 : bj;
+      cos[i] = best;
+    }
+  }
+}
+
+}  // namespace hqmq
+
+extern "C" {
+
+const char* hqmq_version(void) { return "hqmq_b200 0.1.0 (sm_100a)"; }
+
+const char* hqmq_status_string(int status) {
+  switch (status) {
+    case HQMQ_OK: return "ok";
+    case HQMQ_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case HQMQ_ERR_CUDA: return "CUDA error";
+    case HQMQ_ERR_WORKSPACE: return "workspace too small";
+    case HQMQ_ERR_UNSUPPORTED: return "unsupported shape";
+    default: return "unknown status";
+  }
+}
+
+const char* hqmq_last_error(void) { return hqmq::g_last_error; }
+
+int hqmq_nearest_scan(const double* dirs, int64_t n, const double* codewords, int64_t m,
+                      int64_t* idx, double* cos, void* stream) {
+  using namespace hqmq;
+  if (n < 0 || m < 0) return HQMQ_ERR_INVALID_ARGUMENT;
+  if (n == 0) return HQMQ_OK;
+  const int threads = 256;
+  const int64_t blocks = std::min<int64_t>(ceil_div(n, threads / 32), 148 * 32);
+  nearest_scan_kernel<<<(unsigned)blocks, threads, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      dirs, n, codewords, m, idx, cos);
+  return check_launch();
+}
+
+}  // extern "C"

@@ -1,0 +1,417 @@
+// HQMQ decode for sm_100a (HBM-bound) plus the section pack / unpack / token
+// offset / index validation helpers.
+//
+// Reference path replaced: codec.decode_token_range (codec.py:290-328),
+// codec.decode_tensor (codec.py:331-336), radius.dequantize_radii
+// (radius.py:50-54) and the kvpack stream codecs (kvpack.py:66-87,264-287).
+//
+// decode_kernel: one CTA column per (batch, head) row; the head's joint table
+// (24*S codewords, fp32 or fp64) is staged once in shared memory and the CTA
+// then streams its slice of the row: per chunk it reads w + b_r bits of the
+// packed streams (funnel shift across 32-bit words) and the token's fp16
+// scale, gathers the codeword from smem and writes the 4 reconstructed
+// elements.  Flagged chunks come from the fp16 payload rows, addressed through
+// the per-token coded offsets.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstdio>
+
+#include "common.cuh"
+
+namespace hqmq {
+
+constexpr int kDecThreads = 256;
+constexpr int kDecR = 4;
+constexpr size_t kDecSmemLimit = 100 * 1024;
+
+template <typename OutT>
+struct Out;
+template <>
+struct Out<float> {
+  static __device__ __forceinline__ float cvt(float v) { return v; }
+};
+template <>
+struct Out<__half> {
+  static __device__ __forceinline__ __half cvt(float v) { return __float2half_rn(v); }
+};
+template <>
+struct Out<__nv_bfloat16> {
+  static __device__ __forceinline__ __nv_bfloat16 cvt(float v) { return __float2bfloat16_rn(v); }
+};
+
+struct DecParams {
+  int64_t B, H, T, D;
+  int C, S, br, w;
+  int64_t t0, nt;  // token range start, count
+  int aligned4;
+  const uint16_t* scales;
+  const uint32_t* idxw;
+  const uint32_t* radw;
+  const uint32_t* flagw;
+  const uint16_t* payloads;
+  const uint32_t* tokoff;
+  const void* table;  // float4 [H][24S] or double [H][24S][4]
+  void* out;
+  uint32_t* err;
+};
+
+// Coded-stream position of chunk (tok, c) and whether it is flagged.
+__device__ __forceinline__ uint64_t coded_pos(const DecParams& p, int64_t tok, int c, bool& flagged) {
+  const uint64_t g = (uint64_t)tok * p.C + c;
+  if (!p.flagw) {
+    flagged = false;
+    return g;
+  }
+  flagged = (__ldg(p.flagw + (g >> 5)) >> (g & 31)) & 1u;
+  // flagged chunks in [tok*C, g)
+  uint64_t b = (uint64_t)tok * p.C;
+  uint32_t nflag = 0;
+  while (b < g) {
+    const uint32_t word = __ldg(p.flagw + (b >> 5));
+    const uint32_t sh = (uint32_t)(b & 31);
+    const uint64_t take = min((uint64_t)(32 - sh), g - b);
+    const uint32_t m = take == 32 ? 0xffffffffu : ((1u << take) - 1u);
+    nflag += __popc((word >> sh) & m);
+    b += take;
+  }
+  return (uint64_t)__ldg(p.tokoff + tok) + (uint64_t)(c - (int)nflag);
+}
+
+template <typename OutT, bool kSmem>
+__global__ void __launch_bounds__(kDecThreads) decode_kernel(DecParams p) {
+  extern __shared__ float4 tab_s[];
+  const int64_t row = blockIdx.y;
+  const int h = (int)(row % p.H);
+  const int ncw = kGroupOrder * p.S;
+  const float4* __restrict__ gtab = reinterpret_cast<const float4*>(p.table) + (int64_t)h * ncw;
+  if (kSmem) {
+    for (int i = threadIdx.x; i < ncw; i += kDecThreads) tab_s[i] = __ldg(gtab + i);
+    __syncthreads();
+  }
+  const float4* tab = kSmem ? tab_s : gtab;
+  const int C = p.C, w = p.w, br = p.br;
+  const float rtop = 1.0f / (float)((1 << br) - 1);
+  const int64_t nck = p.nt * C;  // chunks of this row in range
+  const int64_t per_blk = ceil_div(ceil_div(nck, gridDim.x), (int64_t)C) * C;
+  const int64_t beg = (int64_t)blockIdx.x * per_blk;
+  const int64_t end = min(nck, beg + per_blk);
+  OutT* __restrict__ out = reinterpret_cast<OutT*>(p.out);
+  for (int64_t base = beg; base < end; base += kDecThreads * kDecR) {
+#pragma unroll
+    for (int j = 0; j < kDecR; ++j) {
+      const int64_t ci = base + j * kDecThreads + threadIdx.x;
+      if (ci >= end) continue;
+      const int64_t tr = ci / C;
+      const int c = (int)(ci - tr * C);
+      const int64_t tok = row * p.T + p.t0 + tr;
+      bool fl;
+      const uint64_t pos = coded_pos(p, tok, c, fl);
+      float v[4];
+      if (!fl) {
+        uint32_t idx = read_bits(p.idxw, pos * (uint64_t)w, w);
+        const uint32_t q = read_bits(p.radw, pos * (uint64_t)br, br);
+        if (idx >= (uint32_t)ncw) {
+          atomicOr(p.err, HQMQ_DEVERR_INDEX_RANGE);
+          idx = 0;
+        }
+        const float sig = __half2float(__ushort_as_half(__ldg(p.scales + tok)));
+        const float rad = ((float)q * sig) * rtop;
+        const float4 cw = tab[idx];
+        v[0] = rad * cw.x; v[1] = rad * cw.y; v[2] = rad * cw.z; v[3] = rad * cw.w;
+      } else {
+        const uint64_t prow = (uint64_t)tok * C + c - pos;
+        const ushort4 hv = __ldg(reinterpret_cast<const ushort4*>(p.payloads) + prow);
+        v[0] = __half2float(__ushort_as_half(hv.x));
+        v[1] = __half2float(__ushort_as_half(hv.y));
+        v[2] = __half2float(__ushort_as_half(hv.z));
+        v[3] = __half2float(__ushort_as_half(hv.w));
+      }
+      OutT* o = out + (row * p.nt + tr) * p.D + 4 * c;
+      if (p.aligned4) {
+        if constexpr (sizeof(OutT) == 4) {
+          *reinterpret_cast<float4*>(o) = make_float4(v[0], v[1], v[2], v[3]);
+        } else {
+          OutT tmp[4] = {Out<OutT>::cvt(v[0]), Out<OutT>::cvt(v[1]), Out<OutT>::cvt(v[2]),
+                         Out<OutT>::cvt(v[3])};
+          *reinterpret_cast<uint2*>(o) = *reinterpret_cast<const uint2*>(tmp);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if (4 * c + i < p.D) o[i] = Out<OutT>::cvt(v[i]);
+      }
+    }
+  }
+}
+
+// Bit-exact fp64 decode: ((q * sigma_w) / top) * codeword (codec.py:315-320).
+__global__ void __launch_bounds__(kDecThreads) decode_f64_kernel(DecParams p) {
+  const int64_t row = blockIdx.y;
+  const int h = (int)(row % p.H);
+  const int ncw = kGroupOrder * p.S;
+  const double* __restrict__ tab = reinterpret_cast<const double*>(p.table) + (int64_t)h * ncw * 4;
+  const double top = (double)((1 << p.br) - 1);
+  const int C = p.C;
+  const int64_t nck = p.nt * C;
+  double* __restrict__ out = reinterpret_cast<double*>(p.out);
+  for (int64_t ci = (int64_t)blockIdx.x * kDecThreads + threadIdx.x; ci < nck;
+       ci += (int64_t)gridDim.x * kDecThreads) {
+    const int64_t tr = ci / C;
+    const int c = (int)(ci - tr * C);
+    const int64_t tok = row * p.T + p.t0 + tr;
+    bool fl;
+    const uint64_t pos = coded_pos(p, tok, c, fl);
+    double v[4];
+    if (!fl) {
+      uint32_t idx = read_bits(p.idxw, pos * (uint64_t)p.w, p.w);
+      const uint32_t q = read_bits(p.radw, pos * (uint64_t)p.br, p.br);
+      if (idx >= (uint32_t)ncw) {
+        atomicOr(p.err, HQMQ_DEVERR_INDEX_RANGE);
+        idx = 0;
+      }
+      const double sw = (double)__half2float(__ushort_as_half(__ldg(p.scales + tok)));
+      const double rad = __ddiv_rn(__dmul_rn((double)q, sw), top);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) v[i] = __dmul_rn(rad, __ldg(tab + 4 * (int64_t)idx + i));
+    } else {
+      const uint64_t prow = (uint64_t)tok * C + c - pos;
+      const ushort4 hv = __ldg(reinterpret_cast<const ushort4*>(p.payloads) + prow);
+      v[0] = (double)__half2float(__ushort_as_half(hv.x));
+      v[1] = (double)__half2float(__ushort_as_half(hv.y));
+      v[2] = (double)__half2float(__ushort_as_half(hv.z));
+      v[3] = (double)__half2float(__ushort_as_half(hv.w));
+    }
+    double* o = out + (row * p.nt + tr) * p.D + 4 * c;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (4 * c + i < p.D) o[i] = v[i];
+  }
+}
+
+__global__ void unpack_kernel(DecParams p, int32_t* indices, uint8_t* quanta, uint8_t* flags) {
+  const int64_t n = p.B * p.H * p.T * p.C;
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t tok = g / p.C;
+    const int c = (int)(g - tok * p.C);
+    bool fl;
+    const uint64_t pos = coded_pos(p, tok, c, fl);
+    if (fl) {
+      indices[g] = 0;
+      quanta[g] = 0;
+    } else {
+      indices[g] = (int32_t)read_bits(p.idxw, pos * (uint64_t)p.w, p.w);
+      quanta[g] = (uint8_t)read_bits(p.radw, pos * (uint64_t)p.br, p.br);
+    }
+    flags[g] = fl ? 1 : 0;
+  }
+}
+
+__global__ void coded_mark_kernel(int64_t n, const uint8_t* flags, uint32_t* mark) {
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n;
+       g += (int64_t)gridDim.x * blockDim.x)
+    mark[g] = flags && flags[g] ? 0u : 1u;
+}
+
+__global__ void pack_kernel(int64_t n, int C, int w, int br, const int32_t* indices,
+                            const uint8_t* quanta, const uint8_t* flags, const uint32_t* pos,
+                            uint32_t* idxw, uint32_t* radw, uint32_t* flagw, uint32_t* tokoff) {
+  for (int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; g < n;
+       g += (int64_t)gridDim.x * blockDim.x) {
+    const bool fl = flags && flags[g];
+    const uint64_t ps = pos[g];
+    if (tokoff && (g % C) == 0) tokoff[g / C] = (uint32_t)ps;
+    if (fl) {
+      atomicOr(flagw + (g >> 5), 1u << (g & 31));
+      continue;
+    }
+    const uint32_t iv = (uint32_t)indices[g];
+    const uint64_t bi = ps * (uint64_t)w;
+    atomicOr(idxw + (bi >> 5), iv << (bi & 31));
+    if ((bi & 31) + w > 32) atomicOr(idxw + (bi >> 5) + 1, iv >> (32 - (bi & 31)));
+    const uint32_t qv = (uint32_t)quanta[g];
+    const uint64_t br_ = ps * (uint64_t)br;
+    atomicOr(radw + (br_ >> 5), qv << (br_ & 31));
+    if ((br_ & 31) + br > 32) atomicOr(radw + (br_ >> 5) + 1, qv >> (32 - (br_ & 31)));
+  }
+}
+
+__global__ void token_coded_kernel(int64_t n_tokens, int C, const uint32_t* flagw, uint32_t* cnt) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n_tokens;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t b = (uint64_t)t * C;
+    const uint64_t e = b + C;
+    uint32_t nflag = 0;
+    while (b < e) {
+      const uint32_t word = __ldg(flagw + (b >> 5));
+      const uint32_t sh = (uint32_t)(b & 31);
+      const uint64_t take = min((uint64_t)(32 - sh), e - b);
+      const uint32_t m = take == 32 ? 0xffffffffu : ((1u << take) - 1u);
+      nflag += __popc((word >> sh) & m);
+      b += take;
+    }
+    cnt[t] = (uint32_t)C - nflag;
+  }
+}
+
+__global__ void validate_kernel(const uint32_t* idxw, int64_t n, int w, int64_t limit,
+                                uint32_t* err) {
+  bool bad = false;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    bad |= (int64_t)read_bits(idxw, (uint64_t)i * w, w) >= limit;
+  if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(err, HQMQ_DEVERR_INDEX_RANGE);
+}
+
+namespace {
+int check() { return check_launch(); }
+int grid_for(int64_t n, int threads) {
+  return (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, threads), 148 * 16));
+}
+
+bool fill(const hqmq_decode_args* a, DecParams& p, bool need_range) {
+  if (!a || a->batch < 1 || a->heads < 1 || a->tokens < 0 || a->head_dim < 1) return false;
+  if (a->codebook_size < 1 || a->radius_bits < 1 || a->radius_bits > 8 || a->index_bits < 1 ||
+      a->index_bits > 32)
+    return false;
+  if (need_range && !(0 <= a->token_start && a->token_start <= a->token_stop &&
+                      a->token_stop <= a->tokens))
+    return false;
+  p.B = a->batch; p.H = a->heads; p.T = a->tokens; p.D = a->head_dim;
+  p.C = (int)ceil_div(a->head_dim, 4);
+  p.S = a->codebook_size; p.br = a->radius_bits; p.w = a->index_bits;
+  p.t0 = a->token_start; p.nt = a->token_stop - a->token_start;
+  p.scales = a->scales; p.idxw = a->index_words; p.radw = a->radius_words;
+  p.flagw = a->flag_words; p.payloads = a->payloads; p.tokoff = a->token_offsets;
+  p.out = a->out; p.err = a->error_word;
+  return true;
+}
+
+template <typename OutT>
+int launch_decode(DecParams& p, const hqmq_decode_args* a, cudaStream_t st) {
+  const int64_t rows = p.B * p.H;
+  const size_t smem = (size_t)kGroupOrder * p.S * sizeof(float4);
+  const bool use_smem = smem <= kDecSmemLimit;
+  p.table = a->joint_f32;
+  p.aligned4 = (p.D % 4 == 0) && (reinterpret_cast<uintptr_t>(a->out) % (4 * sizeof(OutT)) == 0);
+  const int64_t nck = p.nt * p.C;
+  const int64_t want = std::max<int64_t>(1, (148 * 4 + rows - 1) / rows);
+  const int64_t bx = std::max<int64_t>(1, std::min<int64_t>(want, ceil_div(nck, kDecThreads * kDecR)));
+  const dim3 grid((unsigned)bx, (unsigned)rows);
+  if (use_smem) {
+    static thread_local bool set = false;
+    if (!set) {
+      cudaFuncSetAttribute(decode_kernel<OutT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)kDecSmemLimit);
+      set = true;
+    }
+    decode_kernel<OutT, true><<<grid, kDecThreads, smem, st>>>(p);
+  } else {
+    decode_kernel<OutT, false><<<grid, kDecThreads, 0, st>>>(p);
+  }
+  return check();
+}
+}  // namespace
+}  // namespace hqmq
+
+extern "C" {
+
+int hqmq_decode(const hqmq_decode_args* a, void* stream) {
+  using namespace hqmq;
+  DecParams p;
+  if (!fill(a, p, true)) return HQMQ_ERR_INVALID_ARGUMENT;
+  if (p.B * p.H >= 65536) return HQMQ_ERR_UNSUPPORTED;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (p.nt == 0) return HQMQ_OK;
+  switch (a->out_dtype) {
+    case HQMQ_F32: return launch_decode<float>(p, a, st);
+    case HQMQ_F16: return launch_decode<__half>(p, a, st);
+    case HQMQ_BF16: return launch_decode<__nv_bfloat16>(p, a, st);
+    case HQMQ_F64: {
+      p.table = a->joint_f64;
+      const int64_t rows = p.B * p.H;
+      const int64_t bx = std::max<int64_t>(1, std::min<int64_t>(64, ceil_div(p.nt * p.C, kDecThreads)));
+      decode_f64_kernel<<<dim3((unsigned)bx, (unsigned)rows), kDecThreads, 0, st>>>(p);
+      return check();
+    }
+    default: return HQMQ_ERR_INVALID_ARGUMENT;
+  }
+}
+
+int hqmq_unpack(const hqmq_decode_args* a, int32_t* indices, uint8_t* quanta, uint8_t* flags,
+                void* stream) {
+  using namespace hqmq;
+  DecParams p;
+  if (!fill(a, p, false)) return HQMQ_ERR_INVALID_ARGUMENT;
+  const int64_t n = p.B * p.H * p.T * p.C;
+  if (n == 0) return HQMQ_OK;
+  unpack_kernel<<<grid_for(n, 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      p, indices, quanta, flags);
+  return check();
+}
+
+size_t hqmq_pack_workspace_bytes(int64_t n_chunks) {
+  size_t cub_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                (int)std::max<int64_t>(n_chunks, 1));
+  return ((size_t)std::max<int64_t>(n_chunks, 1) * 4 * 2 + 255) / 256 * 256 + cub_bytes;
+}
+
+int hqmq_pack(int64_t n, int32_t C, int32_t w, int32_t br, const int32_t* indices,
+              const uint8_t* quanta, const uint8_t* flags, uint32_t* idxw, uint32_t* radw,
+              uint32_t* flagw, uint32_t* tokoff, void* workspace, size_t workspace_bytes,
+              void* stream) {
+  using namespace hqmq;
+  if (n < 0 || C < 1 || w < 1 || w > 32 || br < 1 || br > 8) return HQMQ_ERR_INVALID_ARGUMENT;
+  if (n >= (1LL << 32)) return HQMQ_ERR_UNSUPPORTED;
+  if (workspace_bytes < hqmq_pack_workspace_bytes(n)) return HQMQ_ERR_WORKSPACE;
+  if (n == 0) return HQMQ_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  char* ws = reinterpret_cast<char*>(workspace);
+  uint32_t* mark = reinterpret_cast<uint32_t*>(ws);
+  uint32_t* pos = mark + n;
+  char* tmp = ws + ((size_t)n * 8 + 255) / 256 * 256;
+  size_t tmp_bytes = workspace_bytes - (size_t)(tmp - ws);
+  coded_mark_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, flags, mark);
+  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, mark, pos, (int)n, st);
+  pack_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, C, w, br, indices, quanta, flags, pos, idxw,
+                                                  radw, flags ? flagw : nullptr,
+                                                  flags ? tokoff : nullptr);
+  return check();
+}
+
+size_t hqmq_token_offsets_workspace_bytes(int64_t n_tokens) {
+  size_t cub_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
+                                (int)std::max<int64_t>(n_tokens, 1));
+  return ((size_t)std::max<int64_t>(n_tokens, 1) * 4 + 255) / 256 * 256 + cub_bytes;
+}
+
+int hqmq_token_offsets(int64_t n_tokens, int32_t C, const uint32_t* flagw, uint32_t* tokoff,
+                       void* workspace, size_t workspace_bytes, void* stream) {
+  using namespace hqmq;
+  if (n_tokens < 0 || C < 1) return HQMQ_ERR_INVALID_ARGUMENT;
+  if (workspace_bytes < hqmq_token_offsets_workspace_bytes(n_tokens)) return HQMQ_ERR_WORKSPACE;
+  if (n_tokens == 0) return HQMQ_OK;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  char* ws = reinterpret_cast<char*>(workspace);
+  uint32_t* cnt = reinterpret_cast<uint32_t*>(ws);
+  char* tmp = ws + ((size_t)n_tokens * 4 + 255) / 256 * 256;
+  size_t tmp_bytes = workspace_bytes - (size_t)(tmp - ws);
+  token_coded_kernel<<<grid_for(n_tokens, 256), 256, 0, st>>>(n_tokens, C, flagw, cnt);
+  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, tokoff, (int)n_tokens, st);
+  return check();
+}
+
+int hqmq_validate_indices(const uint32_t* idxw, int64_t n, int32_t w, int64_t limit,
+                          uint32_t* err, void* stream) {
+  using namespace hqmq;
+  if (n < 0 || w < 1 || w > 32) return HQMQ_ERR_INVALID_ARGUMENT;
+  if (n == 0) return HQMQ_OK;
+  validate_kernel<<<grid_for(n, 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      idxw, n, w, limit, err);
+  return check();
+}
+
+}  // extern "C"

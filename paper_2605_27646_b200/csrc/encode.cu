@@ -1,0 +1,786 @@
+// HQMQ encode for sm_100a: Med3x exact median + fused norm / scale / radius /
+// closed-form 2T x S search / exact fp64 fixup / bit-pack kernel.
+//
+// Reference path replaced: codec.encode_tensor (codec.py:232-287) with
+// outliers.lower_median (outliers.py:50-55), radius.quantize_radii
+// (radius.py:35-47), _kernels.nearest_scan (_kernels.pyx:16-46) and the kvpack
+// section streams (kvpack.py:66-76,134-146).
+//
+// Kernel pipeline for one (layer, role) call, all stream-ordered, no host sync:
+//   [extraction on]  norms_hist (pass 0)  -> radix_hist x4 (exact rank-(n-1)//2
+//                    select on the fp64 bit patterns; last block selects)
+//                    -> tile_count -> cub exclusive scan -> finalize_counts
+//   encode_tile: one CTA per tile of <=1024 chunks of one (batch, head) row.
+//     1. exact fp64 norms, outlier flags (ballot), per-token sigma -> fp16 scale
+//     2. fp32 search: for every secondary s (rotation table staged in smem),
+//        v = u (x) conj(q_s) with 8 FFMA2; coset score = max(max|v_i|, sum|v_i|/2)
+//        (closed form over the 24 elements of 2T); running top-2 per chunk
+//     3. certification: gap between best and runner-up (other cosets and the
+//        within-coset runner-up) > kDelta proves the fp64 reference picks the
+//        same (p, s); otherwise a warp re-scores all candidate cosets with the
+//        reference's exact fp64 arithmetic and lowest-flat-index tie-break
+//     4. pack indices / radius quanta / flag bits into the section streams
+//        (smem staging, plain stores for owned words, atomicOr on shared edge
+//        words), token offsets, fp16 payload rows.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cfloat>
+#include <cmath>
+#include <cstdio>
+#include <type_traits>
+
+#include "common.cuh"
+
+namespace hqmq {
+
+constexpr int kEncThreads = 256;
+constexpr int kEncR = 4;
+constexpr int kTileChunks = kEncThreads * kEncR;  // 1024 chunks per CTA
+constexpr int kSBlock = 512;                      // secondaries per smem stage
+// Certification margin: 2x the worst-case |fp32 - fp64| score error (~1e-6 for
+// unit directions, SURVEY.md §7 hard part 1) with a further 3x safety factor.
+constexpr float kDelta = 6e-6f;
+
+constexpr int kDigitBits = 13;
+constexpr int kBins = 1 << kDigitBits;  // 8192
+constexpr int kPasses = 5;              // lo bits: 50, 37, 24, 11, 0
+__host__ __device__ constexpr int digit_lo(int pass) { return pass < 4 ? 50 - 13 * pass : 0; }
+__host__ __device__ constexpr int digit_width(int pass) { return pass < 4 ? 13 : 11; }
+constexpr int kHistThreads = 256;
+constexpr int kHistChunksPerBlock = 8192;
+
+struct RadixGroup {
+  unsigned long long prefix;
+  unsigned long long rank;
+  double threshold;
+  unsigned long long n;
+};
+
+struct EncParams {
+  int64_t B, H, T, D;
+  int C, S, br, w;
+  int TT;
+  int64_t tiles_per_row;
+  int aligned4;
+  int per_head;
+  const void* data;
+  const float4* rot;    // [H][S][4] float4 (16 floats per secondary)
+  const double* joint;  // [H][24S][4]
+  const RadixGroup* groups;  // null when extraction is disabled
+  const uint32_t* tile_prefix;
+  uint16_t* scales;
+  uint32_t* idxw;
+  uint32_t* radw;
+  uint32_t* flagw;
+  uint16_t* payloads;
+  int64_t payload_capacity;
+  uint32_t* tokoff;
+  int64_t* counters;
+  uint32_t* err;
+};
+
+// ------------------------------------------------------------ fp32 search
+struct Dir2 {
+  float2 a, b, c, d;  // (u0,u0) (u1,u1) (u2,u2) (u3,u3)
+};
+
+__device__ __forceinline__ void rotate(const Dir2& u, float4 t0, float4 t1, float4 t2, float4 t3,
+                                       float2& wx, float2& yz) {
+  wx = __fmul2_rn(u.d, make_float2(t1.z, t1.w));
+  wx = __ffma2_rn(u.c, make_float2(t1.x, t1.y), wx);
+  wx = __ffma2_rn(u.b, make_float2(t0.z, t0.w), wx);
+  wx = __ffma2_rn(u.a, make_float2(t0.x, t0.y), wx);
+  yz = __fmul2_rn(u.d, make_float2(t3.z, t3.w));
+  yz = __ffma2_rn(u.c, make_float2(t3.x, t3.y), yz);
+  yz = __ffma2_rn(u.b, make_float2(t2.z, t2.w), yz);
+  yz = __ffma2_rn(u.a, make_float2(t2.x, t2.y), yz);
+}
+
+// Best score over the 24 elements of one coset: max(max_i |v_i|, sum_i |v_i| / 2).
+__device__ __forceinline__ float coset_score(float2 wx, float2 yz) {
+  const float aw = fabsf(wx.x), ax = fabsf(wx.y), ay = fabsf(yz.x), az = fabsf(yz.y);
+  const float half = ((aw + ax) + (ay + az)) * 0.5f;
+  return fmaxf(fmaxf(fmaxf(aw, ax), fmaxf(ay, az)), half);
+}
+
+// fp32 direction for the fast path.  The exact fp64 norm r is known.
+template <typename InT>
+__device__ __forceinline__ Dir2 fast_dir(const InT (&v)[4], const double (&x)[4], double r) {
+  float u[4];
+  bool slow = sizeof(InT) == 8;
+  if (!slow) {
+    const float x0 = In<InT>::f(v[0]), x1 = In<InT>::f(v[1]);
+    const float x2 = In<InT>::f(v[2]), x3 = In<InT>::f(v[3]);
+    const float ss = fmaf(x3, x3, fmaf(x2, x2, fmaf(x1, x1, x0 * x0)));
+    if (ss >= 1e-30f && ss <= 1e30f) {
+      const float inv = rsqrtf(ss);
+      u[0] = x0 * inv; u[1] = x1 * inv; u[2] = x2 * inv; u[3] = x3 * inv;
+    } else {
+      slow = true;
+    }
+  }
+  if (slow) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) u[i] = (float)__ddiv_rn(x[i], r);
+  }
+  Dir2 d;
+  d.a = make_float2(u[0], u[0]);
+  d.b = make_float2(u[1], u[1]);
+  d.c = make_float2(u[2], u[2]);
+  d.d = make_float2(u[3], u[3]);
+  return d;
+}
+
+// Closed-form primary index of the best element of a coset and the runner-up
+// score inside that coset (hurwitz.py:10-14,28-36 canonical order).
+__device__ __forceinline__ void coset_resolve(float2 wx, float2 yz, int& p, float& top,
+                                              float& within) {
+  const float v[4] = {wx.x, wx.y, yz.x, yz.y};
+  float a[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) a[i] = fabsf(v[i]);
+  int imax = 0;
+  float a1 = a[0];
+#pragma unroll
+  for (int i = 1; i < 4; ++i)
+    if (a[i] > a1) { a1 = a[i]; imax = i; }
+  float a2 = -1.f, a4 = a[0];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (i != imax) a2 = fmaxf(a2, a[i]);
+    a4 = fminf(a4, a[i]);
+  }
+  const float half = ((a[0] + a[1]) + (a[2] + a[3])) * 0.5f;
+  if (a1 > half) {
+    p = 2 * imax + (v[imax] < 0.f ? 1 : 0);
+    top = a1;
+    within = fmaxf(half, a2);
+  } else {
+    p = 8 + ((v[0] < 0.f) << 3) + ((v[1] < 0.f) << 2) + ((v[2] < 0.f) << 1) + (v[3] < 0.f);
+    top = half;
+    within = fmaxf(a1, half - a4);
+  }
+}
+
+// Exact re-scoring of one uncertain chunk by a whole warp.  Candidates: every
+// (p, s) whose coset's fp32 score is within kDelta of the best fp32 coset
+// score; each is scored with the reference's fp64 arithmetic and the lowest
+// flat index p*S+s wins ties (_kernels.pyx:27-45).
+__device__ int warp_exact_index(const double (&x)[4], double r, const Dir2& u32,
+                                const float4* __restrict__ rot, const double* __restrict__ joint,
+                                int S, int lane) {
+  double u[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) u[i] = __ddiv_rn(x[i], r);
+  float best = -1.f;
+  for (int s = lane; s < S; s += kWarp) {
+    float2 wx, yz;
+    rotate(u32, __ldg(rot + 4 * s), __ldg(rot + 4 * s + 1), __ldg(rot + 4 * s + 2),
+           __ldg(rot + 4 * s + 3), wx, yz);
+    best = fmaxf(best, coset_score(wx, yz));
+  }
+  best = warp_max(best);
+  const float cut = best - kDelta;
+  double lbest = -2.0;
+  long long lj = 0x7fffffffffffffffLL;
+  for (int s = lane; s < S; s += kWarp) {
+    float2 wx, yz;
+    rotate(u32, __ldg(rot + 4 * s), __ldg(rot + 4 * s + 1), __ldg(rot + 4 * s + 2),
+           __ldg(rot + 4 * s + 3), wx, yz);
+    if (coset_score(wx, yz) >= cut) {
+      for (int pp = 0; pp < kGroupOrder; ++pp) {
+        const long long j = (long long)pp * S + s;
+        const double sc = exact_dot(u, joint + 4 * j);
+        if (sc > lbest || (sc == lbest && j < lj)) {
+          lbest = sc;
+          lj = j;
+        }
+      }
+    }
+  }
+  warp_argmax_lowest(lbest, lj);
+  return (int)lj;
+}
+
+// ------------------------------------------------------------- bit staging
+__device__ __forceinline__ void stage_bits(uint32_t* stage, uint64_t bit, uint32_t v, int width) {
+  const uint32_t wi = (uint32_t)(bit >> 5), sh = (uint32_t)(bit & 31);
+  atomicOr(stage + wi, v << sh);
+  if (sh + width > 32) atomicOr(stage + wi + 1, v >> (32 - sh));
+}
+
+// Flush staged words [0, nwords) that cover global bits [gbit0, gbit0+nbits):
+// words fully owned by this tile are stored, shared edge words are OR-ed.
+__device__ __forceinline__ void flush_bits(const uint32_t* stage, uint32_t* dst, uint64_t gbit0,
+                                           uint64_t nbits, bool skip_zero_owned) {
+  if (nbits == 0) return;
+  const uint64_t gw0 = gbit0 >> 5;
+  const uint32_t lb0 = (uint32_t)(gbit0 & 31);
+  const uint64_t end = lb0 + nbits;
+  const uint32_t nw = (uint32_t)((end + 31) >> 5);
+  for (uint32_t i = threadIdx.x; i < nw; i += blockDim.x) {
+    const uint32_t word = stage[i];
+    const bool owned = (i > 0 || lb0 == 0) && (i + 1 < nw || (end & 31) == 0);
+    if (owned) {
+      if (!(skip_zero_owned && word == 0)) dst[gw0 + i] = word;
+    } else if (word) {
+      atomicOr(dst + gw0 + i, word);
+    }
+  }
+}
+
+// ----------------------------------------------------------- encode kernel
+template <typename InT>
+__global__ void __launch_bounds__(kEncThreads, 2) encode_tile_kernel(EncParams p) {
+  extern __shared__ float4 tab_s[];  // [min(S, kSBlock)][4]
+  __shared__ double r_s[kTileChunks];
+  __shared__ double sig_s[kTileChunks];
+  __shared__ uint32_t flag_s[kTileChunks / 32];
+  __shared__ uint32_t wpre_s[kTileChunks / 32 + 1];
+  __shared__ uint32_t stage_i[kTileChunks + 2];
+  __shared__ uint32_t stage_r[kTileChunks / 4 + 2];
+  __shared__ uint32_t stage_f[kTileChunks / 32 + 2];
+  __shared__ int32_t idx_s[kTileChunks];
+  __shared__ uint16_t fix_s[kTileChunks];
+  __shared__ int fix_n;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t row = blockIdx.y;
+  const int64_t tile = blockIdx.x;
+  const int h = (int)(row % p.H);
+  const int C = p.C, S = p.S;
+  const int64_t t0 = tile * p.TT;
+  const int ntok = (int)min((int64_t)p.TT, p.T - t0);
+  const int nck = ntok * C;
+  const int64_t cb = (row * p.T + t0) * C;
+  const InT* __restrict__ data = reinterpret_cast<const InT*>(p.data);
+  const float4* __restrict__ rot = p.rot + (int64_t)h * S * 4;
+  const double* __restrict__ joint = p.joint + (int64_t)h * kGroupOrder * S * 4;
+  const double top = (double)((1 << p.br) - 1);
+
+  // Stage the first block of the rotation table while the prologue runs.
+  const int sb0 = min(S, kSBlock);
+  for (int i = tid; i < sb0 * 4; i += kEncThreads) tab_s[i] = __ldg(rot + i);
+  for (int i = tid; i < kTileChunks + 2; i += kEncThreads) stage_i[i] = 0u;
+  for (int i = tid; i < kTileChunks / 4 + 2; i += kEncThreads) stage_r[i] = 0u;
+  for (int i = tid; i < kTileChunks / 32 + 2; i += kEncThreads) stage_f[i] = 0u;
+  if (tid == 0) fix_n = 0;
+
+  const double thr = p.groups ? p.groups[p.per_head ? h : 0].threshold : INFINITY;
+
+  // ---- 1. exact prologue: norms, flags, fp32 directions
+  Dir2 u[kEncR];
+  bool live[kEncR];
+#pragma unroll
+  for (int j = 0; j < kEncR; ++j) {
+    const int k = j * kEncThreads + tid;
+    bool fl = false;
+    live[j] = false;
+    u[j].a = u[j].b = u[j].c = u[j].d = make_float2(0.f, 0.f);
+    if (k < nck) {
+      const int tt = k / C, c = k - tt * C;
+      InT v[4];
+      load_chunk(data + (row * p.T + t0 + tt) * p.D, c, (int)p.D, p.aligned4 != 0, v);
+      double x[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) x[i] = In<InT>::d(v[i]);
+      const double r = exact_norm(x);
+      r_s[k] = r;
+      fl = r > thr;
+      live[j] = !fl && r > 0.0;
+      if (live[j]) u[j] = fast_dir(v, x, r);
+    }
+    const uint32_t ball = __ballot_sync(0xffffffffu, fl);
+    if (lane == 0) flag_s[j * (kEncThreads / 32) + warp] = ball;
+  }
+  __syncthreads();
+
+  // ---- per-token sigma (codec.py:257-261) and fp16 scale
+  for (int tt = tid; tt < ntok; tt += kEncThreads) {
+    double sg = 0.0;
+    for (int c = 0; c < C; ++c) {
+      const int k = tt * C + c;
+      const bool fl = (flag_s[k >> 5] >> (k & 31)) & 1u;
+      const double kept = fl ? 0.0 : r_s[k];
+      sg = kept > sg ? kept : sg;
+    }
+    if (!(sg > 0.0)) sg = 1.0;
+    const __half hs = __double2half(sg);
+    p.scales[row * p.T + t0 + tt] = __half_as_ushort(hs);
+    const double sw = (double)__half2float(hs);
+    if (!(sw > 0.0)) atomicOr(p.err, HQMQ_DEVERR_SIGMA_NONPOSITIVE);
+    sig_s[tt] = sw;
+  }
+  // coded-chunk prefix inside the tile (one warp; <= 32 flag words)
+  const int nwords = (nck + 31) >> 5;
+  if (warp == 0) {
+    uint32_t cnt = 0;
+    if (lane < nwords) {
+      const int valid = min(32, nck - lane * 32);
+      const uint32_t vmask = valid == 32 ? 0xffffffffu : ((1u << valid) - 1u);
+      cnt = __popc(~flag_s[lane] & vmask);
+    }
+    uint32_t inc = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += y;
+    }
+    wpre_s[lane] = inc - cnt;
+    if (lane == 31) wpre_s[32] = inc;
+  }
+  __syncthreads();
+  const uint64_t P0 = p.tile_prefix ? (uint64_t)p.tile_prefix[row * p.tiles_per_row + tile]
+                                    : (uint64_t)cb;
+  const uint32_t ncoded = wpre_s[nwords];
+  auto coded_before = [&](int k) -> uint32_t {
+    return wpre_s[k >> 5] + __popc(~flag_s[k >> 5] & ((1u << (k & 31)) - 1u));
+  };
+  if (p.tokoff) {
+    for (int tt = tid; tt < ntok; tt += kEncThreads)
+      p.tokoff[row * p.T + t0 + tt] = (uint32_t)(P0 + coded_before(tt * C));
+  }
+
+  // ---- 2. fp32 closed-form search over the S cosets
+  float best[kEncR], second[kEncR];
+  int bs[kEncR];
+#pragma unroll
+  for (int j = 0; j < kEncR; ++j) {
+    best[j] = -1.f;
+    second[j] = -1.f;
+    bs[j] = 0;
+  }
+  for (int sb = 0; sb < S; sb += kSBlock) {
+    const int ns = min(kSBlock, S - sb);
+    if (sb > 0) {
+      __syncthreads();
+      for (int i = tid; i < ns * 4; i += kEncThreads) tab_s[i] = __ldg(rot + 4 * sb + i);
+      __syncthreads();
+    }
+#pragma unroll 2
+    for (int s = 0; s < ns; ++s) {
+      const float4 t0v = tab_s[4 * s + 0], t1v = tab_s[4 * s + 1];
+      const float4 t2v = tab_s[4 * s + 2], t3v = tab_s[4 * s + 3];
+      const int sg = sb + s;
+#pragma unroll
+      for (int j = 0; j < kEncR; ++j) {
+        float2 wx, yz;
+        rotate(u[j], t0v, t1v, t2v, t3v, wx, yz);
+        const float sc = coset_score(wx, yz);
+        const bool gt = sc > best[j];
+        second[j] = fmaxf(second[j], fminf(sc, best[j]));
+        best[j] = fmaxf(best[j], sc);
+        bs[j] = gt ? sg : bs[j];
+      }
+    }
+  }
+
+  // ---- 3. certification (closed-form primary index + within-coset runner-up)
+#pragma unroll
+  for (int j = 0; j < kEncR; ++j) {
+    const int k = j * kEncThreads + tid;
+    if (k >= nck) continue;
+    int idx = 0;
+    if (live[j]) {
+      const int s = bs[j];
+      float2 wx, yz;
+      rotate(u[j], __ldg(rot + 4 * s), __ldg(rot + 4 * s + 1), __ldg(rot + 4 * s + 2),
+             __ldg(rot + 4 * s + 3), wx, yz);
+      int pidx;
+      float top32, within;
+      coset_resolve(wx, yz, pidx, top32, within);
+      idx = pidx * S + s;
+      const float runner = fmaxf(second[j], within);
+      if (!(best[j] - runner > kDelta)) {
+        const int e = atomicAdd(&fix_n, 1);
+        fix_s[e] = (uint16_t)k;
+      }
+    }
+    idx_s[k] = idx;
+  }
+  __syncthreads();
+
+  // ---- exact fixup of uncertified chunks, one warp per chunk
+  const int nfix = fix_n;
+  for (int e = warp; e < nfix; e += kEncThreads / 32) {
+    const int k = fix_s[e];
+    const int tt = k / C, c = k - tt * C;
+    InT v[4];
+    load_chunk(data + (row * p.T + t0 + tt) * p.D, c, (int)p.D, p.aligned4 != 0, v);
+    double x[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) x[i] = In<InT>::d(v[i]);
+    const double r = r_s[k];
+    const Dir2 ud = fast_dir(v, x, r);
+    const int idx = warp_exact_index(x, r, ud, rot, joint, S, lane);
+    if (lane == 0) idx_s[k] = idx;
+  }
+  if (tid == 0 && nfix) atomicAdd(reinterpret_cast<unsigned long long*>(p.counters + 2),
+                                  (unsigned long long)nfix);
+  __syncthreads();
+
+  // ---- 4. pack sections
+  const int w = p.w, br = p.br;
+  const uint32_t lbi = (uint32_t)((P0 * (uint64_t)w) & 31);
+  const uint32_t lbr = (uint32_t)((P0 * (uint64_t)br) & 31);
+  const uint32_t lbf = (uint32_t)(cb & 31);
+#pragma unroll
+  for (int j = 0; j < kEncR; ++j) {
+    const int k = j * kEncThreads + tid;
+    if (k >= nck) continue;
+    const bool fl = (flag_s[k >> 5] >> (k & 31)) & 1u;
+    const uint32_t before = coded_before(k);
+    if (!fl) {
+      stage_bits(stage_i, (uint64_t)lbi + (uint64_t)before * w, (uint32_t)idx_s[k], w);
+      const uint32_t q = exact_quantum(r_s[k], sig_s[k / C], top);
+      stage_bits(stage_r, (uint64_t)lbr + (uint64_t)before * br, q, br);
+    } else {
+      const uint32_t b = lbf + (uint32_t)k;
+      atomicOr(stage_f + (b >> 5), 1u << (b & 31));
+      const uint64_t prow = (uint64_t)(cb + k) - (P0 + before);
+      if (prow < (uint64_t)p.payload_capacity) {
+        const int tt = k / C, c = k - tt * C;
+        InT v[4];
+        load_chunk(data + (row * p.T + t0 + tt) * p.D, c, (int)p.D, p.aligned4 != 0, v);
+        ushort4 hv;
+        hv.x = __half_as_ushort(__double2half(In<InT>::d(v[0])));
+        hv.y = __half_as_ushort(__double2half(In<InT>::d(v[1])));
+        hv.z = __half_as_ushort(__double2half(In<InT>::d(v[2])));
+        hv.w = __half_as_ushort(__double2half(In<InT>::d(v[3])));
+        reinterpret_cast<ushort4*>(p.payloads)[prow] = hv;
+      }
+    }
+  }
+  __syncthreads();
+  flush_bits(stage_i, p.idxw, P0 * (uint64_t)w, (uint64_t)ncoded * w, false);
+  flush_bits(stage_r, p.radw, P0 * (uint64_t)br, (uint64_t)ncoded * br, false);
+  if (p.flagw) flush_bits(stage_f, p.flagw, (uint64_t)cb, (uint64_t)nck, true);
+}
+
+// ------------------------------------------------------ Med3x radix select
+struct RadixParams {
+  int64_t B, H, T, D;
+  int C;
+  int per_head;
+  int aligned4;
+  int pass;
+  double multiplier;
+  const void* data;
+  double* norms;
+  RadixGroup* groups;
+  uint32_t* hist;  // [G][kBins]
+  unsigned int* done;
+  int G;
+};
+
+__device__ __forceinline__ void hist_add(uint32_t* hs, uint32_t bin, bool active) {
+  const unsigned m = __match_any_sync(0xffffffffu, active ? bin : 0xffffffffu);
+  const int leader = __ffs(m) - 1;
+  if (active && (int)(threadIdx.x & 31) == leader) atomicAdd(hs + bin, (uint32_t)__popc(m));
+}
+
+// Last block: pick, for every group, the bin holding rank k; narrow the prefix.
+__device__ void radix_select_last(RadixParams& p) {
+  __shared__ uint32_t part[kHistThreads];
+  const int lo = digit_lo(p.pass), width = digit_width(p.pass);
+  const int nb = 1 << width;
+  const int per = nb / kHistThreads;
+  for (int g = 0; g < p.G; ++g) {
+    uint32_t* hg = p.hist + (int64_t)g * kBins;
+    uint32_t sum = 0;
+    for (int i = 0; i < per; ++i) sum += __ldcg(hg + threadIdx.x * per + i);
+    part[threadIdx.x] = sum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned long long k = p.groups[g].rank;
+      unsigned long long acc = 0;
+      int t = 0;
+      for (; t < kHistThreads; ++t) {
+        if (acc + part[t] > k) break;
+        acc += part[t];
+      }
+      int bin = t * per;
+      for (;; ++bin) {
+        const uint32_t c = __ldcg(hg + bin);
+        if (acc + c > k) break;
+        acc += c;
+      }
+      p.groups[g].prefix |= ((unsigned long long)bin) << lo;
+      p.groups[g].rank = k - acc;
+      if (p.pass == kPasses - 1) {
+        const double med = __longlong_as_double((long long)p.groups[g].prefix);
+        p.groups[g].threshold = __dmul_rn(p.multiplier, med);
+      }
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < kBins; i += kHistThreads) hg[i] = 0u;
+    __syncthreads();
+  }
+  (void)width;
+  if (threadIdx.x == 0) *p.done = 0u;
+}
+
+template <typename InT>
+__global__ void __launch_bounds__(kHistThreads) radix_hist_kernel(RadixParams p) {
+  __shared__ uint32_t hs[kBins];
+  __shared__ bool is_last;
+  for (int i = threadIdx.x; i < kBins; i += kHistThreads) hs[i] = 0u;
+  __syncthreads();
+  const int64_t row = blockIdx.y;
+  const int g = p.per_head ? (int)(row % p.H) : 0;
+  const int64_t L = p.T * p.C;
+  const int64_t base = (int64_t)blockIdx.x * kHistChunksPerBlock;
+  const int64_t end = min(L, base + kHistChunksPerBlock);
+  const int lo = digit_lo(p.pass), width = digit_width(p.pass);
+  const uint32_t dmask = (1u << width) - 1u;
+  const int hi_shift = lo + width;
+  const unsigned long long pref = p.groups[g].prefix;
+  const InT* __restrict__ data = reinterpret_cast<const InT*>(p.data);
+  for (int64_t i0 = base; i0 < end; i0 += kHistThreads) {
+    const int64_t i = i0 + threadIdx.x;
+    bool active = i < end;
+    uint32_t bin = 0;
+    if (active) {
+      double r;
+      if (p.pass == 0) {
+        const int64_t t = i / p.C;
+        const int c = (int)(i - t * p.C);
+        InT v[4];
+        load_chunk(data + (row * p.T + t) * p.D, c, (int)p.D, p.aligned4 != 0, v);
+        double x[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) x[k] = In<InT>::d(v[k]);
+        r = exact_norm(x);
+        p.norms[row * L + i] = r;
+      } else {
+        r = p.norms[row * L + i];
+      }
+      const unsigned long long key = (unsigned long long)__double_as_longlong(r);
+      if (hi_shift < 64) active = (key >> hi_shift) == (pref >> hi_shift);
+      bin = (uint32_t)(key >> lo) & dmask;
+    }
+    hist_add(hs, bin, active);
+  }
+  __syncthreads();
+  uint32_t* hg = p.hist + (int64_t)g * kBins;
+  for (int i = threadIdx.x; i < kBins; i += kHistThreads)
+    if (hs[i]) atomicAdd(hg + i, hs[i]);
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned int total = gridDim.x * gridDim.y;
+    is_last = atomicAdd(p.done, 1u) == total - 1;
+  }
+  __syncthreads();
+  if (is_last) {
+    __threadfence();
+    radix_select_last(p);
+  }
+}
+
+__global__ void radix_init_kernel(RadixGroup* groups, int G, unsigned long long n_per_group) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g < G) {
+    groups[g].prefix = 0ull;
+    groups[g].rank = (n_per_group - 1) / 2;
+    groups[g].threshold = 0.0;
+    groups[g].n = n_per_group;
+  }
+}
+
+// Coded (unflagged) chunk count of every encode tile.
+__global__ void tile_count_kernel(const double* __restrict__ norms, const RadixGroup* groups,
+                                  int64_t H, int64_t T, int C, int TT, int64_t tiles_per_row,
+                                  int per_head, uint32_t* counts) {
+  const int64_t row = blockIdx.y;
+  const int64_t tile = blockIdx.x;
+  const double thr = groups[per_head ? (int)(row % H) : 0].threshold;
+  const int64_t t0 = tile * TT;
+  const int ntok = (int)min((int64_t)TT, T - t0);
+  const int nck = ntok * C;
+  const double* nr = norms + (row * T + t0) * C;
+  uint32_t cnt = 0;
+  for (int k = threadIdx.x; k < nck; k += blockDim.x) cnt += nr[k] > thr ? 0u : 1u;
+  typedef cub::BlockReduce<uint32_t, 256> BR;
+  __shared__ typename BR::TempStorage tmp;
+  const uint32_t total = BR(tmp).Sum(cnt);
+  if (threadIdx.x == 0) counts[row * tiles_per_row + tile] = total;
+}
+
+__global__ void finalize_counts_kernel(const uint32_t* counts, const uint32_t* prefix,
+                                       int64_t n_tiles, int64_t n_chunks, int64_t* counters) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    const int64_t coded = n_tiles ? (int64_t)prefix[n_tiles - 1] + counts[n_tiles - 1] : 0;
+    counters[0] = coded;
+    counters[1] = n_chunks - coded;
+  }
+}
+
+__global__ void set_counts_kernel(int64_t n_chunks, int64_t* counters) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    counters[0] = n_chunks;
+    counters[1] = 0;
+  }
+}
+
+// ----------------------------------------------------------------- host
+namespace {
+
+struct Layout {
+  int64_t n_chunks = 0, rows = 0, n_tiles = 0, tiles_per_row = 0;
+  int C = 0, TT = 0, G = 0;
+  size_t off_norms = 0, off_groups = 0, off_hist = 0, off_done = 0, off_counts = 0,
+         off_prefix = 0, off_cub = 0, cub_bytes = 0, total = 0;
+};
+
+size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+bool plan(const hqmq_encode_args* a, Layout& L) {
+  if (!a || a->batch < 1 || a->heads < 1 || a->tokens < 0 || a->head_dim < 1) return false;
+  L.C = (int)ceil_div(a->head_dim, 4);
+  if (L.C > kTileChunks) return false;
+  L.TT = kTileChunks / L.C;
+  L.rows = a->batch * a->heads;
+  L.n_chunks = L.rows * a->tokens * L.C;
+  L.tiles_per_row = ceil_div(a->tokens, L.TT);
+  L.n_tiles = L.rows * L.tiles_per_row;
+  L.G = a->per_head_pooling ? (int)a->heads : 1;
+  size_t off = 0;
+  const bool ext = a->outlier_multiplier > 0.0;
+  if (ext) {
+    L.off_norms = off;
+    off = align_up(off + (size_t)L.n_chunks * 8, 256);
+    L.off_groups = off;
+    off = align_up(off + (size_t)L.G * sizeof(RadixGroup), 256);
+    L.off_hist = off;
+    off = align_up(off + (size_t)L.G * kBins * 4, 256);
+    L.off_done = off;
+    off = align_up(off + 16, 256);
+    L.off_counts = off;
+    off = align_up(off + (size_t)L.n_tiles * 4, 256);
+    L.off_prefix = off;
+    off = align_up(off + (size_t)L.n_tiles * 4, 256);
+    size_t cub_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, (const uint32_t*)nullptr,
+                                  (uint32_t*)nullptr, (int)std::max<int64_t>(L.n_tiles, 1));
+    L.off_cub = off;
+    L.cub_bytes = cub_bytes;
+    off = align_up(off + cub_bytes, 256);
+  }
+  L.total = off;
+  return true;
+}
+
+int cuda_fail(cudaError_t e) { return record_cuda_error(e); }
+
+template <typename InT>
+int launch_encode(const hqmq_encode_args* a, const Layout& L, cudaStream_t st) {
+  char* ws = reinterpret_cast<char*>(a->workspace);
+  const bool ext = a->outlier_multiplier > 0.0;
+  const bool aligned4 = (a->head_dim % 4) == 0 &&
+                        (reinterpret_cast<uintptr_t>(a->data) % (4 * sizeof(InT))) == 0;
+  cudaError_t e;
+  if (a->index_capacity_words) cudaMemsetAsync(a->index_words, 0, a->index_capacity_words * 4, st);
+  if (a->radius_capacity_words) cudaMemsetAsync(a->radius_words, 0, a->radius_capacity_words * 4, st);
+  if (a->flag_words && a->flag_capacity_words)
+    cudaMemsetAsync(a->flag_words, 0, a->flag_capacity_words * 4, st);
+  cudaMemsetAsync(a->counters, 0, 3 * sizeof(int64_t), st);
+  if (L.n_chunks == 0) {
+    set_counts_kernel<<<1, 32, 0, st>>>(0, a->counters);
+    e = cudaGetLastError();
+    return e == cudaSuccess ? HQMQ_OK : cuda_fail(e);
+  }
+  RadixGroup* groups = nullptr;
+  uint32_t* prefix = nullptr;
+  if (ext) {
+    groups = reinterpret_cast<RadixGroup*>(ws + L.off_groups);
+    uint32_t* hist = reinterpret_cast<uint32_t*>(ws + L.off_hist);
+    unsigned int* done = reinterpret_cast<unsigned int*>(ws + L.off_done);
+    cudaMemsetAsync(hist, 0, (size_t)L.G * kBins * 4, st);
+    cudaMemsetAsync(done, 0, 16, st);
+    const unsigned long long n_per_group =
+        (unsigned long long)(L.n_chunks / (a->per_head_pooling ? a->heads : 1));
+    radix_init_kernel<<<(L.G + 127) / 128, 128, 0, st>>>(groups, L.G, n_per_group);
+    RadixParams rp;
+    rp.B = a->batch; rp.H = a->heads; rp.T = a->tokens; rp.D = a->head_dim; rp.C = L.C;
+    rp.per_head = a->per_head_pooling; rp.aligned4 = aligned4; rp.multiplier = a->outlier_multiplier;
+    rp.data = a->data; rp.norms = reinterpret_cast<double*>(ws + L.off_norms);
+    rp.groups = groups; rp.hist = hist; rp.done = done; rp.G = L.G;
+    const dim3 hgrid((unsigned)ceil_div(a->tokens * L.C, kHistChunksPerBlock), (unsigned)L.rows);
+    for (int pass = 0; pass < kPasses; ++pass) {
+      rp.pass = pass;
+      radix_hist_kernel<InT><<<hgrid, kHistThreads, 0, st>>>(rp);
+    }
+    uint32_t* counts = reinterpret_cast<uint32_t*>(ws + L.off_counts);
+    prefix = reinterpret_cast<uint32_t*>(ws + L.off_prefix);
+    tile_count_kernel<<<dim3((unsigned)L.tiles_per_row, (unsigned)L.rows), 256, 0, st>>>(
+        rp.norms, groups, a->heads, a->tokens, L.C, L.TT, L.tiles_per_row,
+        a->per_head_pooling, counts);
+    size_t cub_bytes = L.cub_bytes;
+    cub::DeviceScan::ExclusiveSum(ws + L.off_cub, cub_bytes, counts, prefix, (int)L.n_tiles, st);
+    finalize_counts_kernel<<<1, 32, 0, st>>>(counts, prefix, L.n_tiles, L.n_chunks, a->counters);
+  } else {
+    set_counts_kernel<<<1, 32, 0, st>>>(L.n_chunks, a->counters);
+  }
+  EncParams p;
+  p.B = a->batch; p.H = a->heads; p.T = a->tokens; p.D = a->head_dim;
+  p.C = L.C; p.S = a->codebook_size; p.br = a->radius_bits; p.w = a->index_bits;
+  p.TT = L.TT; p.tiles_per_row = L.tiles_per_row; p.aligned4 = aligned4;
+  p.per_head = a->per_head_pooling;
+  p.data = a->data;
+  p.rot = reinterpret_cast<const float4*>(a->rot_f32);
+  p.joint = a->joint_f64;
+  p.groups = groups;
+  p.tile_prefix = prefix;
+  p.scales = a->scales; p.idxw = a->index_words; p.radw = a->radius_words;
+  p.flagw = ext ? a->flag_words : nullptr;
+  p.payloads = a->payloads; p.payload_capacity = ext ? a->payload_capacity : 0;
+  p.tokoff = ext ? a->token_offsets : nullptr;
+  p.counters = a->counters; p.err = a->error_word;
+  const size_t smem = (size_t)std::min(a->codebook_size, kSBlock) * 4 * sizeof(float4);
+  static thread_local bool attr_set[4] = {false, false, false, false};
+  const int ti = sizeof(InT) == 2 ? (std::is_same<InT, __half>::value ? 0 : 1) : (sizeof(InT) == 4 ? 2 : 3);
+  if (!attr_set[ti]) {
+    cudaFuncSetAttribute(encode_tile_kernel<InT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         kSBlock * 4 * (int)sizeof(float4));
+    attr_set[ti] = true;
+  }
+  encode_tile_kernel<InT><<<dim3((unsigned)L.tiles_per_row, (unsigned)L.rows), kEncThreads, smem, st>>>(p);
+  e = cudaGetLastError();
+  return e == cudaSuccess ? HQMQ_OK : cuda_fail(e);
+}
+
+}  // namespace
+}  // namespace hqmq
+
+extern "C" {
+
+size_t hqmq_encode_workspace_bytes(const hqmq_encode_args* a) {
+  hqmq::Layout L;
+  if (!hqmq::plan(a, L)) return 0;
+  return L.total;
+}
+
+int hqmq_encode(const hqmq_encode_args* a, void* stream) {
+  using namespace hqmq;
+  Layout L;
+  if (!plan(a, L)) return HQMQ_ERR_INVALID_ARGUMENT;
+  if (a->codebook_size < 1 || a->radius_bits < 1 || a->radius_bits > 8 || a->index_bits < 1 ||
+      a->index_bits > 32)
+    return HQMQ_ERR_INVALID_ARGUMENT;
+  if ((int64_t)kGroupOrder * a->codebook_size - 1 >= (1LL << 31)) return HQMQ_ERR_UNSUPPORTED;
+  if (L.n_chunks >= (1LL << 32)) return HQMQ_ERR_UNSUPPORTED;
+  if (L.rows >= 65536) return HQMQ_ERR_UNSUPPORTED;
+  if (a->workspace_bytes < L.total) return HQMQ_ERR_WORKSPACE;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  switch (a->input_dtype) {
+    case HQMQ_F16: return launch_encode<__half>(a, L, st);
+    case HQMQ_BF16: return launch_encode<__nv_bfloat16>(a, L, st);
+    case HQMQ_F32: return launch_encode<float>(a, L, st);
+    case HQMQ_F64: return launch_encode<double>(a, L, st);
+    default: return HQMQ_ERR_INVALID_ARGUMENT;
+  }
+}
+
+}  // extern "C"

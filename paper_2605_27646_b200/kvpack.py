@@ -1,0 +1,203 @@
+"""The kvpack v1 container around the device-packed sections.
+
+Byte-identical to the reference writer (kvpack.py:7-37,126-177): 128-byte
+little-endian header, section table of 5 x (offset u64, length u64), the
+sections in order (scales, indices, radii, flags, payloads), CRC-32 trailer.
+The section bit streams are produced by the encode kernel in HBM already in
+their serialized form (LSB-first, byte-aligned starts), so to_bytes is a
+device->host copy plus the header and checksum; from_bytes validates like
+the reference reader (kvpack.py:194-306) and uploads the sections, deriving
+the per-token coded offsets and checking every index on the GPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import struct
+import zlib
+
+import numpy as np
+
+from . import _native as nat
+from .codebook import ROLE_TAGS
+from .codec import CHUNK_DIM, CodecConfig, QuantizedTensor, TensorShape, _words
+from .errors import CorruptData, InvalidArgument, UnsupportedVersion
+
+MAGIC = b"HQMQ"
+VERSION = 1
+HEADER_BYTES = 128
+_HEADER_FMT = "<4sHHIIIIIBBHQII"
+_SECTION_COUNT = 5
+_FLAG_OUTLIER = 1
+_FLAG_PER_HEAD = 2
+
+
+def _multiplier_to_fixed(multiplier) -> int:
+    if multiplier is None:
+        return 0
+    fixed = int(round(multiplier * 65536.0))
+    if not 0 < fixed <= 0xFFFFFFFF:
+        raise InvalidArgument(f"outlier multiplier {multiplier} not representable")
+    return fixed
+
+
+def expected_file_size(packed: QuantizedTensor) -> int:
+    """kvpack.py:99-112."""
+    s, c = packed.shape, packed.config
+    n = s.n_chunks
+    n_coded = packed.n_coded
+    size = HEADER_BYTES + 2 * s.batch * s.heads * s.tokens
+    size += (n_coded * c.index_bits + 7) // 8
+    size += (n_coded * c.radius_bits + 7) // 8
+    if c.outlier_multiplier is not None:
+        size += (n + 7) // 8
+    size += 8 * packed.n_payload
+    return size + 4
+
+
+def to_bytes(packed: QuantizedTensor) -> bytes:
+    s, c = packed.shape, packed.config
+    if packed.role not in ROLE_TAGS:
+        raise InvalidArgument(f"role must be one of {sorted(ROLE_TAGS)}")
+    if not 0 <= packed.head_base + s.heads <= 0xFFFF:
+        raise InvalidArgument("head_base + heads must fit in 16 bits")
+    sections = packed.section_bytes()
+    flags = (_FLAG_OUTLIER if c.outlier_multiplier is not None else 0) | (
+        _FLAG_PER_HEAD if c.median_pooling == "per_head" else 0)
+    header = struct.pack(_HEADER_FMT, MAGIC, VERSION, flags, s.batch, s.heads, s.tokens,
+                         s.head_dim, c.codebook_size, c.radius_bits, ROLE_TAGS[packed.role],
+                         packed.head_base, c.seed, _multiplier_to_fixed(c.outlier_multiplier),
+                         packed.layer)
+    table = bytearray()
+    off = HEADER_BYTES
+    for body in sections:
+        table += struct.pack("<QQ", off, len(body))
+        off += len(body)
+    payload = header + bytes(table) + b"".join(sections)
+    return payload + struct.pack("<I", zlib.crc32(payload) & 0xFFFFFFFF)
+
+
+def write_kvpack(packed: QuantizedTensor, sink) -> int:
+    blob = to_bytes(packed)
+    if hasattr(sink, "write"):
+        sink.write(blob)
+    else:
+        with open(sink, "wb") as f:
+            f.write(blob)
+    return len(blob)
+
+
+def read_kvpack(source, device="cuda") -> QuantizedTensor:
+    if hasattr(source, "read"):
+        blob = source.read()
+    else:
+        with open(source, "rb") as f:
+            blob = f.read()
+    return from_bytes(blob, device)
+
+
+def _upload_words(buf: bytes, nbits: int, device):
+    import torch
+
+    n = _words(nbits)
+    raw = np.zeros(n * 4, dtype=np.uint8)
+    raw[: len(buf)] = np.frombuffer(buf, dtype=np.uint8)
+    return torch.from_numpy(raw.view("<i4").copy()).to(device)
+
+
+def from_bytes(blob: bytes, device="cuda") -> QuantizedTensor:
+    """Parse and validate (kvpack.py:194-306), then upload to the device."""
+    import torch
+
+    if len(blob) < HEADER_BYTES + 4:
+        raise CorruptData(f"file too short ({len(blob)} bytes)")
+    (magic, version, flags, batch, heads, tokens, head_dim, size, radius_bits, role_tag,
+     head_base, seed, fixed_mult, layer) = struct.unpack_from(_HEADER_FMT, blob, 0)
+    if magic != MAGIC:
+        raise CorruptData(f"bad magic {magic!r}")
+    if version != VERSION:
+        raise UnsupportedVersion(f"format version {version}, expected {VERSION}")
+    (crc_stored,) = struct.unpack_from("<I", blob, len(blob) - 4)
+    if zlib.crc32(blob[:-4]) & 0xFFFFFFFF != crc_stored:
+        raise CorruptData("checksum mismatch")
+    table = []
+    end = HEADER_BYTES
+    for k in range(_SECTION_COUNT):
+        off, length = struct.unpack_from("<QQ", blob, 48 + 16 * k)
+        if off != end:
+            raise CorruptData(f"section {k} offset {off} != expected {end}")
+        end = off + length
+        table.append((off, length))
+    if end + 4 != len(blob):
+        raise CorruptData(f"file length {len(blob)} != sections end {end} + checksum")
+    roles = {tag: role for role, tag in ROLE_TAGS.items()}
+    if role_tag not in roles:
+        raise CorruptData(f"unknown role tag {role_tag:#x}")
+    outlier = bool(flags & _FLAG_OUTLIER)
+    if outlier != (fixed_mult != 0):
+        raise CorruptData("outlier flag and multiplier field disagree")
+    try:
+        shape = TensorShape(batch, heads, tokens, head_dim)
+        config = CodecConfig(codebook_size=size, radius_bits=radius_bits, seed=seed,
+                             outlier_multiplier=fixed_mult / 65536.0 if outlier else None,
+                             median_pooling="per_head" if flags & _FLAG_PER_HEAD else "batch")
+    except InvalidArgument as exc:
+        raise CorruptData(f"invalid header fields: {exc}") from exc
+
+    def section(k):
+        off, length = table[k]
+        return blob[off:off + length]
+
+    nat.require_cuda(device)
+    device = torch.device(device)
+    n_tok = batch * heads * tokens
+    n = n_tok * shape.chunks_per_vector
+    if len(section(0)) != 2 * n_tok:
+        raise CorruptData("scale section has the wrong length")
+    scales = torch.from_numpy(np.frombuffer(section(0), dtype="<f2").astype(np.float16).reshape(
+        batch, heads, tokens)).to(device)
+    if outlier:
+        if len(section(3)) != (n + 7) // 8:
+            raise CorruptData("flag bitmap has the wrong length")
+        fbits = np.unpackbits(np.frombuffer(section(3), dtype=np.uint8), bitorder="little",
+                              count=n)
+        n_flag = int(fbits.sum())
+        fw = _upload_words(section(3), n, device)
+    else:
+        if len(section(3)) != 0:
+            raise CorruptData("unexpected flag bitmap without extraction")
+        n_flag = 0
+        fw = None
+    n_coded = n - n_flag
+    w, br = config.index_bits, config.radius_bits
+    if len(section(1)) != (n_coded * w + 7) // 8:
+        raise CorruptData(f"bit stream length {len(section(1))} != expected {(n_coded * w + 7) // 8}")
+    if len(section(2)) != (n_coded * br + 7) // 8:
+        raise CorruptData(f"bit stream length {len(section(2))} != expected {(n_coded * br + 7) // 8}")
+    iw = _upload_words(section(1), n * w, device)
+    rw = _upload_words(section(2), n * br, device)
+    pay_raw = section(4)
+    if len(pay_raw) != 8 * n_flag:
+        raise CorruptData("payload section has the wrong length")
+    pay = torch.zeros((max(1, n_flag), CHUNK_DIM), dtype=torch.float16, device=device)
+    if n_flag:
+        pay[:n_flag] = torch.from_numpy(np.frombuffer(pay_raw, dtype="<f2").astype(
+            np.float16).reshape(n_flag, CHUNK_DIM)).to(device)
+    L = nat.lib()
+    stream = nat.stream_handle(device)
+    tok = None
+    if outlier:
+        tok = torch.zeros(max(1, n_tok), dtype=torch.int32, device=device)
+        ws = torch.empty(int(L.hqmq_token_offsets_workspace_bytes(n_tok)), dtype=torch.uint8,
+                         device=device)
+        nat.check(L.hqmq_token_offsets(n_tok, shape.chunks_per_vector, fw.data_ptr(),
+                                       tok.data_ptr(), ws.data_ptr(), ws.numel(), stream),
+                  "hqmq_token_offsets")
+    err = torch.zeros(1, dtype=torch.int32, device=device)
+    nat.check(L.hqmq_validate_indices(iw.data_ptr(), n_coded, w, config.index_count,
+                                      err.data_ptr(), stream), "hqmq_validate_indices")
+    if int(err.item()) & nat.DEVERR_INDEX:
+        raise CorruptData("codeword index out of range")
+    meta = torch.tensor([n_coded, n_flag, 0, 0], dtype=torch.int64, device=device)
+    return QuantizedTensor(shape, config, layer, roles[role_tag], head_base, scales, iw, rw, fw,
+                           pay, tok, meta, device, n_coded=n_coded, n_payload=n_flag)

@@ -1,0 +1,368 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference's
+golden fixtures and against the oracle on the same seeded inputs.
+
+Bar (north star): indices, quanta, flags, scales, payloads and kvpack bytes
+bit-exact; fp64 decode bit-exact; fp32 decode within 1e-6 relative.
+"""
+
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+from conftest import GOLDEN, codec_fixtures, load_codec_fixture
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def hq():
+    import paper_2605_27646_b200 as m
+
+    return m
+
+
+def to_device(data: np.ndarray, cast: str, dev):
+    dt = {"f16": torch.float16, "bf16": torch.bfloat16, "f32": torch.float32,
+          "f64": torch.float64}[cast]
+    t = torch.from_numpy(np.ascontiguousarray(data)).to(dev).to(dt)
+    assert torch.equal(t.to(torch.float64).cpu(), torch.from_numpy(data)), "cast must be exact"
+    return t
+
+
+def config_of(meta):
+    return hq().CodecConfig(codebook_size=meta["codebook_size"], radius_bits=meta["radius_bits"],
+                            seed=meta["seed"], outlier_multiplier=meta["outlier_multiplier"],
+                            median_pooling=meta["median_pooling"])
+
+
+def assert_same_fields(qt, ref):
+    np.testing.assert_array_equal(qt.scales.cpu().numpy().view(np.uint16),
+                                  np.asarray(ref["scales"], np.float16).view(np.uint16))
+    np.testing.assert_array_equal(qt.indices.cpu().numpy(), ref["indices"])
+    np.testing.assert_array_equal(qt.quanta.cpu().numpy(), ref["quanta"])
+    np.testing.assert_array_equal(qt.flags.cpu().numpy(), ref["flags"])
+    np.testing.assert_array_equal(qt.payloads.cpu().numpy().view(np.uint16),
+                                  np.asarray(ref["payloads"], np.float16).view(np.uint16))
+
+
+def assert_fp32_close(got, want):
+    got = got.astype(np.float64)
+    err = np.abs(got - want)
+    bound = 1e-6 * np.abs(want) + 1e-30
+    assert np.all(err <= bound), f"max rel err {np.max(err / (np.abs(want) + 1e-30)):.3e}"
+
+
+# ----------------------------------------------------------- golden fixtures
+@pytest.mark.parametrize("name", codec_fixtures())
+def test_encode_matches_reference_golden(cuda, name):
+    m = hq()
+    meta, g = load_codec_fixture(name)
+    x = to_device(g["data"], meta["cast"], cuda)
+    cfg = config_of(meta)
+    bank = m.CodebookBank(seed=cfg.seed, size=cfg.codebook_size)
+    qt = m.encode_tensor(x, cfg, layer=meta["layer"], role=meta["role"], bank=bank,
+                         head_base=meta["head_base"])
+    assert_same_fields(qt, g)
+    blob = m.to_bytes(qt)
+    assert blob == g["blob"].tobytes()
+    assert hashlib.sha256(blob).hexdigest() == meta["digest"]
+    assert m.expected_file_size(qt) == len(blob)
+    # fp64 decode is bit-identical to the reference decode_tensor
+    d64 = m.decode_tensor(qt, bank, dtype=torch.float64).cpu().numpy()
+    np.testing.assert_array_equal(d64, g["decoded"])
+    # fp32 decode within 1e-6 relative, elementwise
+    assert_fp32_close(m.decode_tensor(qt, bank, dtype=torch.float32).cpu().numpy(), g["decoded"])
+    # tile decode == slice of full decode (test_codec.py:171-180)
+    t = qt.shape.tokens
+    for a, b in ((0, t), (0, t // 3), (t // 3, t), (t - 1, t), (t // 2, t // 2)):
+        tile = m.decode_token_range(qt, bank, a, b, dtype=torch.float64).cpu().numpy()
+        np.testing.assert_array_equal(tile, g["decoded"][:, :, a:b])
+    # kvpack round trip on the device
+    back = m.from_bytes(blob)
+    assert m.to_bytes(back) == blob
+    np.testing.assert_array_equal(m.decode_tensor(back, bank, dtype=torch.float64).cpu().numpy(),
+                                  g["decoded"])
+    assert_same_fields(back, g)
+
+
+def test_frozen_reference_digest(cuda):
+    """The reference's frozen digest (test_kvpack.py:28), produced by the GPU path."""
+    m = hq()
+    data = m.RandomStream(0x5EA1).gaussian(1 * 2 * 16 * 32).reshape(1, 2, 16, 32)
+    data[0, 0, 3, 0:4] *= 60.0
+    cfg = m.CodecConfig(codebook_size=48, radius_bits=4, seed=7, outlier_multiplier=3.0)
+    qt = m.encode_tensor(data, cfg)
+    digest = hashlib.sha256(m.to_bytes(qt)).hexdigest()
+    assert digest == "12b2dfad207652800819a0ab439f8ef44c1c5ce33eff0f70979bc4e8b2cc1039"
+
+
+def test_from_arrays_pack_matches_encoder(cuda):
+    m = hq()
+    meta, g = load_codec_fixture("outlier_heavy")
+    cfg = config_of(meta)
+    shape = m.TensorShape(*g["data"].shape)
+    qt = m.QuantizedTensor.from_arrays(shape, cfg, meta["layer"], meta["role"], g["scales"],
+                                       g["indices"], g["quanta"], g["flags"], g["payloads"],
+                                       meta["head_base"], device=cuda)
+    assert m.to_bytes(qt) == g["blob"].tobytes()
+
+
+def test_nearest_scan_known_answers(cuda):
+    m = hq()
+    z = np.load(os.path.join(GOLDEN, "scan.npz"))
+    for dirs, cw, idx, cos in (("tie_dirs", "cell", "tie_idx", "tie_cos"),
+                               ("rnd", "j96", "rnd_idx", "rnd_cos"),
+                               ("hits", "j96", "hit_idx", "hit_cos")):
+        i, c = m.nearest_scan(z[dirs], z[cw])
+        np.testing.assert_array_equal(i.cpu().numpy(), z[idx])
+        np.testing.assert_array_equal(c.cpu().numpy(), z[cos])
+
+
+def test_nearest_scan_vs_oracle_random(cuda, oracle):
+    m = hq()
+    rs = np.random.default_rng(1)
+    dirs = rs.standard_normal((20000, 4))
+    dirs /= np.sqrt((dirs * dirs).sum(1))[:, None]
+    cw = oracle.joint(3, 2, 1, "V", 64)
+    i, c = m.nearest_scan(dirs, cw)
+    oi, oc = oracle.nearest_scan(dirs, cw, threads=os.cpu_count() or 1)
+    np.testing.assert_array_equal(i.cpu().numpy(), oi)
+    np.testing.assert_array_equal(c.cpu().numpy(), oc)
+    # empty codebook: idx 0, cos -2.0 (_kernels.pyx:32-33)
+    i0, c0 = m.nearest_scan(dirs[:3], np.zeros((0, 4)))
+    assert i0.tolist() == [0, 0, 0] and c0.tolist() == [-2.0, -2.0, -2.0]
+
+
+# --------------------------------------------------- oracle parity, seeded
+def _oracle_encode(oracle, x64, cfg, layer=0, role="K", head_base=0):
+    return oracle.encode(x64, cfg.codebook_size, cfg.radius_bits, seed=cfg.seed,
+                         multiplier=cfg.outlier_multiplier, pooling=cfg.median_pooling,
+                         layer=layer, role=role, head_base=head_base,
+                         threads=os.cpu_count() or 1)
+
+
+CASES = [
+    # (shape, S, b_r, C, pooling, profile, dtype, layer, role)
+    ((1, 8, 4096, 128), 16, 4, 3.0, "batch", "gauss", "f16", 0, "K"),   # C1, full
+    ((1, 8, 1024, 128), 64, 4, None, "batch", "gauss", "f16", 7, "V"),
+    ((1, 2, 512, 128), 256, 4, None, "batch", "gauss", "f16", 79, "K"),
+    ((1, 4, 2048, 128), 64, 6, 3.0, "batch", "outlier", "f16", 3, "K"),
+    ((2, 4, 300, 128), 64, 6, 3.0, "per_head", "outlier", "f16", 1, "V"),
+    ((1, 4, 256, 64), 32, 5, 2.0, "batch", "gauss", "bf16", 0, "K"),
+    ((3, 2, 77, 96), 40, 7, 3.0, "batch", "gauss", "f32", 4, "V"),
+    ((1, 3, 33, 20), 24, 3, 0.5, "batch", "gauss", "f64", 2, "K"),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[f"{c[0]}-S{c[1]}-{c[5]}-{c[6]}" for c in CASES])
+def test_encode_decode_vs_oracle(cuda, oracle, case):
+    m = hq()
+    shape, S, br, C, pool, prof, dt, layer, role = case
+    seed = 100 + CASES.index(case)
+    if prof == "gauss":
+        x = oracle.gen_gaussian(shape, seed=seed)
+    else:
+        x = oracle.gen_outlier_heavy(shape, seed=seed)
+    xt = torch.from_numpy(x).to(cuda).to({"f16": torch.float16, "bf16": torch.bfloat16,
+                                            "f32": torch.float32, "f64": torch.float64}[dt])
+    x64 = xt.to(torch.float64).cpu().numpy()
+    cfg = m.CodecConfig(codebook_size=S, radius_bits=br, seed=11, outlier_multiplier=C,
+                        median_pooling=pool)
+    bank = m.CodebookBank(11, S)
+    qt = m.encode_tensor(xt, cfg, layer=layer, role=role, bank=bank)
+    ref = _oracle_encode(oracle, x64, cfg, layer, role)
+    assert_same_fields(qt, {f: getattr(ref, f) for f in
+                            ("scales", "indices", "quanta", "flags", "payloads")})
+    assert m.to_bytes(qt) == oracle.to_bytes(ref)
+    dec = oracle.decode(ref)
+    np.testing.assert_array_equal(m.decode_tensor(qt, bank, dtype=torch.float64).cpu().numpy(), dec)
+    assert_fp32_close(m.decode_tensor(qt, bank).cpu().numpy(), dec)
+    h16 = m.decode_tensor(qt, bank, dtype=torch.float16).cpu().numpy().astype(np.float64)
+    assert np.max(np.abs(h16 - dec) / (np.abs(dec) + 1e-3)) < 1e-2
+
+
+def test_full_size_c2_unit_sampled(cuda, oracle):
+    """Llama-3-8B unit at full size (1, 8, 32768, 128), S=64: without extraction
+    the encode is token-local, so sampled token slices are compared exactly."""
+    m = hq()
+    g = torch.Generator(device=cuda).manual_seed(1234)
+    x = torch.randn((1, 8, 32768, 128), generator=g, device=cuda).to(torch.float16)
+    cfg = m.CodecConfig(codebook_size=64, radius_bits=4)
+    bank = m.CodebookBank(0, 64)
+    qt = m.encode_tensor(x, cfg, layer=17, role="V", bank=bank)
+    rs = np.random.default_rng(0)
+    toks = np.sort(rs.choice(32768, 256, replace=False))
+    xs = x[:, :, toks].to(torch.float64).cpu().numpy()
+    ref = _oracle_encode(oracle, xs, cfg, 17, "V")
+    idx = qt.indices.cpu().numpy()[:, :, toks]
+    np.testing.assert_array_equal(idx, ref.indices)
+    np.testing.assert_array_equal(qt.quanta.cpu().numpy()[:, :, toks], ref.quanta)
+    np.testing.assert_array_equal(qt.scales.cpu().numpy()[:, :, toks].view(np.uint16),
+                                  ref.scales.view(np.uint16))
+    d = m.decode_tensor(qt, bank, dtype=torch.float64)[:, :, toks].cpu().numpy()
+    np.testing.assert_array_equal(d, oracle.decode(ref))
+    # size-independent property: decode(encode(x)) error bounded by the
+    # radius step + covering radius; the round trip is stable (re-encode of the
+    # fp64 decode reproduces identical codes for cell-exact inputs)
+    dec = m.decode_tensor(qt, bank)
+    rel = (torch.linalg.vector_norm(dec - x.float()) / torch.linalg.vector_norm(x.float())).item()
+    assert rel < 0.2
+
+
+def test_full_size_c3_unit(cuda, oracle):
+    """Qwen2.5-7B unit at full size (1, 4, 32768, 128), outlier-heavy, S=64,
+    b_r=6, Med3x over the whole call: compared exactly against the oracle."""
+    m = hq()
+    x64 = oracle.gen_outlier_heavy((1, 4, 32768, 128), seed=9)
+    xt = torch.from_numpy(x64).to(cuda).to(torch.float16)
+    x64 = xt.to(torch.float64).cpu().numpy()
+    cfg = m.CodecConfig(codebook_size=64, radius_bits=6, outlier_multiplier=3.0)
+    bank = m.CodebookBank(0, 64)
+    qt = m.encode_tensor(xt, cfg, layer=3, role="K", bank=bank)
+    ref = _oracle_encode(oracle, x64, cfg, 3, "K")
+    assert qt.n_payload == ref.payloads.shape[0]
+    assert m.to_bytes(qt) == oracle.to_bytes(ref)
+
+
+def test_edge_cases(cuda):
+    m = hq()
+    cfg = m.CodecConfig(codebook_size=24, radius_bits=3, outlier_multiplier=3.0)
+    # empty token axis (test_codec.py:219-224)
+    qt = m.encode_tensor(np.zeros((1, 2, 0, 8)), cfg)
+    assert m.decode_tensor(qt).shape == (1, 2, 0, 8)
+    assert qt.n_payload == 0
+    # all-zero tensor: sentinel scale 1.0, zero indices, decode zeros
+    qt = m.encode_tensor(np.zeros((1, 1, 4, 8)), m.CodecConfig(24, 3))
+    assert torch.all(qt.scales.float() == 1.0)
+    assert torch.count_nonzero(m.decode_tensor(qt)) == 0
+    # sigma underflow -> InvalidArgument (radius.py:42-43)
+    with pytest.raises(m.InvalidArgument):
+        m.encode_tensor(np.full((1, 1, 2, 4), 1e-9), m.CodecConfig(24, 3))
+    # sigma overflow: fp16 scale inf, decode NaN (reference behaviour)
+    qt = m.encode_tensor(np.full((1, 1, 1, 4), 1e5), m.CodecConfig(24, 3))
+    assert torch.isinf(qt.scales.float()).all()
+    # validation
+    with pytest.raises(m.InvalidArgument):
+        m.encode_tensor(np.zeros((1, 1, 4)), cfg)
+    with pytest.raises(m.InvalidArgument):
+        m.encode_tensor(np.zeros((1, 1, 4, 4)), cfg, role="Q")
+    qt = m.encode_tensor(np.ones((1, 1, 4, 8)), m.CodecConfig(24, 3))
+    with pytest.raises(m.InvalidArgument):
+        m.decode_token_range(qt, m.CodebookBank(0, 24), 2, 1)
+    with pytest.raises(m.InvalidArgument):
+        m.decode_token_range(qt, m.CodebookBank(0, 24), 0, 5)
+    with pytest.raises(m.InvalidArgument):
+        m.decode_tensor(qt, m.CodebookBank(1, 24))
+
+
+def test_corrupt_index_detected(cuda):
+    """An out-of-range code in a CRC-valid file raises CorruptData (kvpack.py:279-280)."""
+    import struct
+    import zlib
+
+    m = hq()
+    cfg = m.CodecConfig(codebook_size=48, radius_bits=4)  # 1152 codewords, 11-bit codes
+    qt = m.encode_tensor(np.random.default_rng(0).standard_normal((1, 1, 4, 8)), cfg)
+    blob = bytearray(m.to_bytes(qt))
+    off, length = struct.unpack_from("<QQ", blob, 48 + 16)
+    blob[off] = 0xFF
+    blob[off + 1] |= 0x07  # first code = 2047 >= 1152
+    body = bytes(blob[:-4])
+    blob[-4:] = struct.pack("<I", zlib.crc32(body) & 0xFFFFFFFF)
+    with pytest.raises(m.CorruptData):
+        m.from_bytes(bytes(blob))
+    blob2 = bytearray(m.to_bytes(qt))
+    blob2[200 % len(blob2)] ^= 1
+    with pytest.raises(m.CorruptData):
+        m.from_bytes(bytes(blob2))
+
+
+def test_head_base_keying(cuda):
+    """head_base shifts codebook keys (test_codec.py:197-206)."""
+    m = hq()
+    x = np.random.default_rng(5).standard_normal((1, 2, 8, 8))
+    cfg = m.CodecConfig(24, 4)
+    bank = m.CodebookBank(0, 24)
+    whole = m.encode_tensor(x, cfg, bank=bank)
+    tail = m.encode_tensor(x[:, 1:], cfg, bank=bank, head_base=1)
+    assert torch.equal(whole.indices[:, 1:], tail.indices)
+
+
+# ------------------------------------------------------------- attention
+@pytest.mark.parametrize("name", ["decode_gqa", "prefill_causal"])
+def test_attention_golden(cuda, name):
+    m = hq()
+    z = np.load(os.path.join(GOLDEN, f"attn_{name}.npz"))
+    b, hq_, hkv, tq, tkv, d = (int(v) for v in z["dims"])
+    cfg = m.AttentionConfig(b, hq_, hkv, tq, tkv, d)
+    codec = m.CodecConfig(24, 4)
+    bank = m.CodebookBank(0, 24)
+    pk = m.encode_tensor(z["k"], codec, role="K", bank=bank)
+    pv = m.encode_tensor(z["v"], codec, role="V", bank=bank)
+    for splits in (0, 1, 3):
+        out = m.fused_attend(torch.from_numpy(z["q"]), pk, pv, bank, cfg, num_splits=splits)
+        err = np.max(np.abs(out.double().cpu().numpy() - z["dense"]))
+        assert err <= 2e-5, (splits, err)
+
+
+def test_attention_decode_llama_shape(cuda, oracle):
+    """Llama-3-8B decode step shape (GQA 32/8, T_q=1, d=128), S=64, 4k keys."""
+    m = hq()
+    B, HQ, HKV, T, D = 2, 32, 8, 4096, 128
+    g = torch.Generator(device=cuda).manual_seed(7)
+    k = torch.randn((B, HKV, T, D), generator=g, device=cuda).half()
+    v = torch.randn((B, HKV, T, D), generator=g, device=cuda).half()
+    q = torch.randn((B, HQ, 1, D), generator=g, device=cuda)
+    codec = m.CodecConfig(64, 4)
+    bank = m.CodebookBank(0, 64)
+    pk = m.encode_tensor(k, codec, role="K", bank=bank, layer=4)
+    pv = m.encode_tensor(v, codec, role="V", bank=bank, layer=4)
+    cfg = m.AttentionConfig(B, HQ, HKV, 1, T, D)
+    out = m.fused_attend(q, pk, pv, bank, cfg).double()
+    dense = m.reference_attend(q, m.decode_tensor(pk, bank, dtype=torch.float64),
+                               m.decode_tensor(pv, bank, dtype=torch.float64), cfg)
+    assert (out - dense).abs().max().item() <= 2e-5
+
+
+def test_attention_with_outliers(cuda):
+    m = hq()
+    B, HQ, HKV, TQ, T, D = 1, 8, 2, 3, 200, 64
+    rs = np.random.default_rng(3)
+    k = rs.standard_normal((B, HKV, T, D))
+    k[:, :, ::17, 8:12] *= 40.0
+    v = rs.standard_normal((B, HKV, T, D))
+    q = rs.standard_normal((B, HQ, TQ, D))
+    codec = m.CodecConfig(32, 5, outlier_multiplier=3.0)
+    bank = m.CodebookBank(0, 32)
+    pk = m.encode_tensor(k, codec, role="K", bank=bank)
+    pv = m.encode_tensor(v, codec, role="V", bank=bank)
+    assert pk.n_payload > 0
+    cfg = m.AttentionConfig(B, HQ, HKV, TQ, T, D)
+    out = m.fused_attend(q, pk, pv, bank, cfg).double()
+    dense = m.reference_attend(torch.from_numpy(q).to(cuda),
+                               m.decode_tensor(pk, bank, dtype=torch.float64),
+                               m.decode_tensor(pv, bank, dtype=torch.float64), cfg)
+    assert (out - dense).abs().max().item() <= 1e-4
+
+
+def test_attention_mismatch_errors(cuda):
+    m = hq()
+    z = np.load(os.path.join(GOLDEN, "attn_prefill_causal.npz"))
+    b, hq_, hkv, tq, tkv, d = (int(v) for v in z["dims"])
+    cfg = m.AttentionConfig(b, hq_, hkv, tq, tkv, d)
+    codec = m.CodecConfig(24, 4)
+    bank = m.CodebookBank(0, 24)
+    pk = m.encode_tensor(z["k"], codec, role="K", bank=bank)
+    pv = m.encode_tensor(z["v"], codec, role="V", bank=bank)
+    q = torch.from_numpy(z["q"])
+    with pytest.raises(m.ConfigMismatch):
+        m.fused_attend(q, pv, pk, bank, cfg)
+    with pytest.raises(m.ConfigMismatch):
+        m.fused_attend(q, pk, pv, m.CodebookBank(99, 24), cfg)
+    with pytest.raises(m.InvalidArgument):
+        m.fused_attend(q[:, :, :, :8], pk, pv, bank, cfg)
+    with pytest.raises(m.InvalidArgument):
+        m.fused_attend(q, pk, pv, bank, cfg, tile=0)
