@@ -65,6 +65,12 @@ const char* hqmq_status_string(int status);
 /* Last CUDA error string recorded by a failing call on this thread. */
 const char* hqmq_last_error(void);
 
+/* FP32-pipe calibration probe: `blocks` CTAs x 256 threads each run `iters`
+ * iterations of 16 independent fp32 FMAs (packed = 0: scalar FFMA; packed = 1:
+ * 8 FFMA2).  Lane-ops per launch = blocks*256*iters*16.  Used by bench.py to
+ * measure the encode roofline denominator on the box. */
+int hqmq_fp32_probe(float* out, int32_t blocks, int32_t iters, int32_t packed, void* stream);
+
 /* --------------------------------------------------------- nearest scan */
 /* Exact twin of _kernels.nearest_scan (_kernels.pyx:16-46): for each of the n
  * directions (n x 4 fp64) the argmax over the m codewords (m x 4 fp64) of

@@ -84,6 +84,7 @@ SIGNATURES = {
     "hqmq_version": ([], ctypes.c_char_p),
     "hqmq_status_string": ([c_i32], ctypes.c_char_p),
     "hqmq_last_error": ([], ctypes.c_char_p),
+    "hqmq_fp32_probe": ([c_vp, c_i32, c_i32, c_i32, c_vp], c_i32),
     "hqmq_nearest_scan": ([c_vp, c_i64, c_vp, c_i64, c_vp, c_vp, c_vp], c_i32),
     "hqmq_encode_workspace_bytes": ([ctypes.POINTER(EncodeArgs)], ctypes.c_size_t),
     "hqmq_encode": ([ctypes.POINTER(EncodeArgs), c_vp], c_i32),

@@ -49,9 +49,52 @@ __global__ void nearest_scan_kernel(const double* __restrict__ dirs, int64_t n,
   }
 }
 
+// FP32-pipe calibration: independent FMA chains (scalar FFMA or packed FFMA2)
+// so the encode roofline denominator is measured on the box, not assumed.
+template <bool kPacked>
+__global__ void __launch_bounds__(256) fp32_probe_kernel(float* out, int iters, float seed) {
+  if (kPacked) {
+    float2 a[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) a[i] = make_float2(seed + i + threadIdx.x, seed - i);
+    const float2 b = make_float2(0.9999f, 1.0001f), c = make_float2(1e-7f, -1e-7f);
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = __ffma2_rn(a[i], b, c);
+    }
+    float acc = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc += a[i].x + a[i].y;
+    if (acc == 12345.678f) out[threadIdx.x] = acc;
+  } else {
+    float a[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) a[i] = seed + i + threadIdx.x;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) a[i] = fmaf(a[i], 0.9999f, 1e-7f);
+    }
+    float acc = 0.f;
+#pragma unroll
+    for (int i = 0; i < 16; ++i) acc += a[i];
+    if (acc == 12345.678f) out[threadIdx.x] = acc;
+  }
+}
+
 }  // namespace hqmq
 
 extern "C" {
+
+int hqmq_fp32_probe(float* out, int32_t blocks, int32_t iters, int32_t packed, void* stream) {
+  using namespace hqmq;
+  if (blocks < 1 || iters < 1) return HQMQ_ERR_INVALID_ARGUMENT;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (packed)
+    fp32_probe_kernel<true><<<blocks, 256, 0, st>>>(out, iters, 1.0f);
+  else
+    fp32_probe_kernel<false><<<blocks, 256, 0, st>>>(out, iters, 1.0f);
+  return check_launch();
+}
 
 const char* hqmq_version(void) { return "hqmq_b200 0.1.0 (sm_100a)"; }
 
