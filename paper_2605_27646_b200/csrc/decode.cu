@@ -145,6 +145,115 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(DecParams p) {
   }
 }
 
+// ------------------------------------------------ TMA-pipelined fast path
+// Token-aligned layout (head_dim 128, no extraction): token t's codes are the
+// index_bits words [t*w, (t+1)*w) and radius_bits words [t*br, (t+1)*br).  A
+// CTA owns one (batch, head) row slice; thread 0 streams 64-token tiles of the
+// three sections into a kFDStages-deep shared-memory ring with 1-D bulk
+// copies (cp.async.bulk, completion on an mbarrier) while all 8 warps decode
+// the previous tiles (warp = token, lane = chunk) and write coalesced rows.
+constexpr int kFDTok = 64;
+constexpr int kFDStages = 4;
+
+struct FastDecodeGeom {
+  uint32_t idx_off, rad_off, sc_off, stage_bytes;
+};
+
+__host__ __device__ inline FastDecodeGeom fd_geom(int w, int br) {
+  FastDecodeGeom g;
+  const uint32_t ib = kFDTok * w * 4 + 16, rb = kFDTok * br * 4 + 16, sb = kFDTok * 2;
+  g.idx_off = 0;
+  g.rad_off = (ib + 127) / 128 * 128;
+  g.sc_off = g.rad_off + (rb + 127) / 128 * 128;
+  g.stage_bytes = g.sc_off + (sb + 127) / 128 * 128;
+  return g;
+}
+
+template <typename OutT>
+__global__ void __launch_bounds__(256) decode_fast_kernel(DecParams p) {
+  extern __shared__ __align__(128) unsigned char dsm[];
+  __shared__ __align__(8) uint64_t full[kFDStages];
+  const int64_t row = blockIdx.y;
+  const int h = (int)(row % p.H);
+  const int ncw = kGroupOrder * p.S;
+  const int w = p.w, br = p.br;
+  const FastDecodeGeom g = fd_geom(w, br);
+  float4* tab = reinterpret_cast<float4*>(dsm);
+  unsigned char* ring = dsm + (size_t)ncw * sizeof(float4);
+  const float4* __restrict__ gtab = reinterpret_cast<const float4*>(p.table) + (int64_t)h * ncw;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t ntile = ceil_div(p.nt, kFDTok);
+  const int64_t tok_base = row * p.T + p.t0;  // first token of the range in this row
+
+  auto issue = [&](int64_t tile, int stage) {
+    const int64_t t = tok_base + tile * kFDTok;
+    const int ntok = (int)min((int64_t)kFDTok, p.nt - tile * kFDTok);
+    unsigned char* s = ring + (size_t)stage * g.stage_bytes;
+    const uint32_t ib = ntok * w * 4, rb = ntok * br * 4, sb = ntok * 2;
+    fence_proxy_async();
+    mbar_arrive_expect_tx(&full[stage], ib + rb + sb);
+    bulk_g2s(s + g.idx_off, p.idxw + t * w, ib, &full[stage]);
+    bulk_g2s(s + g.rad_off, p.radw + t * br, rb, &full[stage]);
+    bulk_g2s(s + g.sc_off, p.scales + t, sb, &full[stage]);
+  };
+
+  if (tid == 0) {
+    for (int s = 0; s < kFDStages; ++s) mbar_init(&full[s], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int s = 0;
+    for (int64_t tile = blockIdx.x; tile < ntile && s < kFDStages; tile += gridDim.x, ++s)
+      issue(tile, s);
+  }
+  for (int i = tid; i < ncw; i += 256) tab[i] = __ldg(gtab + i);
+  __syncthreads();
+
+  const float rtop = 1.0f / (float)((1 << br) - 1);
+  const uint32_t imask = w == 32 ? 0xffffffffu : ((1u << w) - 1u);
+  const uint32_t rmask = (1u << br) - 1u;
+  OutT* __restrict__ out = reinterpret_cast<OutT*>(p.out);
+  int k = 0;
+  for (int64_t tile = blockIdx.x; tile < ntile; tile += gridDim.x, ++k) {
+    const int stage = k % kFDStages;
+    mbar_wait(&full[stage], (uint32_t)((k / kFDStages) & 1));
+    const unsigned char* s = ring + (size_t)stage * g.stage_bytes;
+    const uint32_t* iw = reinterpret_cast<const uint32_t*>(s + g.idx_off);
+    const uint32_t* rw = reinterpret_cast<const uint32_t*>(s + g.rad_off);
+    const uint16_t* sc = reinterpret_cast<const uint16_t*>(s + g.sc_off);
+    const int ntok = (int)min((int64_t)kFDTok, p.nt - tile * kFDTok);
+#pragma unroll 4
+    for (int tt = warp; tt < ntok; tt += 8) {
+      const uint32_t bi = (uint32_t)(tt * w * 32 + lane * w);
+      const uint32_t* wp = iw + (bi >> 5);
+      uint32_t idx = __funnelshift_r(wp[0], wp[1], bi & 31) & imask;
+      const uint32_t bq = (uint32_t)(tt * br * 32 + lane * br);
+      const uint32_t* qp = rw + (bq >> 5);
+      const uint32_t q = __funnelshift_r(qp[0], qp[1], bq & 31) & rmask;
+      if (idx >= (uint32_t)ncw) {
+        atomicOr(p.err, HQMQ_DEVERR_INDEX_RANGE);
+        idx = 0;
+      }
+      const float rad = ((float)q * __half2float(__ushort_as_half(sc[tt]))) * rtop;
+      const float4 cw = tab[idx];
+      OutT* o = out + ((row * p.nt + tile * kFDTok + tt) * 128 + 4 * lane);
+      if constexpr (sizeof(OutT) == 4) {
+        *reinterpret_cast<float4*>(o) = make_float4(rad * cw.x, rad * cw.y, rad * cw.z, rad * cw.w);
+      } else {
+        OutT t4[4] = {Out<OutT>::cvt(rad * cw.x), Out<OutT>::cvt(rad * cw.y),
+                      Out<OutT>::cvt(rad * cw.z), Out<OutT>::cvt(rad * cw.w)};
+        *reinterpret_cast<uint2*>(o) = *reinterpret_cast<const uint2*>(t4);
+      }
+    }
+    __syncthreads();  // every warp is done with this stage
+    if (tid == 0) {
+      const int64_t nxt = tile + (int64_t)kFDStages * gridDim.x;
+      if (nxt < ntile) issue(nxt, stage);
+    }
+  }
+}
+
 // Bit-exact fp64 decode: ((q * sigma_w) / top) * codeword (codec.py:315-320).
 __global__ void __launch_bounds__(kDecThreads) decode_f64_kernel(DecParams p) {
   const int64_t row = blockIdx.y;
@@ -295,6 +404,26 @@ int launch_decode(DecParams& p, const hqmq_decode_args* a, cudaStream_t st) {
   const bool use_smem = smem <= kDecSmemLimit;
   p.table = a->joint_f32;
   p.aligned4 = (p.D % 4 == 0) && (reinterpret_cast<uintptr_t>(a->out) % (4 * sizeof(OutT)) == 0);
+  auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  const bool fast = p.D == 128 && !p.flagw && use_smem && p.aligned4 && p.T % 8 == 0 &&
+                    p.t0 % 8 == 0 && p.nt % 8 == 0 && al16(p.idxw) && al16(p.radw) &&
+                    al16(p.scales);
+  if (fast) {
+    const FastDecodeGeom g = fd_geom(p.w, p.br);
+    const size_t fsmem = smem + (size_t)kFDStages * g.stage_bytes;
+    static thread_local bool fset = false;
+    if (!fset) {
+      cudaFuncSetAttribute(decode_fast_kernel<OutT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           200 * 1024);
+      fset = true;
+    }
+    const int64_t ntile = ceil_div(p.nt, kFDTok);
+    const int per_sm = std::max<int>(1, std::min<int>(8, (int)((200 * 1024) / fsmem)));
+    const int64_t want = std::max<int64_t>(1, ceil_div((int64_t)148 * per_sm, rows));
+    const int64_t bx = std::max<int64_t>(1, std::min<int64_t>(want, ntile));
+    decode_fast_kernel<OutT><<<dim3((unsigned)bx, (unsigned)rows), 256, fsmem, st>>>(p);
+    return check();
+  }
   const int64_t nck = p.nt * p.C;
   const int64_t want = std::max<int64_t>(1, (148 * 4 + rows - 1) / rows);
   const int64_t bx = std::max<int64_t>(1, std::min<int64_t>(want, ceil_div(nck, kDecThreads * kDecR)));

@@ -166,9 +166,10 @@ __device__ __forceinline__ void coset_resolve(float2 wx, float2 yz, int& p, floa
 // Exact re-scoring of one uncertain chunk by a whole warp.  Candidates: every
 // (p, s) whose coset's fp32 score is within kDelta of the best fp32 coset
 // score; each is scored with the reference's fp64 arithmetic and the lowest
-// flat index p*S+s wins ties (_kernels.pyx:27-45).
+// flat index p*S+s wins ties (_kernels.pyx:27-45).  `rot` may point to global
+// or shared memory (generic loads).  Every lane returns the result.
 __device__ int warp_exact_index(const double (&x)[4], double r, const Dir2& u32,
-                                const float4* __restrict__ rot, const double* __restrict__ joint,
+                                const float4* rot, const double* __restrict__ joint,
                                 int S, int lane) {
   double u[4];
 #pragma unroll
@@ -176,8 +177,7 @@ __device__ int warp_exact_index(const double (&x)[4], double r, const Dir2& u32,
   float best = -1.f;
   for (int s = lane; s < S; s += kWarp) {
     float2 wx, yz;
-    rotate(u32, __ldg(rot + 4 * s), __ldg(rot + 4 * s + 1), __ldg(rot + 4 * s + 2),
-           __ldg(rot + 4 * s + 3), wx, yz);
+    rotate(u32, rot[4 * s], rot[4 * s + 1], rot[4 * s + 2], rot[4 * s + 3], wx, yz);
     best = fmaxf(best, coset_score(wx, yz));
   }
   best = warp_max(best);
@@ -186,8 +186,7 @@ __device__ int warp_exact_index(const double (&x)[4], double r, const Dir2& u32,
   long long lj = 0x7fffffffffffffffLL;
   for (int s = lane; s < S; s += kWarp) {
     float2 wx, yz;
-    rotate(u32, __ldg(rot + 4 * s), __ldg(rot + 4 * s + 1), __ldg(rot + 4 * s + 2),
-           __ldg(rot + 4 * s + 3), wx, yz);
+    rotate(u32, rot[4 * s], rot[4 * s + 1], rot[4 * s + 2], rot[4 * s + 3], wx, yz);
     if (coset_score(wx, yz) >= cut) {
       for (int pp = 0; pp < kGroupOrder; ++pp) {
         const long long j = (long long)pp * S + s;
@@ -458,6 +457,260 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_tile_kernel(EncParams p
   if (p.flagw) flush_bits(stage_f, p.flagw, (uint64_t)cb, (uint64_t)nck, true);
 }
 
+// ------------------------------------------- head_dim == 128 warp kernel
+// One warp owns a tile of kWT consecutive tokens of one (batch, head) row; lane
+// c holds chunk c of every token (32 chunks = 128 dims), so per-token sigma is
+// a warp max, the coded-prefix is a ballot/popc and a token's index codes fill
+// exactly index_bits whole words — no block barriers after the table load.
+// The next tile's input is prefetched into registers while the S-loop runs.
+constexpr int kWT = 4;  // tokens (chunks per lane) per warp tile
+constexpr int kWWarps = 8;
+constexpr int kWThreads = kWWarps * 32;
+
+__device__ __forceinline__ double warp_max_f64(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double w = __shfl_xor_sync(0xffffffffu, v, o);
+    v = w > v ? w : v;
+  }
+  return v;
+}
+
+template <typename InT>
+__global__ void __launch_bounds__(kWThreads, 3) encode_warp_kernel(EncParams p) {
+  extern __shared__ float4 tab_s[];  // [S][4]
+  __shared__ uint32_t stage_i[kWWarps][kWT * 32 + 2];
+  __shared__ uint32_t stage_r[kWWarps][kWT * 8 + 2];
+
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t row = blockIdx.y;
+  const int h = (int)(row % p.H);
+  const int S = p.S, w = p.w, br = p.br;
+  const float4* __restrict__ rot = p.rot + (int64_t)h * S * 4;
+  const double* __restrict__ joint = p.joint + (int64_t)h * kGroupOrder * S * 4;
+  for (int i = threadIdx.x; i < S * 4; i += kWThreads) tab_s[i] = __ldg(rot + i);
+  for (int i = lane; i < kWT * 32 + 2; i += 32) stage_i[warp][i] = 0u;
+  for (int i = lane; i < kWT * 8 + 2; i += 32) stage_r[warp][i] = 0u;
+  __syncthreads();
+
+  const double top = (double)((1 << br) - 1);
+  const double thr = p.groups ? p.groups[p.per_head ? h : 0].threshold : INFINITY;
+  const int64_t ntiles = ceil_div(p.T, kWT);
+  const int64_t stride = (int64_t)gridDim.x * kWWarps;
+  const InT* __restrict__ data = reinterpret_cast<const InT*>(p.data);
+  const uint32_t lanemask_lt = (1u << lane) - 1u;
+  uint32_t* __restrict__ st_i = stage_i[warp];
+  uint32_t* __restrict__ st_r = stage_r[warp];
+  const bool ext = p.tokoff != nullptr;
+
+  auto load_tile = [&](int64_t wt, uint2 (&raw)[kWT]) {
+#pragma unroll
+    for (int j = 0; j < kWT; ++j) {
+      const int64_t t = wt * kWT + j;
+      raw[j] = make_uint2(0u, 0u);
+      if (wt < ntiles && t < p.T)
+        raw[j] = __ldg(reinterpret_cast<const uint2*>(data + (row * p.T + t) * 128) + lane);
+    }
+  };
+
+  int64_t wt = (int64_t)blockIdx.x * kWWarps + warp;
+  uint2 raw[kWT];
+  load_tile(wt, raw);
+  for (; wt < ntiles; wt += stride) {
+    uint2 nxt[kWT];
+    load_tile(wt + stride, nxt);  // prefetch: latency hidden behind the S-loop
+    const int64_t t0 = wt * kWT;
+    const int ntok = (int)min((int64_t)kWT, p.T - t0);
+    const int64_t tok0 = row * p.T + t0;
+    const uint64_t P0 = ext ? (uint64_t)p.tokoff[tok0] : (uint64_t)tok0 * 32;
+
+    // ---- exact fp64 prologue: norms, flags, scales, quanta, payloads, fp32 dirs
+    uint32_t fmask[kWT];
+    uint32_t qpack = 0, livebits = 0, coded_run = 0;
+    float4 u4[kWT];
+#pragma unroll
+    for (int j = 0; j < kWT; ++j) {
+      const InT* v = reinterpret_cast<const InT*>(&raw[j]);
+      InT vv[4] = {v[0], v[1], v[2], v[3]};
+      double x[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) x[i] = In<InT>::d(vv[i]);
+      const double r = exact_norm(x);
+      const bool valid = j < ntok;
+      const bool fl = valid && r > thr;
+      fmask[j] = __ballot_sync(0xffffffffu, fl);
+      const bool live = valid && !fl && r > 0.0;
+      double sg = warp_max_f64(fl ? 0.0 : r);
+      if (!(sg > 0.0)) sg = 1.0;
+      const __half hs = __double2half(sg);
+      const double sw = (double)__half2float(hs);
+      if (valid && lane == j) {
+        p.scales[tok0 + j] = __half_as_ushort(hs);
+        if (!(sw > 0.0)) atomicOr(p.err, HQMQ_DEVERR_SIGMA_NONPOSITIVE);
+      }
+      if (valid && !fl) qpack |= exact_quantum(r, sw, top) << (8 * j);
+      livebits |= (live ? 1u : 0u) << j;
+      u4[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (live) {
+        const Dir2 d = fast_dir(vv, x, r);
+        u4[j] = make_float4(d.a.x, d.b.x, d.c.x, d.d.x);
+      }
+      if (ext && valid) {
+        if (fl) {
+          const uint64_t rel = coded_run + __popc(~fmask[j] & lanemask_lt);
+          const uint64_t prow = (uint64_t)(tok0 + j) * 32 + lane - (P0 + rel);
+          if (prow < (uint64_t)p.payload_capacity) {
+            ushort4 hv;
+            hv.x = __half_as_ushort(__double2half(x[0]));
+            hv.y = __half_as_ushort(__double2half(x[1]));
+            hv.z = __half_as_ushort(__double2half(x[2]));
+            hv.w = __half_as_ushort(__double2half(x[3]));
+            reinterpret_cast<ushort4*>(p.payloads)[prow] = hv;
+          }
+        }
+        if (lane == j) p.flagw[tok0 + j] = fmask[j];
+        coded_run += __popc(~fmask[j]);
+      }
+    }
+
+    // ---- fp32 closed-form search over the S cosets (table broadcast from smem)
+    float best[kWT], second[kWT];
+    int bs[kWT];
+#pragma unroll
+    for (int j = 0; j < kWT; ++j) {
+      best[j] = -1.f;
+      second[j] = -1.f;
+      bs[j] = 0;
+    }
+#pragma unroll 2
+    for (int s = 0; s < S; ++s) {
+      const float4 a0 = tab_s[4 * s + 0], a1 = tab_s[4 * s + 1];
+      const float4 a2 = tab_s[4 * s + 2], a3 = tab_s[4 * s + 3];
+#pragma unroll
+      for (int j = 0; j < kWT; ++j) {
+        Dir2 d;
+        d.a = make_float2(u4[j].x, u4[j].x);
+        d.b = make_float2(u4[j].y, u4[j].y);
+        d.c = make_float2(u4[j].z, u4[j].z);
+        d.d = make_float2(u4[j].w, u4[j].w);
+        float2 wx, yz;
+        rotate(d, a0, a1, a2, a3, wx, yz);
+        const float sc = coset_score(wx, yz);
+        const bool gt = sc > best[j];
+        second[j] = fmaxf(second[j], fminf(sc, best[j]));
+        best[j] = fmaxf(best[j], sc);
+        bs[j] = gt ? s : bs[j];
+      }
+    }
+
+    // ---- certification + warp-cooperative exact fixup (input re-read from L2)
+    int idx[kWT];
+#pragma unroll
+    for (int j = 0; j < kWT; ++j) {
+      idx[j] = 0;
+      bool unsure = false;
+      if ((livebits >> j) & 1u) {
+        const int s = bs[j];
+        Dir2 d;
+        d.a = make_float2(u4[j].x, u4[j].x);
+        d.b = make_float2(u4[j].y, u4[j].y);
+        d.c = make_float2(u4[j].z, u4[j].z);
+        d.d = make_float2(u4[j].w, u4[j].w);
+        float2 wx, yz;
+        rotate(d, tab_s[4 * s], tab_s[4 * s + 1], tab_s[4 * s + 2], tab_s[4 * s + 3], wx, yz);
+        int pidx;
+        float top32, within;
+        coset_resolve(wx, yz, pidx, top32, within);
+        idx[j] = pidx * S + s;
+        unsure = !(best[j] - fmaxf(second[j], within) > kDelta);
+      }
+      uint32_t um = __ballot_sync(0xffffffffu, unsure);
+      if (um && lane == 0)
+        atomicAdd(reinterpret_cast<unsigned long long*>(p.counters + 2),
+                  (unsigned long long)__popc(um));
+      while (um) {
+        const int L = __ffs(um) - 1;
+        um &= um - 1;
+        const uint2 rw = __ldg(reinterpret_cast<const uint2*>(data + (tok0 + j) * 128) + L);
+        const InT* v = reinterpret_cast<const InT*>(&rw);
+        InT vv[4] = {v[0], v[1], v[2], v[3]};
+        double x[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) x[i] = In<InT>::d(vv[i]);
+        const double rl = exact_norm(x);
+        const Dir2 ud = fast_dir(vv, x, rl);
+        const int ex = warp_exact_index(x, rl, ud, tab_s, joint, S, lane);
+        if (lane == L) idx[j] = ex;
+      }
+    }
+
+    // ---- pack the index / radius streams
+    uint32_t coded_before = 0;
+    const uint32_t lbi = (uint32_t)((P0 * (uint64_t)w) & 31);
+    const uint32_t lbr = (uint32_t)((P0 * (uint64_t)br) & 31);
+#pragma unroll
+    for (int j = 0; j < kWT; ++j) {
+      if (j >= ntok) continue;
+      const bool fl = (fmask[j] >> lane) & 1u;
+      const uint32_t rel = coded_before + __popc(~fmask[j] & lanemask_lt);
+      if (!fl) {
+        stage_bits(st_i, (uint64_t)lbi + (uint64_t)rel * w, (uint32_t)idx[j], w);
+        stage_bits(st_r, (uint64_t)lbr + (uint64_t)rel * br, (qpack >> (8 * j)) & 0xffu, br);
+      }
+      coded_before += __popc(~fmask[j]);
+    }
+    __syncwarp();
+    {
+      // no extraction: words are token-aligned and fully owned -> plain stores;
+      // with extraction the two edge words may be shared with neighbours -> OR.
+      const uint64_t end = lbi + (uint64_t)coded_before * w;
+      const uint32_t nw = (uint32_t)((end + 31) >> 5);
+      const uint64_t gw0 = (P0 * (uint64_t)w) >> 5;
+      for (uint32_t i = lane; i < nw; i += 32) {
+        const uint32_t word = st_i[i];
+        const bool owned = (i > 0 || lbi == 0) && (i + 1 < nw || (end & 31) == 0);
+        if (owned) p.idxw[gw0 + i] = word;
+        else if (word) atomicOr(p.idxw + gw0 + i, word);
+        st_i[i] = 0u;
+      }
+    }
+    {
+      const uint64_t end = lbr + (uint64_t)coded_before * br;
+      const uint32_t nw = (uint32_t)((end + 31) >> 5);
+      const uint64_t gw0 = (P0 * (uint64_t)br) >> 5;
+      for (uint32_t i = lane; i < nw; i += 32) {
+        const uint32_t word = st_r[i];
+        const bool owned = (i > 0 || lbr == 0) && (i + 1 < nw || (end & 31) == 0);
+        if (owned) p.radw[gw0 + i] = word;
+        else if (word) atomicOr(p.radw + gw0 + i, word);
+        st_r[i] = 0u;
+      }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int j = 0; j < kWT; ++j) raw[j] = nxt[j];
+  }
+}
+
+// Per-token coded (unflagged) chunk count from the stored norms (C = 32).
+__global__ void token_coded_norms_kernel(const double* __restrict__ norms,
+                                         const RadixGroup* groups, int64_t H, int64_t T,
+                                         int64_t n_tok, int per_head, uint32_t* cnt) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n_tok;
+       t += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t row = t / T;
+    const double thr = groups[per_head ? (int)(row % H) : 0].threshold;
+    const double2* nr = reinterpret_cast<const double2*>(norms + t * 32);
+    uint32_t c = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const double2 v = nr[k];
+      c += (v.x > thr ? 0u : 1u) + (v.y > thr ? 0u : 1u);
+    }
+    cnt[t] = c;
+  }
+}
+
 // ------------------------------------------------------ Med3x radix select
 struct RadixParams {
   int64_t B, H, T, D;
@@ -630,9 +883,17 @@ namespace {
 struct Layout {
   int64_t n_chunks = 0, rows = 0, n_tiles = 0, tiles_per_row = 0;
   int C = 0, TT = 0, G = 0;
+  bool warp_path = false;
   size_t off_norms = 0, off_groups = 0, off_hist = 0, off_done = 0, off_counts = 0,
          off_prefix = 0, off_cub = 0, cub_bytes = 0, total = 0;
 };
+
+// The barrier-free warp kernel covers the model shapes: head_dim 128 with
+// 2-byte inputs and the whole rotation table resident in shared memory.
+bool use_warp_path(const hqmq_encode_args* a) {
+  return a->head_dim == 128 && (a->input_dtype == HQMQ_F16 || a->input_dtype == HQMQ_BF16) &&
+         a->codebook_size <= kSBlock && (reinterpret_cast<uintptr_t>(a->data) % 8) == 0;
+}
 
 size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
@@ -646,6 +907,9 @@ bool plan(const hqmq_encode_args* a, Layout& L) {
   L.tiles_per_row = ceil_div(a->tokens, L.TT);
   L.n_tiles = L.rows * L.tiles_per_row;
   L.G = a->per_head_pooling ? (int)a->heads : 1;
+  L.warp_path = use_warp_path(a);
+  // prefix granularity: per token on the warp path, per tile otherwise
+  const int64_t n_pre = L.warp_path ? L.rows * a->tokens : L.n_tiles;
   size_t off = 0;
   const bool ext = a->outlier_multiplier > 0.0;
   if (ext) {
@@ -658,12 +922,12 @@ bool plan(const hqmq_encode_args* a, Layout& L) {
     L.off_done = off;
     off = align_up(off + 16, 256);
     L.off_counts = off;
-    off = align_up(off + (size_t)L.n_tiles * 4, 256);
+    off = align_up(off + (size_t)n_pre * 4, 256);
     L.off_prefix = off;
-    off = align_up(off + (size_t)L.n_tiles * 4, 256);
+    off = align_up(off + (size_t)n_pre * 4, 256);
     size_t cub_bytes = 0;
     cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, (const uint32_t*)nullptr,
-                                  (uint32_t*)nullptr, (int)std::max<int64_t>(L.n_tiles, 1));
+                                  (uint32_t*)nullptr, (int)std::max<int64_t>(n_pre, 1));
     L.off_cub = off;
     L.cub_bytes = cub_bytes;
     off = align_up(off + cub_bytes, 256);
@@ -681,9 +945,14 @@ int launch_encode(const hqmq_encode_args* a, const Layout& L, cudaStream_t st) {
   const bool aligned4 = (a->head_dim % 4) == 0 &&
                         (reinterpret_cast<uintptr_t>(a->data) % (4 * sizeof(InT))) == 0;
   cudaError_t e;
-  if (a->index_capacity_words) cudaMemsetAsync(a->index_words, 0, a->index_capacity_words * 4, st);
-  if (a->radius_capacity_words) cudaMemsetAsync(a->radius_words, 0, a->radius_capacity_words * 4, st);
-  if (a->flag_words && a->flag_capacity_words)
+  // The warp path writes every word of a token-aligned stream (no extraction)
+  // and every flag word; only OR-ed edge words need a zeroed destination.
+  const bool need_zero = !L.warp_path || ext;
+  if (need_zero && a->index_capacity_words)
+    cudaMemsetAsync(a->index_words, 0, a->index_capacity_words * 4, st);
+  if (need_zero && a->radius_capacity_words)
+    cudaMemsetAsync(a->radius_words, 0, a->radius_capacity_words * 4, st);
+  if (!L.warp_path && a->flag_words && a->flag_capacity_words)
     cudaMemsetAsync(a->flag_words, 0, a->flag_capacity_words * 4, st);
   cudaMemsetAsync(a->counters, 0, 3 * sizeof(int64_t), st);
   if (L.n_chunks == 0) {
@@ -713,13 +982,27 @@ int launch_encode(const hqmq_encode_args* a, const Layout& L, cudaStream_t st) {
       radix_hist_kernel<InT><<<hgrid, kHistThreads, 0, st>>>(rp);
     }
     uint32_t* counts = reinterpret_cast<uint32_t*>(ws + L.off_counts);
-    prefix = reinterpret_cast<uint32_t*>(ws + L.off_prefix);
-    tile_count_kernel<<<dim3((unsigned)L.tiles_per_row, (unsigned)L.rows), 256, 0, st>>>(
-        rp.norms, groups, a->heads, a->tokens, L.C, L.TT, L.tiles_per_row,
-        a->per_head_pooling, counts);
     size_t cub_bytes = L.cub_bytes;
-    cub::DeviceScan::ExclusiveSum(ws + L.off_cub, cub_bytes, counts, prefix, (int)L.n_tiles, st);
-    finalize_counts_kernel<<<1, 32, 0, st>>>(counts, prefix, L.n_tiles, L.n_chunks, a->counters);
+    if (L.warp_path) {
+      // per-token coded counts -> exclusive scan straight into token_offsets
+      const int64_t n_tok = L.rows * a->tokens;
+      token_coded_norms_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n_tok, 256), 148 * 16), 256,
+                                 0, st>>>(rp.norms, groups, a->heads, a->tokens, n_tok,
+                                          a->per_head_pooling, counts);
+      cub::DeviceScan::ExclusiveSum(ws + L.off_cub, cub_bytes, counts, a->token_offsets,
+                                    (int)n_tok, st);
+      finalize_counts_kernel<<<1, 32, 0, st>>>(counts, a->token_offsets, n_tok, L.n_chunks,
+                                               a->counters);
+    } else {
+      prefix = reinterpret_cast<uint32_t*>(ws + L.off_prefix);
+      tile_count_kernel<<<dim3((unsigned)L.tiles_per_row, (unsigned)L.rows), 256, 0, st>>>(
+          rp.norms, groups, a->heads, a->tokens, L.C, L.TT, L.tiles_per_row,
+          a->per_head_pooling, counts);
+      cub::DeviceScan::ExclusiveSum(ws + L.off_cub, cub_bytes, counts, prefix, (int)L.n_tiles,
+                                    st);
+      finalize_counts_kernel<<<1, 32, 0, st>>>(counts, prefix, L.n_tiles, L.n_chunks,
+                                               a->counters);
+    }
   } else {
     set_counts_kernel<<<1, 32, 0, st>>>(L.n_chunks, a->counters);
   }
@@ -739,6 +1022,23 @@ int launch_encode(const hqmq_encode_args* a, const Layout& L, cudaStream_t st) {
   p.tokoff = ext ? a->token_offsets : nullptr;
   p.counters = a->counters; p.err = a->error_word;
   const size_t smem = (size_t)std::min(a->codebook_size, kSBlock) * 4 * sizeof(float4);
+  if constexpr (sizeof(InT) == 2) {
+    if (L.warp_path) {
+      static thread_local bool wattr[2] = {false, false};
+      const int wi = std::is_same<InT, __half>::value ? 0 : 1;
+      if (!wattr[wi]) {
+        cudaFuncSetAttribute(encode_warp_kernel<InT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             kSBlock * 4 * (int)sizeof(float4));
+        wattr[wi] = true;
+      }
+      const int64_t ntiles = ceil_div(a->tokens, kWT);
+      const int64_t want = ceil_div(148 * 3, L.rows);
+      const int64_t bx = std::max<int64_t>(1, std::min<int64_t>(want, ceil_div(ntiles, kWWarps)));
+      encode_warp_kernel<InT><<<dim3((unsigned)bx, (unsigned)L.rows), kWThreads, smem, st>>>(p);
+      e = cudaGetLastError();
+      return e == cudaSuccess ? HQMQ_OK : cuda_fail(e);
+    }
+  }
   static thread_local bool attr_set[4] = {false, false, false, false};
   const int ti = sizeof(InT) == 2 ? (std::is_same<InT, __half>::value ? 0 : 1) : (sizeof(InT) == 4 ? 2 : 3);
   if (!attr_set[ti]) {
