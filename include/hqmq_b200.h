@@ -212,7 +212,9 @@ typedef struct {
   hqmq_packed_view k, v;
   float* out;
   int32_t num_splits; /* 0 = choose automatically */
-  int32_t _pad0;
+  int32_t precise;    /* 1: fp32 CUDA-core path (|err| <= 2e-5 vs fp64);
+                         0: fp16 tensor-core path (|err| <= 1e-3, the reference's
+                         fp32 tolerance, test_attention.py:97-102) */
   void* workspace;
   size_t workspace_bytes;
 } hqmq_attention_args;

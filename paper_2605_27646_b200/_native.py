@@ -74,7 +74,7 @@ class AttentionArgs(ctypes.Structure):
         ("causal", c_i32),
         ("scale", ctypes.c_double),
         ("q", c_vp), ("k", PackedView), ("v", PackedView), ("out", c_vp),
-        ("num_splits", c_i32), ("_pad0", c_i32),
+        ("num_splits", c_i32), ("precise", c_i32),
         ("workspace", c_vp), ("workspace_bytes", ctypes.c_size_t),
     ]
 

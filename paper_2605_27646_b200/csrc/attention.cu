@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <cmath>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -240,6 +241,375 @@ __global__ void combine_kernel(AttParams p) {
   }
 }
 
+// ------------------------------------------------------------------------
+// Tensor-core fast path (head_dim 128, no outlier extraction, <= 8 query rows
+// per kv head, i.e. decode with GQA group <= 8) — warp-independent
+// flash-decoding inside the CTA:
+//   * 128-key tiles of the K and V sections (index / radius words and fp16
+//     scales) stream into a kMStages-deep shared ring with cp.async.bulk; a
+//     full mbarrier per stage signals arrival, and the last warp to release a
+//     stage (shared-memory counter) issues that stage's next tile;
+//   * consumer warp w owns keys [16w, 16w+16) of every tile: it decodes its K
+//     rows into a private fp16 tile (lane = chunk; half2 radius x codeword from
+//     fp16 copies of the joint tables), runs S = Q K^T on mma.sync.m16n8k16
+//     (query rows on M, padded to 16; keys on N), updates its own online
+//     softmax, decodes its V rows into the same buffer and runs O += P V with
+//     the S accumulators reused as the P operand (no block barriers);
+//   * at the end the 8 warps' (m, l, O) are merged through shared memory.
+constexpr int kMT = 128;          // keys per CTA tile (8 warps x 16)
+constexpr int kMStages = 3;
+constexpr int kKVStride = 136;    // halves per smem row: 128 + 8 (conflict-free ldmatrix)
+constexpr int kMConsumers = 8;
+constexpr int kMThreads = kMConsumers * 32;
+
+struct RingGeom {
+  uint32_t ki, kr, ks, vi, vr, vs, bytes;
+};
+
+__host__ __device__ inline RingGeom ring_geom(int w, int br) {
+  auto up = [](uint32_t x) { return (x + 127u) / 128u * 128u; };
+  RingGeom g;
+  uint32_t o = 0;
+  g.ki = o; o += up(kMT * w * 4 + 16);
+  g.kr = o; o += up(kMT * br * 4 + 16);
+  g.ks = o; o += up(kMT * 2);
+  g.vi = o; o += up(kMT * w * 4 + 16);
+  g.vr = o; o += up(kMT * br * 4 + 16);
+  g.vs = o; o += up(kMT * 2);
+  g.bytes = o;
+  return g;
+}
+
+__host__ __device__ inline size_t mma_smem_bytes(int S, int w, int br) {
+  const size_t tab = 2 * (size_t)kGroupOrder * S * 8;
+  const size_t ring = kMStages * (size_t)ring_geom(w, br).bytes;
+  const size_t merge = (size_t)kMConsumers * 8 * 130 * 4;  // O + (m, l) per warp/row
+  return tab + (ring > merge ? ring : merge) + (size_t)kMConsumers * 16 * kKVStride * 2;
+}
+
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* ptr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(smem_u32(ptr)));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], const void* ptr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(smem_u32(ptr)));
+}
+// D(16x8 fp32) += A(16x16 fp16, rows 8-15 zero) * B(16x8 fp16)
+__device__ __forceinline__ void mma_rows8(float (&d)[4], uint32_t a0, uint32_t a2, uint32_t b0,
+                                          uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
+  const __half2 h = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Decode 16 key rows (tokens tt0..tt0+15 of the staged tile) of one tensor into
+// a [16][kKVStride] fp16 tile of quantum x codeword (lane = chunk).  The
+// per-key scale sigma/top is NOT applied here: it is constant per key, so the
+// caller folds it into S (K) and into P (V) after the MMAs.  W / BR are
+// compile-time so every stream offset is an immediate; rows are processed in
+// batches of 8 with all shared loads issued before the dependent math.
+template <int W, int BR>
+__device__ __forceinline__ void decode_rows16(const uint32_t* __restrict__ iw,
+                                              const uint32_t* __restrict__ rw,
+                                              const uint2* __restrict__ tab,
+                                              __half* __restrict__ dst, int tt0, int nvalid,
+                                              int lane) {
+  constexpr uint32_t kIMask = W == 32 ? 0xffffffffu : ((1u << W) - 1u);
+  constexpr uint32_t kRMask = (1u << BR) - 1u;
+  const uint32_t lwi = (uint32_t)lane * W, lwr = (uint32_t)lane * BR;
+  const uint32_t ish = lwi & 31, rsh = lwr & 31;
+  const uint32_t* __restrict__ ip = iw + tt0 * W + (lwi >> 5);
+  const uint32_t* __restrict__ rp = rw + tt0 * BR + (lwr >> 5);
+  __half* __restrict__ dp = dst + 4 * lane;
+#pragma unroll
+  for (int j0 = 0; j0 < 16; j0 += 8) {
+    uint32_t idx[8], q[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int jj = j0 + j;
+      idx[j] = __funnelshift_r(ip[jj * W], ip[jj * W + 1], ish) & kIMask;
+      if constexpr (32 % BR == 0) q[j] = (rp[jj * BR] >> rsh) & kRMask;
+      else q[j] = __funnelshift_r(rp[jj * BR], rp[jj * BR + 1], rsh) & kRMask;
+    }
+    uint2 cw[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) cw[j] = tab[idx[j]];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int jj = j0 + j;
+      const __half2 h = __half2half2(__uint2half_rn(q[j]));
+      const __half2 e0 = __hmul2(h, *reinterpret_cast<const __half2*>(&cw[j].x));
+      const __half2 e1 = __hmul2(h, *reinterpret_cast<const __half2*>(&cw[j].y));
+      uint2 out = make_uint2(*reinterpret_cast<const uint32_t*>(&e0),
+                             *reinterpret_cast<const uint32_t*>(&e1));
+      if (jj >= nvalid) out = make_uint2(0u, 0u);
+      *reinterpret_cast<uint2*>(dp + jj * kKVStride) = out;
+    }
+  }
+}
+
+template <int W, int BR>
+__global__ void __launch_bounds__(kMThreads, 2) attention_mma_kernel(AttParams p) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  __shared__ __align__(8) uint64_t full[kMStages];
+  __shared__ unsigned int released[kMStages];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int ncw = kGroupOrder * p.S;
+  constexpr int w = W, br = BR;
+  const RingGeom gm = ring_geom(w, br);
+  uint2* ktab = reinterpret_cast<uint2*>(sm);
+  uint2* vtab = ktab + ncw;
+  unsigned char* ring = reinterpret_cast<unsigned char*>(vtab + ncw);
+  const size_t ring_bytes = kMStages * (size_t)gm.bytes;
+  const size_t merge_bytes = (size_t)kMConsumers * 8 * 130 * 4;
+  __half* kvbuf = reinterpret_cast<__half*>(ring + (ring_bytes > merge_bytes ? ring_bytes : merge_bytes));
+
+  const int64_t bh = blockIdx.y;
+  const int64_t b = bh / p.Hkv, hkv = bh % p.Hkv;
+  const int64_t kbeg = (int64_t)blockIdx.x * p.keys_per_split;
+  const int64_t kend = min(p.Tkv, kbeg + p.keys_per_split);
+  const int64_t ntile = kend > kbeg ? ceil_div(kend - kbeg, kMT) : 0;
+  const int64_t tokrow = bh * p.Tkv;
+
+  if (tid == 0) {
+    for (int s = 0; s < kMStages; ++s) {
+      mbar_init(&full[s], 1);
+      released[s] = 0u;
+    }
+    fence_mbar_init();
+  }
+  const float4* gk = p.k.table + hkv * ncw;
+  const float4* gv = p.v.table + hkv * ncw;
+  for (int i = tid; i < ncw; i += kMThreads) {
+    const float4 a = __ldg(gk + i), c = __ldg(gv + i);
+    ktab[i] = make_uint2(pack_half2(a.x, a.y), pack_half2(a.z, a.w));
+    vtab[i] = make_uint2(pack_half2(c.x, c.y), pack_half2(c.z, c.w));
+  }
+  __syncthreads();
+
+  const int g4 = lane >> 2, t4 = lane & 3;  // mma fragment coordinates
+  float m_run = -INFINITY, l_run = 0.f;
+  // O^T accumulators: m-tile md covers dims 16md..16md+15; c0/c1 = (dim 16md+g4,
+  // rows 2t4 / 2t4+1), c2/c3 = (dim 16md+g4+8, rows 2t4 / 2t4+1)
+  float oT[8][4];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) oT[i][0] = oT[i][1] = oT[i][2] = oT[i][3] = 0.f;
+
+  auto issue = [&](int64_t k, int stage) {
+    const int64_t t = tokrow + kbeg + k * kMT;
+    const int ntok = (int)min((int64_t)kMT, kend - (kbeg + k * kMT));
+    unsigned char* s = ring + (size_t)stage * gm.bytes;
+    const uint32_t ib = ntok * w * 4, rb = ntok * br * 4, sb = ntok * 2;
+    fence_proxy_async();
+    mbar_arrive_expect_tx(&full[stage], 2 * (ib + rb + sb));
+    bulk_g2s(s + gm.ki, p.k.idxw + t * w, ib, &full[stage]);
+    bulk_g2s(s + gm.kr, p.k.radw + t * br, rb, &full[stage]);
+    bulk_g2s(s + gm.ks, p.k.scales + t, sb, &full[stage]);
+    bulk_g2s(s + gm.vi, p.v.idxw + t * w, ib, &full[stage]);
+    bulk_g2s(s + gm.vr, p.v.radw + t * br, rb, &full[stage]);
+    bulk_g2s(s + gm.vs, p.v.scales + t, sb, &full[stage]);
+  };
+  // release a stage; the last of the 8 warps refills it with tile k + kMStages
+  auto release = [&](int64_t k, int stage) {
+    if (lane == 0) {
+      if (atomicAdd(&released[stage], 1u) == kMConsumers - 1) {
+        released[stage] = 0u;
+        if (k + kMStages < ntile) issue(k + kMStages, stage);
+      }
+    }
+  };
+  if (tid == 0)
+    for (int s = 0; s < kMStages && s < ntile; ++s) issue(s, s);
+  {
+    // ---------------- consumers
+    // Q A-fragments (rows x dims, rows 8..15 zero): qa[ks] = {a0, a2}
+    uint32_t qa[8][2];
+    const bool row_valid = g4 < p.nrows;
+    {
+      const int gi = row_valid ? g4 / (int)p.Tq : 0, qi = row_valid ? g4 - gi * (int)p.Tq : 0;
+      const float* qrow = p.q + ((b * p.Hq + hkv * p.g + gi) * p.Tq + qi) * 128;
+#pragma unroll
+      for (int ks = 0; ks < 8; ++ks) {
+        const int d = ks * 16 + t4 * 2;
+        float v0 = 0.f, v1 = 0.f, v8 = 0.f, v9 = 0.f;
+        if (row_valid) {
+          v0 = qrow[d] * p.scale_log2; v1 = qrow[d + 1] * p.scale_log2;
+          v8 = qrow[d + 8] * p.scale_log2; v9 = qrow[d + 9] * p.scale_log2;
+        }
+        qa[ks][0] = pack_half2(v0, v1);
+        qa[ks][1] = pack_half2(v8, v9);
+      }
+    }
+    int64_t vis = p.Tkv;  // keys j < vis are visible to row g4
+    if (row_valid && p.causal) vis = (g4 % (int)p.Tq) + (p.Tkv - p.Tq) + 1;
+    const float rtop = 1.0f / (float)((1 << br) - 1);
+    __half* mybuf = kvbuf + warp * 16 * kKVStride;
+
+    for (int64_t k = 0; k < ntile; ++k) {
+      const int stage = (int)(k % kMStages);
+      mbar_wait(&full[stage], (uint32_t)((k / kMStages) & 1));
+      const unsigned char* s = ring + (size_t)stage * gm.bytes;
+      const int64_t t0 = kbeg + k * kMT + warp * 16;  // this warp's first key
+      const int nvalid = (int)max((int64_t)0, min((int64_t)16, kend - t0));
+      if (nvalid > 0) {
+        // ---- K rows -> fp16 tile, S = Q K^T (two 8-key n-tiles)
+        decode_rows16<W, BR>(reinterpret_cast<const uint32_t*>(s + gm.ki),
+                             reinterpret_cast<const uint32_t*>(s + gm.kr), ktab, mybuf, warp * 16,
+                             nvalid, lane);
+        // per-key scales sigma/top of the 4 keys this thread's fragments touch
+        float kst[4], vst[4];
+        {
+          const uint16_t* ks = reinterpret_cast<const uint16_t*>(s + gm.ks) + warp * 16;
+          const uint16_t* vs = reinterpret_cast<const uint16_t*>(s + gm.vs) + warp * 16;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int key = (e >> 1) * 8 + t4 * 2 + (e & 1);
+            kst[e] = __half2float(__ushort_as_half(ks[key])) * rtop;
+            vst[e] = __half2float(__ushort_as_half(vs[key])) * rtop;
+          }
+        }
+        __syncwarp();
+        float sc[2][4];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk) {  // two k-steps per ldmatrix.x4
+            uint32_t bf[4];
+            ldsm_x4(bf, mybuf + (nt * 8 + (lane & 7)) * kKVStride + kk * 32 + (lane >> 3) * 8);
+            mma_rows8(sc[nt], qa[2 * kk][0], qa[2 * kk][1], bf[0], bf[1]);
+            mma_rows8(sc[nt], qa[2 * kk + 1][0], qa[2 * kk + 1][1], bf[2], bf[3]);
+          }
+        }
+        // ---- online softmax for row g4 over this warp's 16 keys (log2 domain)
+        float sv[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int nt = e >> 1;
+          const int64_t key = t0 + nt * 8 + t4 * 2 + (e & 1);
+          const bool ok = row_valid && key < kend && key < vis;
+          sv[e] = ok ? sc[nt][e & 1] * kst[e] : -INFINITY;
+        }
+        float mx = fmaxf(fmaxf(sv[0], sv[1]), fmaxf(sv[2], sv[3]));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        const float m_new = fmaxf(m_run, mx);
+        float pe[4], alpha = 1.f;
+        if (m_new == -INFINITY) {
+          pe[0] = pe[1] = pe[2] = pe[3] = 0.f;
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) pe[e] = sv[e] == -INFINITY ? 0.f : exp2f(sv[e] - m_new);
+          alpha = m_run == -INFINITY ? 0.f : exp2f(m_run - m_new);
+        }
+        float ps = (pe[0] + pe[1]) + (pe[2] + pe[3]);
+        ps += __shfl_xor_sync(0xffffffffu, ps, 1);
+        ps += __shfl_xor_sync(0xffffffffu, ps, 2);
+        l_run = l_run * alpha + ps;
+        m_run = m_new;
+        // rescale: this thread's O^T columns are rows 2t4 and 2t4+1, whose
+        // softmax state lives in lanes 8t4 and 8t4+4
+        const float a_lo = __shfl_sync(0xffffffffu, alpha, t4 * 8);
+        const float a_hi = __shfl_sync(0xffffffffu, alpha, t4 * 8 + 4);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          oT[i][0] *= a_lo; oT[i][1] *= a_hi; oT[i][2] *= a_lo; oT[i][3] *= a_hi;
+        }
+        // P^T (keys x rows) B-fragments straight from the S accumulators,
+        // with the V per-key scale sigma/top folded in
+        const uint32_t pb0 = pack_half2(pe[0] * vst[0], pe[1] * vst[1]);
+        const uint32_t pb1 = pack_half2(pe[2] * vst[2], pe[3] * vst[3]);
+        __syncwarp();
+        // ---- V rows -> same fp16 tile, O^T += V^T P^T (8 dim m-tiles)
+        decode_rows16<W, BR>(reinterpret_cast<const uint32_t*>(s + gm.vi),
+                             reinterpret_cast<const uint32_t*>(s + gm.vr), vtab, mybuf, warp * 16,
+                             nvalid, lane);
+        __syncwarp();
+        release(k, stage);
+#pragma unroll
+        for (int md = 0; md < 8; ++md) {
+          uint32_t af[4];
+          ldsm_x4_t(af, mybuf + ((lane & 7) + (lane >> 4) * 8) * kKVStride + md * 16 +
+                            ((lane >> 3) & 1) * 8);
+          asm volatile(
+              "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+              "{%8,%9}, {%0,%1,%2,%3};"
+              : "+f"(oT[md][0]), "+f"(oT[md][1]), "+f"(oT[md][2]), "+f"(oT[md][3])
+              : "r"(af[0]), "r"(af[1]), "r"(af[2]), "r"(af[3]), "r"(pb0), "r"(pb1));
+        }
+        __syncwarp();
+      } else {
+        release(k, stage);
+      }
+    }
+  }
+  // every consumer is past its last read of the ring (and no bulk copy is in
+  // flight: each issued tile was consumed) -> reuse the ring for the merge
+  __syncthreads();
+  {
+    float* mo = reinterpret_cast<float*>(ring);  // [warp][row][130]
+#pragma unroll
+    for (int md = 0; md < 8; ++md) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int row = t4 * 2 + (e & 1);
+        const int dim = md * 16 + g4 + (e >> 1) * 8;
+        mo[((size_t)warp * 8 + row) * 130 + dim] = oT[md][e];
+      }
+    }
+    if (t4 == 0) {
+      mo[((size_t)warp * 8 + g4) * 130 + 128] = m_run;
+      mo[((size_t)warp * 8 + g4) * 130 + 129] = l_run;
+    }
+  }
+  __syncthreads();
+  // ---- merge the consumers' (m, l, O) and write
+  const float* mo = reinterpret_cast<const float*>(ring);
+  for (int i = tid; i < 8 * 128; i += kMThreads) {
+    const int r = i >> 7, d = i & 127;
+    if (r >= p.nrows) continue;
+    float M = -INFINITY;
+#pragma unroll
+    for (int ww = 0; ww < kMConsumers; ++ww) M = fmaxf(M, mo[((size_t)ww * 8 + r) * 130 + 128]);
+    float L = 0.f, O = 0.f;
+    if (M != -INFINITY) {
+#pragma unroll
+      for (int ww = 0; ww < kMConsumers; ++ww) {
+        const float* st = mo + ((size_t)ww * 8 + r) * 130;
+        if (st[128] != -INFINITY) {
+          const float f = exp2f(st[128] - M);
+          L += st[129] * f;
+          O += st[d] * f;
+        }
+      }
+    }
+    const int gi = r / (int)p.Tq, qi = r - gi * (int)p.Tq;
+    const int64_t hq = hkv * p.g + gi;
+    if (p.splits == 1) {
+      p.out[((b * p.Hq + hq) * p.Tq + qi) * 128 + d] = O / L;
+    } else {
+      const int64_t idx = (bh * p.nrows + r) * p.splits + blockIdx.x;
+      p.part_o[idx * 128 + d] = O;
+      if (d == 0) {
+        p.part_ml[2 * idx] = M;
+        p.part_ml[2 * idx + 1] = L;
+      }
+    }
+  }
+}
+
 namespace {
 
 struct AttPlan {
@@ -266,7 +636,7 @@ bool plan_att(const hqmq_attention_args* a, AttPlan& pl) {
     splits = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(target, ctas),
                                                            ceil_div(a->kv_tokens, 256)));
   }
-  pl.keys_per_split = ceil_div(ceil_div(a->kv_tokens, splits), kKT) * kKT;
+  pl.keys_per_split = ceil_div(ceil_div(a->kv_tokens, splits), 64) * 64;
   pl.splits = (int)ceil_div(a->kv_tokens, pl.keys_per_split);
   const int64_t parts = a->batch * a->kv_heads * nrows * pl.splits;
   pl.ws = pl.splits > 1 ? (size_t)parts * (a->head_dim + 2) * sizeof(float) + 256 : 0;
@@ -319,7 +689,31 @@ int hqmq_attention_decode(const hqmq_attention_args* a, void* stream) {
   p.part_ml = ws ? ws + parts * a->head_dim : nullptr;
   const size_t tab_bytes = 2 * (size_t)kGroupOrder * a->codebook_size * sizeof(float4);
   const dim3 grid((unsigned)pl.splits, (unsigned)(a->batch * a->kv_heads), (unsigned)pl.row_groups);
-  if (tab_bytes <= 160 * 1024) {
+  auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  const size_t msmem = mma_smem_bytes(a->codebook_size, a->index_bits, a->radius_bits);
+  const bool mma_path = a->head_dim == 128 && !a->k.flag_words && !a->v.flag_words &&
+                        p.nrows <= 8 && a->kv_tokens % 8 == 0 && pl.keys_per_split % 64 == 0 &&
+                        msmem <= 200 * 1024 && al16(a->k.index_words) && al16(a->k.radius_words) &&
+                        al16(a->k.scales) && al16(a->v.index_words) && al16(a->v.radius_words) &&
+                        al16(a->v.scales) && !a->precise;
+  // (index_bits, radius_bits) instances of the tensor-core kernel
+  void (*mk)(AttParams) = nullptr;
+  const int wb = a->index_bits * 16 + a->radius_bits;
+  switch (wb) {
+    case 9 * 16 + 4: mk = attention_mma_kernel<9, 4>; break;    // S = 16..21, b_r 4
+    case 10 * 16 + 4: mk = attention_mma_kernel<10, 4>; break;
+    case 11 * 16 + 4: mk = attention_mma_kernel<11, 4>; break;  // S = 43..85 (S=64), b_r 4
+    case 12 * 16 + 4: mk = attention_mma_kernel<12, 4>; break;
+    case 13 * 16 + 4: mk = attention_mma_kernel<13, 4>; break;  // S = 171..341 (S=256)
+    case 11 * 16 + 6: mk = attention_mma_kernel<11, 6>; break;  // Qwen config b_r 6
+    case 11 * 16 + 3: mk = attention_mma_kernel<11, 3>; break;
+    case 12 * 16 + 3: mk = attention_mma_kernel<12, 3>; break;
+    default: break;
+  }
+  if (mma_path && mk) {
+    cudaFuncSetAttribute(mk, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    mk<<<dim3((unsigned)pl.splits, (unsigned)(a->batch * a->kv_heads)), kMThreads, msmem, st>>>(p);
+  } else if (tab_bytes <= 160 * 1024) {
     static thread_local bool set = false;
     if (!set) {
       cudaFuncSetAttribute(attention_split_kernel<true>,

@@ -28,6 +28,7 @@
 #include <cfloat>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -48,7 +49,6 @@ constexpr int kPasses = 5;              // lo bits: 50, 37, 24, 11, 0
 __host__ __device__ constexpr int digit_lo(int pass) { return pass < 4 ? 50 - 13 * pass : 0; }
 __host__ __device__ constexpr int digit_width(int pass) { return pass < 4 ? 13 : 11; }
 constexpr int kHistThreads = 256;
-constexpr int kHistChunksPerBlock = 8192;
 
 struct RadixGroup {
   unsigned long long prefix;
@@ -98,10 +98,16 @@ __device__ __forceinline__ void rotate(const Dir2& u, float4 t0, float4 t1, floa
 }
 
 // Best score over the 24 elements of one coset: max(max_i |v_i|, sum_i |v_i| / 2).
+__device__ __forceinline__ float fmax3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
 __device__ __forceinline__ float coset_score(float2 wx, float2 yz) {
   const float aw = fabsf(wx.x), ax = fabsf(wx.y), ay = fabsf(yz.x), az = fabsf(yz.y);
   const float half = ((aw + ax) + (ay + az)) * 0.5f;
-  return fmaxf(fmaxf(fmaxf(aw, ax), fmaxf(ay, az)), half);
+  return fmax3(fmax3(aw, ax, ay), az, half);
 }
 
 // fp32 direction for the fast path.  The exact fp64 norm r is known.
@@ -463,7 +469,6 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_tile_kernel(EncParams p
 // a warp max, the coded-prefix is a ballot/popc and a token's index codes fill
 // exactly index_bits whole words — no block barriers after the table load.
 // The next tile's input is prefetched into registers while the S-loop runs.
-constexpr int kWT = 4;  // tokens (chunks per lane) per warp tile
 constexpr int kWWarps = 8;
 constexpr int kWThreads = kWWarps * 32;
 
@@ -476,8 +481,8 @@ __device__ __forceinline__ double warp_max_f64(double v) {
   return v;
 }
 
-template <typename InT>
-__global__ void __launch_bounds__(kWThreads, 3) encode_warp_kernel(EncParams p) {
+template <typename InT, int kWT, int kMinB>
+__global__ void __launch_bounds__(kWThreads, kMinB) encode_warp_kernel(EncParams p) {
   extern __shared__ float4 tab_s[];  // [S][4]
   __shared__ uint32_t stage_i[kWWarps][kWT * 32 + 2];
   __shared__ uint32_t stage_r[kWWarps][kWT * 8 + 2];
@@ -712,6 +717,13 @@ __global__ void token_coded_norms_kernel(const double* __restrict__ norms,
 }
 
 // ------------------------------------------------------ Med3x radix select
+// Exact lower median (rank (n-1)//2, outliers.py:50-55) of the fp64 chunk
+// norms of every pooling group: non-negative doubles order like their uint64
+// bit patterns, so 5 histogram passes over 13/13/13/13/11-bit digits of bits
+// [62:0] pin the element.  Passes 0-2 stream the whole call (pass 0 computes
+// and stores the exact norms from the input); pass 2 also compacts the
+// elements still matching the 26-bit prefix into per-group candidate lists,
+// so passes 3-4 touch only those.  Each pass's last CTA selects the digit.
 struct RadixParams {
   int64_t B, H, T, D;
   int C;
@@ -721,6 +733,9 @@ struct RadixParams {
   double multiplier;
   const void* data;
   double* norms;
+  double* cand;           // [G][n_per_group]
+  unsigned int* cand_n;   // [G]
+  unsigned long long n_per_group;
   RadixGroup* groups;
   uint32_t* hist;  // [G][kBins]
   unsigned int* done;
@@ -735,25 +750,21 @@ __device__ __forceinline__ void hist_add(uint32_t* hs, uint32_t bin, bool active
 
 // Last block: pick, for every group, the bin holding rank k; narrow the prefix.
 __device__ void radix_select_last(RadixParams& p) {
-  __shared__ uint32_t part[kHistThreads];
   const int lo = digit_lo(p.pass), width = digit_width(p.pass);
   const int nb = 1 << width;
   const int per = nb / kHistThreads;
+  typedef cub::BlockScan<uint32_t, kHistThreads> BS;
+  __shared__ typename BS::TempStorage scan_tmp;
   for (int g = 0; g < p.G; ++g) {
     uint32_t* hg = p.hist + (int64_t)g * kBins;
     uint32_t sum = 0;
     for (int i = 0; i < per; ++i) sum += __ldcg(hg + threadIdx.x * per + i);
-    part[threadIdx.x] = sum;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      unsigned long long k = p.groups[g].rank;
-      unsigned long long acc = 0;
-      int t = 0;
-      for (; t < kHistThreads; ++t) {
-        if (acc + part[t] > k) break;
-        acc += part[t];
-      }
-      int bin = t * per;
+    const unsigned long long k = p.groups[g].rank;  // read before the scan's barriers
+    uint32_t excl;
+    BS(scan_tmp).ExclusiveSum(sum, excl);
+    if (excl <= k && k < (unsigned long long)excl + sum) {
+      unsigned long long acc = excl;
+      int bin = threadIdx.x * per;
       for (;; ++bin) {
         const uint32_t c = __ldcg(hg + bin);
         if (acc + c > k) break;
@@ -770,7 +781,6 @@ __device__ void radix_select_last(RadixParams& p) {
     for (int i = threadIdx.x; i < kBins; i += kHistThreads) hg[i] = 0u;
     __syncthreads();
   }
-  (void)width;
   if (threadIdx.x == 0) *p.done = 0u;
 }
 
@@ -780,42 +790,81 @@ __global__ void __launch_bounds__(kHistThreads) radix_hist_kernel(RadixParams p)
   __shared__ bool is_last;
   for (int i = threadIdx.x; i < kBins; i += kHistThreads) hs[i] = 0u;
   __syncthreads();
-  const int64_t row = blockIdx.y;
-  const int g = p.per_head ? (int)(row % p.H) : 0;
-  const int64_t L = p.T * p.C;
-  const int64_t base = (int64_t)blockIdx.x * kHistChunksPerBlock;
-  const int64_t end = min(L, base + kHistChunksPerBlock);
   const int lo = digit_lo(p.pass), width = digit_width(p.pass);
   const uint32_t dmask = (1u << width) - 1u;
   const int hi_shift = lo + width;
-  const unsigned long long pref = p.groups[g].prefix;
-  const InT* __restrict__ data = reinterpret_cast<const InT*>(p.data);
-  for (int64_t i0 = base; i0 < end; i0 += kHistThreads) {
-    const int64_t i = i0 + threadIdx.x;
-    bool active = i < end;
-    uint32_t bin = 0;
-    if (active) {
-      double r;
+  const int lane = threadIdx.x & 31;
+  if (p.pass <= 2) {
+    // full pass: grid (bx, rows); the block strides over its row, kRB elements
+    // per thread per step with all loads issued before use (memory-level
+    // parallelism: the pass is a pure stream over 8 B/chunk)
+    constexpr int kRB = 8;
+    const int64_t row = blockIdx.y;
+    const int g = p.per_head ? (int)(row % p.H) : 0;
+    const int64_t L = p.T * p.C;
+    const unsigned long long pref = p.groups[g].prefix;
+    const InT* __restrict__ data = reinterpret_cast<const InT*>(p.data);
+    double* __restrict__ nrow = p.norms + row * L;
+    for (int64_t i0 = (int64_t)blockIdx.x * kHistThreads * kRB; i0 < L;
+         i0 += (int64_t)gridDim.x * kHistThreads * kRB) {
+      double rr[kRB];
       if (p.pass == 0) {
-        const int64_t t = i / p.C;
-        const int c = (int)(i - t * p.C);
-        InT v[4];
-        load_chunk(data + (row * p.T + t) * p.D, c, (int)p.D, p.aligned4 != 0, v);
-        double x[4];
+        InT v[kRB][4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) x[k] = In<InT>::d(v[k]);
-        r = exact_norm(x);
-        p.norms[row * L + i] = r;
+        for (int j = 0; j < kRB; ++j) {
+          const int64_t i = i0 + j * kHistThreads + threadIdx.x;
+          if (i < L) {
+            const int64_t t = i / p.C;
+            const int c = (int)(i - t * p.C);
+            load_chunk(data + (row * p.T + t) * p.D, c, (int)p.D, p.aligned4 != 0, v[j]);
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < kRB; ++j) {
+          const int64_t i = i0 + j * kHistThreads + threadIdx.x;
+          rr[j] = 0.0;
+          if (i < L) {
+            double x[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) x[k] = In<InT>::d(v[j][k]);
+            rr[j] = exact_norm(x);
+            nrow[i] = rr[j];
+          }
+        }
       } else {
-        r = p.norms[row * L + i];
+#pragma unroll
+        for (int j = 0; j < kRB; ++j) {
+          const int64_t i = i0 + j * kHistThreads + threadIdx.x;
+          rr[j] = i < L ? __ldcs(nrow + i) : 0.0;
+        }
       }
-      const unsigned long long key = (unsigned long long)__double_as_longlong(r);
-      if (hi_shift < 64) active = (key >> hi_shift) == (pref >> hi_shift);
-      bin = (uint32_t)(key >> lo) & dmask;
+#pragma unroll
+      for (int j = 0; j < kRB; ++j) {
+        const int64_t i = i0 + j * kHistThreads + threadIdx.x;
+        const unsigned long long key = (unsigned long long)__double_as_longlong(rr[j]);
+        const bool active = i < L && (key >> hi_shift) == (pref >> hi_shift);
+        const uint32_t bin = (uint32_t)(key >> lo) & dmask;
+        if (p.pass == 2) {
+          // compact the survivors of the 26-bit prefix for passes 3-4
+          const unsigned m = __ballot_sync(0xffffffffu, active);
+          if (m) {
+            const int leader = __ffs(m) - 1;
+            unsigned int base = 0;
+            if (lane == leader) base = atomicAdd(p.cand_n + g, (unsigned)__popc(m));
+            base = __shfl_sync(0xffffffffu, base, leader);
+            if (active)
+              p.cand[(unsigned long long)g * p.n_per_group + base +
+                     __popc(m & ((1u << lane) - 1u))] = rr[j];
+          }
+        } else {
+          hist_add(hs, bin, active);
+        }
+      }
     }
-    hist_add(hs, bin, active);
   }
+  if (p.pass == 2) return;  // compaction only; passes 2-4 finish in radix_tail_kernel
   __syncthreads();
+  const int g = p.per_head ? (int)(blockIdx.y % p.H) : 0;
   uint32_t* hg = p.hist + (int64_t)g * kBins;
   for (int i = threadIdx.x; i < kBins; i += kHistThreads)
     if (hs[i]) atomicAdd(hg + i, hs[i]);
@@ -832,13 +881,69 @@ __global__ void __launch_bounds__(kHistThreads) radix_hist_kernel(RadixParams p)
   }
 }
 
-__global__ void radix_init_kernel(RadixGroup* groups, int G, unsigned long long n_per_group) {
+// Digits 2..4 of every group's select over its compacted candidates (the
+// elements matching the 26-bit prefix of passes 0-1), one CTA per group with
+// shared-memory histograms; sets the group's threshold C * median.
+constexpr int kTailThreads = 1024;
+__global__ void __launch_bounds__(kTailThreads) radix_tail_kernel(RadixParams p) {
+  __shared__ uint32_t hs[kBins];
+  __shared__ unsigned long long s_pref, s_rank;
+  const int g = blockIdx.x;
+  const unsigned int n = p.cand_n[g];
+  const double* __restrict__ cg = p.cand + (unsigned long long)g * p.n_per_group;
+  if (threadIdx.x == 0) {
+    s_pref = p.groups[g].prefix;
+    s_rank = p.groups[g].rank;
+  }
+  for (int pass = 2; pass < kPasses; ++pass) {
+    const int lo = digit_lo(pass), width = digit_width(pass);
+    const uint32_t dmask = (1u << width) - 1u;
+    const int hi_shift = lo + width;
+    for (int i = threadIdx.x; i < kBins; i += kTailThreads) hs[i] = 0u;
+    __syncthreads();
+    const unsigned long long pref = s_pref;
+    for (unsigned int i = threadIdx.x; i < n; i += kTailThreads) {
+      const unsigned long long key = (unsigned long long)__double_as_longlong(cg[i]);
+      if ((key >> hi_shift) == (pref >> hi_shift)) atomicAdd(hs + ((uint32_t)(key >> lo) & dmask), 1u);
+    }
+    __syncthreads();
+    const int per = kBins / kTailThreads;  // 8 bins per thread
+    uint32_t sum = 0;
+    for (int i = 0; i < per; ++i) sum += hs[threadIdx.x * per + i];
+    typedef cub::BlockScan<uint32_t, kTailThreads> BS;
+    __shared__ typename BS::TempStorage scan_tmp;
+    uint32_t excl;
+    BS(scan_tmp).ExclusiveSum(sum, excl);
+    const unsigned long long k = s_rank;
+    __syncthreads();
+    if (excl <= k && k < (unsigned long long)excl + sum) {
+      unsigned long long acc = excl;
+      int bin = threadIdx.x * per;
+      for (;; ++bin) {
+        if (acc + hs[bin] > k) break;
+        acc += hs[bin];
+      }
+      s_pref = pref | (((unsigned long long)bin) << lo);
+      s_rank = k - acc;
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    p.groups[g].prefix = s_pref;
+    p.groups[g].rank = s_rank;
+    p.groups[g].threshold = __dmul_rn(p.multiplier, __longlong_as_double((long long)s_pref));
+  }
+}
+
+__global__ void radix_init_kernel(RadixGroup* groups, unsigned int* cand_n, int G,
+                                  unsigned long long n_per_group) {
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g < G) {
     groups[g].prefix = 0ull;
     groups[g].rank = (n_per_group - 1) / 2;
     groups[g].threshold = 0.0;
     groups[g].n = n_per_group;
+    cand_n[g] = 0u;
   }
 }
 
@@ -884,8 +989,8 @@ struct Layout {
   int64_t n_chunks = 0, rows = 0, n_tiles = 0, tiles_per_row = 0;
   int C = 0, TT = 0, G = 0;
   bool warp_path = false;
-  size_t off_norms = 0, off_groups = 0, off_hist = 0, off_done = 0, off_counts = 0,
-         off_prefix = 0, off_cub = 0, cub_bytes = 0, total = 0;
+  size_t off_norms = 0, off_cand = 0, off_cand_n = 0, off_groups = 0, off_hist = 0, off_done = 0,
+         off_counts = 0, off_prefix = 0, off_cub = 0, cub_bytes = 0, total = 0;
 };
 
 // The barrier-free warp kernel covers the model shapes: head_dim 128 with
@@ -915,6 +1020,10 @@ bool plan(const hqmq_encode_args* a, Layout& L) {
   if (ext) {
     L.off_norms = off;
     off = align_up(off + (size_t)L.n_chunks * 8, 256);
+    L.off_cand = off;
+    off = align_up(off + (size_t)L.n_chunks * 8, 256);
+    L.off_cand_n = off;
+    off = align_up(off + (size_t)L.G * 4, 256);
     L.off_groups = off;
     off = align_up(off + (size_t)L.G * sizeof(RadixGroup), 256);
     L.off_hist = off;
@@ -970,17 +1079,25 @@ int launch_encode(const hqmq_encode_args* a, const Layout& L, cudaStream_t st) {
     cudaMemsetAsync(done, 0, 16, st);
     const unsigned long long n_per_group =
         (unsigned long long)(L.n_chunks / (a->per_head_pooling ? a->heads : 1));
-    radix_init_kernel<<<(L.G + 127) / 128, 128, 0, st>>>(groups, L.G, n_per_group);
+    unsigned int* cand_n = reinterpret_cast<unsigned int*>(ws + L.off_cand_n);
+    radix_init_kernel<<<(L.G + 127) / 128, 128, 0, st>>>(groups, cand_n, L.G, n_per_group);
     RadixParams rp;
     rp.B = a->batch; rp.H = a->heads; rp.T = a->tokens; rp.D = a->head_dim; rp.C = L.C;
     rp.per_head = a->per_head_pooling; rp.aligned4 = aligned4; rp.multiplier = a->outlier_multiplier;
     rp.data = a->data; rp.norms = reinterpret_cast<double*>(ws + L.off_norms);
+    rp.cand = reinterpret_cast<double*>(ws + L.off_cand);
+    rp.cand_n = cand_n;
+    rp.n_per_group = n_per_group;
     rp.groups = groups; rp.hist = hist; rp.done = done; rp.G = L.G;
-    const dim3 hgrid((unsigned)ceil_div(a->tokens * L.C, kHistChunksPerBlock), (unsigned)L.rows);
-    for (int pass = 0; pass < kPasses; ++pass) {
+    const int64_t row_chunks = a->tokens * L.C;
+    const int64_t bx_full = std::max<int64_t>(
+        1, std::min<int64_t>(ceil_div((int64_t)148 * 4, L.rows), ceil_div(row_chunks, kHistThreads * 8)));
+
+    for (int pass = 0; pass <= 2; ++pass) {
       rp.pass = pass;
-      radix_hist_kernel<InT><<<hgrid, kHistThreads, 0, st>>>(rp);
+      radix_hist_kernel<InT><<<dim3((unsigned)bx_full, (unsigned)L.rows), kHistThreads, 0, st>>>(rp);
     }
+    radix_tail_kernel<<<L.G, kTailThreads, 0, st>>>(rp);
     uint32_t* counts = reinterpret_cast<uint32_t*>(ws + L.off_counts);
     size_t cub_bytes = L.cub_bytes;
     if (L.warp_path) {
@@ -1024,17 +1141,25 @@ int launch_encode(const hqmq_encode_args* a, const Layout& L, cudaStream_t st) {
   const size_t smem = (size_t)std::min(a->codebook_size, kSBlock) * 4 * sizeof(float4);
   if constexpr (sizeof(InT) == 2) {
     if (L.warp_path) {
-      static thread_local bool wattr[2] = {false, false};
-      const int wi = std::is_same<InT, __half>::value ? 0 : 1;
-      if (!wattr[wi]) {
-        cudaFuncSetAttribute(encode_warp_kernel<InT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      // tile size / occupancy variant (HQMQ_ENC_VARIANT for tuning: 0..3)
+      static const int variant = [] {
+        const char* v = getenv("HQMQ_ENC_VARIANT");
+        return v ? atoi(v) : 0;
+      }();
+      auto launch = [&](auto kern, int wt, int minb) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              kSBlock * 4 * (int)sizeof(float4));
-        wattr[wi] = true;
+        const int64_t ntiles = ceil_div(a->tokens, wt);
+        const int64_t want = ceil_div((int64_t)148 * minb, L.rows);
+        const int64_t bx = std::max<int64_t>(1, std::min<int64_t>(want, ceil_div(ntiles, kWWarps)));
+        kern<<<dim3((unsigned)bx, (unsigned)L.rows), kWThreads, smem, st>>>(p);
+      };
+      switch (variant) {
+        case 1: launch(encode_warp_kernel<InT, 4, 3>, 4, 3); break;
+        case 2: launch(encode_warp_kernel<InT, 8, 2>, 8, 2); break;
+        case 3: launch(encode_warp_kernel<InT, 8, 1>, 8, 1); break;
+        default: launch(encode_warp_kernel<InT, 4, 2>, 4, 2); break;
       }
-      const int64_t ntiles = ceil_div(a->tokens, kWT);
-      const int64_t want = ceil_div(148 * 3, L.rows);
-      const int64_t bx = std::max<int64_t>(1, std::min<int64_t>(want, ceil_div(ntiles, kWWarps)));
-      encode_warp_kernel<InT><<<dim3((unsigned)bx, (unsigned)L.rows), kWThreads, smem, st>>>(p);
       e = cudaGetLastError();
       return e == cudaSuccess ? HQMQ_OK : cuda_fail(e);
     }
