@@ -131,10 +131,11 @@ def measured_peaks():
 
 # --------------------------------------------------------------- workload
 def units_for_rank(wl, world, rank):
-    units = [(layer, role) for layer in range(wl["layers"]) for role in ("K", "V")]
-    if wl["shard"] == "strong":
-        return units[rank::world]
-    return units
+    """(layer, role) units of this rank: contiguous layer blocks for the
+    strong-scaled cache (c5), a full replica per rank otherwise."""
+    from paper_2605_27646_b200.shard import ShardPlan
+
+    return ShardPlan(wl["layers"], world, rank, wl["shard"]).units()
 
 
 def make_input(torch, wl, layer, role, dev):

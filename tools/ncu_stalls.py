@@ -11,6 +11,8 @@ reasons = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
 tot = {r: 0 for r in reasons}
 samples = []
 for row in data:
+    if len(row) < len(hdr):
+        continue
     try:
         s = int(row[col["Warp Stall Sampling (All Samples)"]] or 0)
     except ValueError:
