@@ -14,6 +14,7 @@
 // online-softmax update, and one thread per (row, 4-dim chunk) accumulates
 // P.V.  Partial (m, l, o) per split are merged by combine_kernel.
 #include <algorithm>
+#include <cstdint>
 #include <cfloat>
 #include <cmath>
 #include <cstdlib>
@@ -244,21 +245,32 @@ __global__ void combine_kernel(AttParams p) {
 // ------------------------------------------------------------------------
 // Tensor-core fast path (head_dim 128, no outlier extraction, <= 8 query rows
 // per kv head, i.e. decode with GQA group <= 8) — warp-independent
-// flash-decoding inside the CTA:
+// flash-decoding inside the CTA, with K/V decoded straight into mma.sync
+// operand registers (no fp16 K/V tile in shared memory):
 //   * 128-key tiles of the K and V sections (index / radius words and fp16
 //     scales) stream into a kMStages-deep shared ring with cp.async.bulk; a
 //     full mbarrier per stage signals arrival, and the last warp to release a
 //     stage (shared-memory counter) issues that stage's next tile;
-//   * consumer warp w owns keys [16w, 16w+16) of every tile: it decodes its K
-//     rows into a private fp16 tile (lane = chunk; half2 radius x codeword from
-//     fp16 copies of the joint tables), runs S = Q K^T on mma.sync.m16n8k16
-//     (query rows on M, padded to 16; keys on N), updates its own online
-//     softmax, decodes its V rows into the same buffer and runs O += P V with
-//     the S accumulators reused as the P operand (no block barriers);
-//   * at the end the 8 warps' (m, l, O) are merged through shared memory.
+//   * consumer warp w owns keys [16w, 16w+16) of every tile.  QK^T and PV are
+//     sums over head dims, so any permutation of the dims applied to both
+//     operands (and undone when O is written) leaves them unchanged.  The
+//     permutations below make every mma fragment element come from ONE
+//     decoded 4-dim chunk, so each (key, chunk) is decoded exactly once, by
+//     the lane whose fragment needs it:
+//       S = Q K^T  (m16n8k16, M = query rows, N = 8 keys, K = 16 dims):
+//         lane (g, t) holds B[k = 2t, 2t+1, 2t+8, 2t+9][key g]; k-slab ks maps
+//         those 4 positions to chunk 8t + ks  ->  the lane decodes chunks
+//         8t..8t+7 of key g (one contiguous run of 8 codes per stream);
+//       O^T += V^T P^T (M = 16 dims, N = query rows, K = 16 keys):
+//         lane (g, t) holds A[m = g, g+8][k = 2t, 2t+1, 2t+8, 2t+9]; m-tiles
+//         (2j, 2j+1) map (m = g, g+8) to elements (0, 1) / (2, 3) of chunk
+//         4g + j  ->  the lane decodes chunks 4g..4g+3 of keys 2t, 2t+1,
+//         2t+8, 2t+9;
+//     P^T's B fragments are the S accumulators themselves (S->P register
+//     reuse), with the per-key scale sigma/top folded into S (K) and P (V);
+//   * the warps' (m, l, O) are merged through shared memory at the end.
 constexpr int kMT = 128;          // keys per CTA tile (8 warps x 16)
-constexpr int kMStages = 3;
-constexpr int kKVStride = 136;    // halves per smem row: 128 + 8 (conflict-free ldmatrix)
+constexpr int kMStages = 4;
 constexpr int kMConsumers = 8;
 constexpr int kMThreads = kMConsumers * 32;
 
@@ -284,19 +296,9 @@ __host__ __device__ inline size_t mma_smem_bytes(int S, int w, int br) {
   const size_t tab = 2 * (size_t)kGroupOrder * S * 8;
   const size_t ring = kMStages * (size_t)ring_geom(w, br).bytes;
   const size_t merge = (size_t)kMConsumers * 8 * 130 * 4;  // O + (m, l) per warp/row
-  return tab + (ring > merge ? ring : merge) + (size_t)kMConsumers * 16 * kKVStride * 2;
+  return tab + (ring > merge ? ring : merge);
 }
 
-__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* ptr) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-               : "r"(smem_u32(ptr)));
-}
-__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], const void* ptr) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-               : "r"(smem_u32(ptr)));
-}
 // D(16x8 fp32) += A(16x16 fp16, rows 8-15 zero) * B(16x8 fp16)
 __device__ __forceinline__ void mma_rows8(float (&d)[4], uint32_t a0, uint32_t a2, uint32_t b0,
                                           uint32_t b1) {
@@ -306,59 +308,54 @@ __device__ __forceinline__ void mma_rows8(float (&d)[4], uint32_t a0, uint32_t a
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
 }
+__device__ __forceinline__ void mma_full(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                         uint32_t a3, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
+      "{%8,%9}, {%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
 __device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
   const __half2 h = __floats2half2_rn(lo, hi);
   return *reinterpret_cast<const uint32_t*>(&h);
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+__device__ __forceinline__ uint32_t hmul2u(uint32_t a, uint32_t b) {
+  const __half2 r = __hmul2(*reinterpret_cast<const __half2*>(&a), *reinterpret_cast<const __half2*>(&b));
+  return *reinterpret_cast<const uint32_t*>(&r);
 }
 
-// Decode 16 key rows (tokens tt0..tt0+15 of the staged tile) of one tensor into
-// a [16][kKVStride] fp16 tile of quantum x codeword (lane = chunk).  The
-// per-key scale sigma/top is NOT applied here: it is constant per key, so the
-// caller folds it into S (K) and into P (V) after the MMAs.  W / BR are
-// compile-time so every stream offset is an immediate; rows are processed in
-// batches of 8 with all shared loads issued before the dependent math.
-template <int W, int BR>
-__device__ __forceinline__ void decode_rows16(const uint32_t* __restrict__ iw,
-                                              const uint32_t* __restrict__ rw,
-                                              const uint2* __restrict__ tab,
-                                              __half* __restrict__ dst, int tt0, int nvalid,
-                                              int lane) {
-  constexpr uint32_t kIMask = W == 32 ? 0xffffffffu : ((1u << W) - 1u);
-  constexpr uint32_t kRMask = (1u << BR) - 1u;
-  const uint32_t lwi = (uint32_t)lane * W, lwr = (uint32_t)lane * BR;
-  const uint32_t ish = lwi & 31, rsh = lwr & 31;
-  const uint32_t* __restrict__ ip = iw + tt0 * W + (lwi >> 5);
-  const uint32_t* __restrict__ rp = rw + tt0 * BR + (lwr >> 5);
-  __half* __restrict__ dp = dst + 4 * lane;
-#pragma unroll
-  for (int j0 = 0; j0 < 16; j0 += 8) {
-    uint32_t idx[8], q[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int jj = j0 + j;
-      idx[j] = __funnelshift_r(ip[jj * W], ip[jj * W + 1], ish) & kIMask;
-      if constexpr (32 % BR == 0) q[j] = (rp[jj * BR] >> rsh) & kRMask;
-      else q[j] = __funnelshift_r(rp[jj * BR], rp[jj * BR + 1], rsh) & kRMask;
-    }
-    uint2 cw[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) cw[j] = tab[idx[j]];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) {
-      const int jj = j0 + j;
-      const __half2 h = __half2half2(__uint2half_rn(q[j]));
-      const __half2 e0 = __hmul2(h, *reinterpret_cast<const __half2*>(&cw[j].x));
-      const __half2 e1 = __hmul2(h, *reinterpret_cast<const __half2*>(&cw[j].y));
-      uint2 out = make_uint2(*reinterpret_cast<const uint32_t*>(&e0),
-                             *reinterpret_cast<const uint32_t*>(&e1));
-      if (jj >= nvalid) out = make_uint2(0u, 0u);
-      *reinterpret_cast<uint2*>(dp + jj * kKVStride) = out;
-    }
-  }
+// N codes of WIDTH bits starting at bit `bit` of a shared-memory stream
+// (LSB-first 32-bit words): NW words are loaded, aligned by one runtime
+// funnel shift, then every code sits at a compile-time position.
+// The run starts at bit key*32*WIDTH + t*N*WIDTH (t < NT), so its in-word
+// shift is (t*N*WIDTH) & 31 and the worst case is known at compile time.
+__host__ __device__ constexpr int max_run_shift(int n, int width, int nt) {
+  int m = 0;
+  for (int t = 0; t < nt; ++t) m = ((t * n * width) & 31) > m ? ((t * n * width) & 31) : m;
+  return m;
 }
+template <int N, int WIDTH, int NT>
+struct CodeRun {
+  static constexpr int kSpan = max_run_shift(N, WIDTH, NT) + N * WIDTH;  // bits to cover
+  static constexpr int kNW = (kSpan + 31) / 32;                          // words loaded
+  uint32_t r[kNW];
+  __device__ __forceinline__ void load(const uint32_t* __restrict__ s, uint32_t bit) {
+    const uint32_t* p = s + (bit >> 5);
+    const uint32_t sh = bit & 31;
+    uint32_t w[kNW + 1];
+#pragma unroll
+    for (int i = 0; i < kNW; ++i) w[i] = p[i];
+    w[kNW] = 0u;
+#pragma unroll
+    for (int i = 0; i < kNW; ++i) r[i] = __funnelshift_r(w[i], w[i + 1], sh);
+  }
+  __device__ __forceinline__ uint32_t get(int i) const {
+    const int b = i * WIDTH, wi = b >> 5, sh = b & 31;
+    uint32_t v = sh == 0 ? r[wi] : __funnelshift_r(r[wi], wi + 1 < kNW ? r[wi + 1] : 0u, sh);
+    return WIDTH == 32 ? v : (v & ((1u << WIDTH) - 1u));
+  }
+};
 
 template <int W, int BR>
 __global__ void __launch_bounds__(kMThreads, 2) attention_mma_kernel(AttParams p) {
@@ -372,9 +369,6 @@ __global__ void __launch_bounds__(kMThreads, 2) attention_mma_kernel(AttParams p
   uint2* ktab = reinterpret_cast<uint2*>(sm);
   uint2* vtab = ktab + ncw;
   unsigned char* ring = reinterpret_cast<unsigned char*>(vtab + ncw);
-  const size_t ring_bytes = kMStages * (size_t)gm.bytes;
-  const size_t merge_bytes = (size_t)kMConsumers * 8 * 130 * 4;
-  __half* kvbuf = reinterpret_cast<__half*>(ring + (ring_bytes > merge_bytes ? ring_bytes : merge_bytes));
 
   const int64_t bh = blockIdx.y;
   const int64_t b = bh / p.Hkv, hkv = bh % p.Hkv;
@@ -390,22 +384,7 @@ __global__ void __launch_bounds__(kMThreads, 2) attention_mma_kernel(AttParams p
     }
     fence_mbar_init();
   }
-  const float4* gk = p.k.table + hkv * ncw;
-  const float4* gv = p.v.table + hkv * ncw;
-  for (int i = tid; i < ncw; i += kMThreads) {
-    const float4 a = __ldg(gk + i), c = __ldg(gv + i);
-    ktab[i] = make_uint2(pack_half2(a.x, a.y), pack_half2(a.z, a.w));
-    vtab[i] = make_uint2(pack_half2(c.x, c.y), pack_half2(c.z, c.w));
-  }
   __syncthreads();
-
-  const int g4 = lane >> 2, t4 = lane & 3;  // mma fragment coordinates
-  float m_run = -INFINITY, l_run = 0.f;
-  // O^T accumulators: m-tile md covers dims 16md..16md+15; c0/c1 = (dim 16md+g4,
-  // rows 2t4 / 2t4+1), c2/c3 = (dim 16md+g4+8, rows 2t4 / 2t4+1)
-  float oT[8][4];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) oT[i][0] = oT[i][1] = oT[i][2] = oT[i][3] = 0.f;
 
   auto issue = [&](int64_t k, int stage) {
     const int64_t t = tokrow + kbeg + k * kMT;
@@ -430,129 +409,152 @@ __global__ void __launch_bounds__(kMThreads, 2) attention_mma_kernel(AttParams p
       }
     }
   };
+  // the first tiles stream in while the joint tables are converted to fp16
   if (tid == 0)
     for (int s = 0; s < kMStages && s < ntile; ++s) issue(s, s);
-  {
-    // ---------------- consumers
-    // Q A-fragments (rows x dims, rows 8..15 zero): qa[ks] = {a0, a2}
-    uint32_t qa[8][2];
-    const bool row_valid = g4 < p.nrows;
-    {
-      const int gi = row_valid ? g4 / (int)p.Tq : 0, qi = row_valid ? g4 - gi * (int)p.Tq : 0;
-      const float* qrow = p.q + ((b * p.Hq + hkv * p.g + gi) * p.Tq + qi) * 128;
-#pragma unroll
-      for (int ks = 0; ks < 8; ++ks) {
-        const int d = ks * 16 + t4 * 2;
-        float v0 = 0.f, v1 = 0.f, v8 = 0.f, v9 = 0.f;
-        if (row_valid) {
-          v0 = qrow[d] * p.scale_log2; v1 = qrow[d + 1] * p.scale_log2;
-          v8 = qrow[d + 8] * p.scale_log2; v9 = qrow[d + 9] * p.scale_log2;
-        }
-        qa[ks][0] = pack_half2(v0, v1);
-        qa[ks][1] = pack_half2(v8, v9);
-      }
-    }
-    int64_t vis = p.Tkv;  // keys j < vis are visible to row g4
-    if (row_valid && p.causal) vis = (g4 % (int)p.Tq) + (p.Tkv - p.Tq) + 1;
-    const float rtop = 1.0f / (float)((1 << br) - 1);
-    __half* mybuf = kvbuf + warp * 16 * kKVStride;
+  const float4* gk = p.k.table + hkv * ncw;
+  const float4* gv = p.v.table + hkv * ncw;
+  for (int i = tid; i < ncw; i += kMThreads) {
+    const float4 a = __ldg(gk + i), c = __ldg(gv + i);
+    ktab[i] = make_uint2(pack_half2(a.x, a.y), pack_half2(a.z, a.w));
+    vtab[i] = make_uint2(pack_half2(c.x, c.y), pack_half2(c.z, c.w));
+  }
+  __syncthreads();
 
-    for (int64_t k = 0; k < ntile; ++k) {
-      const int stage = (int)(k % kMStages);
-      mbar_wait(&full[stage], (uint32_t)((k / kMStages) & 1));
-      const unsigned char* s = ring + (size_t)stage * gm.bytes;
-      const int64_t t0 = kbeg + k * kMT + warp * 16;  // this warp's first key
-      const int nvalid = (int)max((int64_t)0, min((int64_t)16, kend - t0));
-      if (nvalid > 0) {
-        // ---- K rows -> fp16 tile, S = Q K^T (two 8-key n-tiles)
-        decode_rows16<W, BR>(reinterpret_cast<const uint32_t*>(s + gm.ki),
-                             reinterpret_cast<const uint32_t*>(s + gm.kr), ktab, mybuf, warp * 16,
-                             nvalid, lane);
-        // per-key scales sigma/top of the 4 keys this thread's fragments touch
-        float kst[4], vst[4];
-        {
-          const uint16_t* ks = reinterpret_cast<const uint16_t*>(s + gm.ks) + warp * 16;
-          const uint16_t* vs = reinterpret_cast<const uint16_t*>(s + gm.vs) + warp * 16;
+  const int g4 = lane >> 2, t4 = lane & 3;  // mma fragment coordinates
+  const uint32_t cwmax = (uint32_t)ncw - 1u;
+  float m_run = -INFINITY, l_run = 0.f;
+  // O^T accumulators, m-tile 2j+h: c0/c1 = (dim 4(4g4+j)+2h, rows 2t4 / 2t4+1),
+  // c2/c3 = (dim 4(4g4+j)+2h+1, rows 2t4 / 2t4+1)
+  float oT[8][4];
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int key = (e >> 1) * 8 + t4 * 2 + (e & 1);
-            kst[e] = __half2float(__ushort_as_half(ks[key])) * rtop;
-            vst[e] = __half2float(__ushort_as_half(vs[key])) * rtop;
-          }
+  for (int i = 0; i < 8; ++i) oT[i][0] = oT[i][1] = oT[i][2] = oT[i][3] = 0.f;
+
+  // Q A-fragments (rows x permuted dims, rows 8..15 zero): k-slab ks holds
+  // chunk 8*t4 + ks of row g4: qa[ks] = {elements 0,1 ; elements 2,3}
+  uint32_t qa[8][2];
+  const bool row_valid = g4 < p.nrows;
+  {
+    const int gi = row_valid ? g4 / (int)p.Tq : 0, qi = row_valid ? g4 - gi * (int)p.Tq : 0;
+    const float4* qrow =
+        reinterpret_cast<const float4*>(p.q + ((b * p.Hq + hkv * p.g + gi) * p.Tq + qi) * 128);
+#pragma unroll
+    for (int ks = 0; ks < 8; ++ks) {
+      float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+      if (row_valid) v = __ldg(qrow + 8 * t4 + ks);
+      qa[ks][0] = pack_half2(v.x * p.scale_log2, v.y * p.scale_log2);
+      qa[ks][1] = pack_half2(v.z * p.scale_log2, v.w * p.scale_log2);
+    }
+  }
+  int64_t vis = p.Tkv;  // keys j < vis are visible to row g4
+  if (row_valid && p.causal) vis = (g4 % (int)p.Tq) + (p.Tkv - p.Tq) + 1;
+  const float rtop = 1.0f / (float)((1 << br) - 1);
+
+  for (int64_t k = 0; k < ntile; ++k) {
+    const int stage = (int)(k % kMStages);
+    mbar_wait(&full[stage], (uint32_t)((k / kMStages) & 1));
+    const unsigned char* s = ring + (size_t)stage * gm.bytes;
+    const uint32_t* kiw = reinterpret_cast<const uint32_t*>(s + gm.ki);
+    const uint32_t* krw = reinterpret_cast<const uint32_t*>(s + gm.kr);
+    const uint16_t* ksc = reinterpret_cast<const uint16_t*>(s + gm.ks);
+    const uint32_t* viw = reinterpret_cast<const uint32_t*>(s + gm.vi);
+    const uint32_t* vrw = reinterpret_cast<const uint32_t*>(s + gm.vr);
+    const uint16_t* vsc = reinterpret_cast<const uint16_t*>(s + gm.vs);
+    const int kw0 = warp * 16;                       // this warp's first key in the tile
+    const int64_t t0 = kbeg + k * kMT + kw0;         // ... as a key index
+    if (t0 < kend) {
+      // ---- S = Q K^T: lane decodes chunks 8*t4 .. 8*t4+7 of key kw0 + 8*nt + g4
+      float sc[2][4];
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
+        const uint32_t key = (uint32_t)(kw0 + nt * 8 + g4);
+        CodeRun<8, W, 4> ic;
+        CodeRun<8, BR, 4> rc;
+        ic.load(kiw, key * 32u * W + (uint32_t)t4 * 8u * W);
+        rc.load(krw, key * 32u * BR + (uint32_t)t4 * 8u * BR);
+#pragma unroll
+        for (int ks = 0; ks < 8; ++ks) {
+          const uint2 cw = ktab[min(ic.get(ks), cwmax)];
+          const __half hq = __uint2half_rn(rc.get(ks));
+          const __half2 q2 = __half2half2(hq);
+          const uint32_t qq = *reinterpret_cast<const uint32_t*>(&q2);
+          mma_rows8(sc[nt], qa[ks][0], qa[ks][1], hmul2u(qq, cw.x), hmul2u(qq, cw.y));
         }
-        __syncwarp();
-        float sc[2][4];
-#pragma unroll
-        for (int nt = 0; nt < 2; ++nt) {
-          sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
-#pragma unroll
-          for (int kk = 0; kk < 4; ++kk) {  // two k-steps per ldmatrix.x4
-            uint32_t bf[4];
-            ldsm_x4(bf, mybuf + (nt * 8 + (lane & 7)) * kKVStride + kk * 32 + (lane >> 3) * 8);
-            mma_rows8(sc[nt], qa[2 * kk][0], qa[2 * kk][1], bf[0], bf[1]);
-            mma_rows8(sc[nt], qa[2 * kk + 1][0], qa[2 * kk + 1][1], bf[2], bf[3]);
-          }
-        }
-        // ---- online softmax for row g4 over this warp's 16 keys (log2 domain)
-        float sv[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int nt = e >> 1;
-          const int64_t key = t0 + nt * 8 + t4 * 2 + (e & 1);
-          const bool ok = row_valid && key < kend && key < vis;
-          sv[e] = ok ? sc[nt][e & 1] * kst[e] : -INFINITY;
-        }
-        float mx = fmaxf(fmaxf(sv[0], sv[1]), fmaxf(sv[2], sv[3]));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-        const float m_new = fmaxf(m_run, mx);
-        float pe[4], alpha = 1.f;
-        if (m_new == -INFINITY) {
-          pe[0] = pe[1] = pe[2] = pe[3] = 0.f;
-        } else {
-#pragma unroll
-          for (int e = 0; e < 4; ++e) pe[e] = sv[e] == -INFINITY ? 0.f : exp2f(sv[e] - m_new);
-          alpha = m_run == -INFINITY ? 0.f : exp2f(m_run - m_new);
-        }
-        float ps = (pe[0] + pe[1]) + (pe[2] + pe[3]);
-        ps += __shfl_xor_sync(0xffffffffu, ps, 1);
-        ps += __shfl_xor_sync(0xffffffffu, ps, 2);
-        l_run = l_run * alpha + ps;
-        m_run = m_new;
-        // rescale: this thread's O^T columns are rows 2t4 and 2t4+1, whose
-        // softmax state lives in lanes 8t4 and 8t4+4
-        const float a_lo = __shfl_sync(0xffffffffu, alpha, t4 * 8);
-        const float a_hi = __shfl_sync(0xffffffffu, alpha, t4 * 8 + 4);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          oT[i][0] *= a_lo; oT[i][1] *= a_hi; oT[i][2] *= a_lo; oT[i][3] *= a_hi;
-        }
-        // P^T (keys x rows) B-fragments straight from the S accumulators,
-        // with the V per-key scale sigma/top folded in
-        const uint32_t pb0 = pack_half2(pe[0] * vst[0], pe[1] * vst[1]);
-        const uint32_t pb1 = pack_half2(pe[2] * vst[2], pe[3] * vst[3]);
-        __syncwarp();
-        // ---- V rows -> same fp16 tile, O^T += V^T P^T (8 dim m-tiles)
-        decode_rows16<W, BR>(reinterpret_cast<const uint32_t*>(s + gm.vi),
-                             reinterpret_cast<const uint32_t*>(s + gm.vr), vtab, mybuf, warp * 16,
-                             nvalid, lane);
-        __syncwarp();
-        release(k, stage);
-#pragma unroll
-        for (int md = 0; md < 8; ++md) {
-          uint32_t af[4];
-          ldsm_x4_t(af, mybuf + ((lane & 7) + (lane >> 4) * 8) * kKVStride + md * 16 +
-                            ((lane >> 3) & 1) * 8);
-          asm volatile(
-              "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
-              "{%8,%9}, {%0,%1,%2,%3};"
-              : "+f"(oT[md][0]), "+f"(oT[md][1]), "+f"(oT[md][2]), "+f"(oT[md][3])
-              : "r"(af[0]), "r"(af[1]), "r"(af[2]), "r"(af[3]), "r"(pb0), "r"(pb1));
-        }
-        __syncwarp();
-      } else {
-        release(k, stage);
       }
+      // per-key scales sigma/top of this lane's 4 keys (2t4, 2t4+1, 2t4+8, 2t4+9)
+      float kst[4], vst[4], sv[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int kk = kw0 + (e >> 1) * 8 + t4 * 2 + (e & 1);
+        const int64_t key = kbeg + k * kMT + kk;
+        const bool in = key < kend;
+        kst[e] = __half2float(__ushort_as_half(ksc[kk])) * rtop;
+        vst[e] = in ? __half2float(__ushort_as_half(vsc[kk])) * rtop : 0.f;
+        const bool ok = row_valid && in && key < vis;
+        sv[e] = ok ? sc[e >> 1][e & 1] * kst[e] : -INFINITY;
+      }
+      // ---- online softmax for row g4 over this warp's 16 keys (log2 domain)
+      float mx = fmaxf(fmaxf(sv[0], sv[1]), fmaxf(sv[2], sv[3]));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+      const float m_new = fmaxf(m_run, mx);
+      float pe[4], alpha = 1.f;
+      if (m_new == -INFINITY) {
+        pe[0] = pe[1] = pe[2] = pe[3] = 0.f;
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) pe[e] = exp2f(sv[e] - m_new);
+        alpha = exp2f(m_run - m_new);
+      }
+      float ps = (pe[0] + pe[1]) + (pe[2] + pe[3]);
+      ps += __shfl_xor_sync(0xffffffffu, ps, 1);
+      ps += __shfl_xor_sync(0xffffffffu, ps, 2);
+      l_run = l_run * alpha + ps;
+      m_run = m_new;
+      // rescale: this thread's O^T columns are rows 2t4 and 2t4+1, whose
+      // softmax state lives in lanes 8t4 and 8t4+4
+      const float a_lo = __shfl_sync(0xffffffffu, alpha, t4 * 8);
+      const float a_hi = __shfl_sync(0xffffffffu, alpha, t4 * 8 + 4);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        oT[i][0] *= a_lo; oT[i][1] *= a_hi; oT[i][2] *= a_lo; oT[i][3] *= a_hi;
+      }
+      // P^T B-fragments straight from the S accumulators, V scale folded in
+      const uint32_t pb0 = pack_half2(pe[0] * vst[0], pe[1] * vst[1]);
+      const uint32_t pb1 = pack_half2(pe[2] * vst[2], pe[3] * vst[3]);
+      // ---- O^T += V^T P^T: lane decodes chunks 4*g4 .. 4*g4+3 of its 4 keys
+      uint2 vv[4][4];  // [key e][chunk j] -> 4 halves
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t key = (uint32_t)(kw0 + (e >> 1) * 8 + t4 * 2 + (e & 1));
+        CodeRun<4, W, 8> ic;
+        CodeRun<4, BR, 8> rc;
+        ic.load(viw, key * 32u * W + (uint32_t)g4 * 4u * W);
+        rc.load(vrw, key * 32u * BR + (uint32_t)g4 * 4u * BR);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint2 cw = vtab[min(ic.get(j), cwmax)];
+          const __half2 q2 = __half2half2(__uint2half_rn(rc.get(j)));
+          const uint32_t qq = *reinterpret_cast<const uint32_t*>(&q2);
+          vv[e][j] = make_uint2(hmul2u(qq, cw.x), hmul2u(qq, cw.y));
+        }
+      }
+      release(k, stage);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        // m-tile 2j: (m = g4, g4+8) = elements (0, 1); m-tile 2j+1: elements (2, 3)
+        // a0 = keys (2t4, 2t4+1) at m = g4 ; a1 = same keys at m = g4+8
+        // a2 = keys (2t4+8, 2t4+9) at m = g4 ; a3 = same keys at m = g4+8
+        const uint32_t x0 = vv[0][j].x, x1 = vv[1][j].x, x2 = vv[2][j].x, x3 = vv[3][j].x;
+        const uint32_t y0 = vv[0][j].y, y1 = vv[1][j].y, y2 = vv[2][j].y, y3 = vv[3][j].y;
+        mma_full(oT[2 * j], __byte_perm(x0, x1, 0x5410), __byte_perm(x0, x1, 0x7632),
+                 __byte_perm(x2, x3, 0x5410), __byte_perm(x2, x3, 0x7632), pb0, pb1);
+        mma_full(oT[2 * j + 1], __byte_perm(y0, y1, 0x5410), __byte_perm(y0, y1, 0x7632),
+                 __byte_perm(y2, y3, 0x5410), __byte_perm(y2, y3, 0x7632), pb0, pb1);
+      }
+    } else {
+      release(k, stage);
     }
   }
   // every consumer is past its last read of the ring (and no bulk copy is in
@@ -561,12 +563,12 @@ __global__ void __launch_bounds__(kMThreads, 2) attention_mma_kernel(AttParams p
   {
     float* mo = reinterpret_cast<float*>(ring);  // [warp][row][130]
 #pragma unroll
-    for (int md = 0; md < 8; ++md) {
+    for (int mt = 0; mt < 8; ++mt) {
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int row = t4 * 2 + (e & 1);
-        const int dim = md * 16 + g4 + (e >> 1) * 8;
-        mo[((size_t)warp * 8 + row) * 130 + dim] = oT[md][e];
+        const int dim = 4 * (4 * g4 + (mt >> 1)) + 2 * (mt & 1) + (e >> 1);
+        mo[((size_t)warp * 8 + row) * 130 + dim] = oT[mt][e];
       }
     }
     if (t4 == 0) {
@@ -632,9 +634,20 @@ bool plan_att(const hqmq_attention_args* a, AttPlan& pl) {
   const int64_t ctas = a->batch * a->kv_heads * pl.row_groups;
   int splits = a->num_splits;
   if (splits <= 0) {
-    const int64_t target = 148 * 8;
-    splits = (int)std::max<int64_t>(1, std::min<int64_t>(ceil_div(target, ctas),
-                                                           ceil_div(a->kv_tokens, 256)));
+    // Per-SM load model: a split costs its 128-key tiles plus ~3 tiles of
+    // prologue (table staging, ring fill) and the busiest of the 148 SMs
+    // runs ceil(ctas*splits/148) CTAs; pick the cheapest split count.
+    int64_t best = INT64_MAX;
+    splits = 1;
+    const int64_t max_s = std::max<int64_t>(1, std::min<int64_t>(64, ceil_div(a->kv_tokens, 256)));
+    for (int64_t s = 1; s <= max_s; ++s) {
+      const int64_t tiles = ceil_div(ceil_div(a->kv_tokens, s), 128);
+      const int64_t cost = ceil_div(ctas * s, 148) * (tiles + 3);
+      if (cost < best) {
+        best = cost;
+        splits = (int)s;
+      }
+    }
   }
   pl.keys_per_split = ceil_div(ceil_div(a->kv_tokens, splits), 64) * 64;
   pl.splits = (int)ceil_div(a->kv_tokens, pl.keys_per_split);

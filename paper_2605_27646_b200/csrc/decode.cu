@@ -16,6 +16,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -169,14 +170,63 @@ __host__ __device__ inline FastDecodeGeom fd_geom(int w, int br) {
   return g;
 }
 
-template <typename OutT>
+// One token of the fast path: lane = chunk.  W / BR compile-time (0 = read
+// from p): the lane's bit offsets inside a token are then constants, and the
+// token stride (W words of index codes, BR words of radius codes) folds into
+// immediate load offsets when the caller unrolls over tokens.
+template <typename OutT, int W, int BR>
+__device__ __forceinline__ void decode_token_fast(const DecParams& p, const uint32_t* __restrict__ iw,
+                                                  const uint32_t* __restrict__ rw,
+                                                  const uint16_t* __restrict__ sc,
+                                                  const float4* __restrict__ tab, int tt,
+                                                  OutT* __restrict__ o, int lane, uint32_t ncw,
+                                                  float rtop, bool& bad) {
+  const int w = W ? W : p.w, br = BR ? BR : p.br;
+  const uint32_t imask = w == 32 ? 0xffffffffu : ((1u << w) - 1u);
+  const uint32_t rmask = (1u << br) - 1u;
+  const uint32_t bi = (uint32_t)lane * w, bq = (uint32_t)lane * br;
+  const uint32_t* wp = iw + tt * w + (bi >> 5);
+  uint32_t idx = __funnelshift_r(wp[0], wp[1], bi & 31) & imask;
+  const uint32_t* qp = rw + tt * br + (bq >> 5);
+  uint32_t q;
+  if ((BR != 0) && (32 % (BR ? BR : 1) == 0)) q = (qp[0] >> (bq & 31)) & rmask;
+  else q = __funnelshift_r(qp[0], qp[1], bq & 31) & rmask;
+  bad |= idx >= ncw;  // reported once per thread at the end (no branch here)
+  idx = idx < ncw ? idx : 0u;
+  const float rad = (float)q * (__half2float(__ushort_as_half(sc[tt])) * rtop);
+  if constexpr (sizeof(OutT) == 4) {
+    const float4 cw = tab[idx];
+    *reinterpret_cast<float4*>(o) = make_float4(rad * cw.x, rad * cw.y, rad * cw.z, rad * cw.w);
+  } else {
+    // 16-bit outputs gather from the fp16 copy of the table (8-byte entries:
+    // half the shared-memory wavefronts of the fp32 gather, the kernel's
+    // bottleneck); the extra rounding is far below the output's own ulp.
+    const uint2 cw = reinterpret_cast<const uint2*>(tab)[idx];
+    const __half2 c01 = *reinterpret_cast<const __half2*>(&cw.x);
+    const __half2 c23 = *reinterpret_cast<const __half2*>(&cw.y);
+    uint2 ov;
+    if constexpr (std::is_same<OutT, __half>::value) {
+      const __half2 r2 = __float2half2_rn(rad);
+      const __half2 o01 = __hmul2(r2, c01), o23 = __hmul2(r2, c23);
+      ov = make_uint2(*reinterpret_cast<const uint32_t*>(&o01), *reinterpret_cast<const uint32_t*>(&o23));
+    } else {
+      const float2 f01 = __half22float2(c01), f23 = __half22float2(c23);
+      const __nv_bfloat162 o01 = __floats2bfloat162_rn(rad * f01.x, rad * f01.y);
+      const __nv_bfloat162 o23 = __floats2bfloat162_rn(rad * f23.x, rad * f23.y);
+      ov = make_uint2(*reinterpret_cast<const uint32_t*>(&o01), *reinterpret_cast<const uint32_t*>(&o23));
+    }
+    *reinterpret_cast<uint2*>(o) = ov;
+  }
+}
+
+template <typename OutT, int W, int BR>
 __global__ void __launch_bounds__(256) decode_fast_kernel(DecParams p) {
   extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ __align__(8) uint64_t full[kFDStages];
   const int64_t row = blockIdx.y;
   const int h = (int)(row % p.H);
   const int ncw = kGroupOrder * p.S;
-  const int w = p.w, br = p.br;
+  const int w = W ? W : p.w, br = BR ? BR : p.br;
   const FastDecodeGeom g = fd_geom(w, br);
   float4* tab = reinterpret_cast<float4*>(dsm);
   unsigned char* ring = dsm + (size_t)ncw * sizeof(float4);
@@ -207,13 +257,21 @@ __global__ void __launch_bounds__(256) decode_fast_kernel(DecParams p) {
     for (int64_t tile = blockIdx.x; tile < ntile && s < kFDStages; tile += gridDim.x, ++s)
       issue(tile, s);
   }
-  for (int i = tid; i < ncw; i += 256) tab[i] = __ldg(gtab + i);
+  if constexpr (sizeof(OutT) == 4) {
+    for (int i = tid; i < ncw; i += 256) tab[i] = __ldg(gtab + i);
+  } else {
+    uint2* t16 = reinterpret_cast<uint2*>(tab);
+    for (int i = tid; i < ncw; i += 256) {
+      const float4 c = __ldg(gtab + i);
+      const __half2 a = __floats2half2_rn(c.x, c.y), b = __floats2half2_rn(c.z, c.w);
+      t16[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b));
+    }
+  }
   __syncthreads();
 
   const float rtop = 1.0f / (float)((1 << br) - 1);
-  const uint32_t imask = w == 32 ? 0xffffffffu : ((1u << w) - 1u);
-  const uint32_t rmask = (1u << br) - 1u;
   OutT* __restrict__ out = reinterpret_cast<OutT*>(p.out);
+  bool bad = false;
   int k = 0;
   for (int64_t tile = blockIdx.x; tile < ntile; tile += gridDim.x, ++k) {
     const int stage = k % kFDStages;
@@ -223,28 +281,21 @@ __global__ void __launch_bounds__(256) decode_fast_kernel(DecParams p) {
     const uint32_t* rw = reinterpret_cast<const uint32_t*>(s + g.rad_off);
     const uint16_t* sc = reinterpret_cast<const uint16_t*>(s + g.sc_off);
     const int ntok = (int)min((int64_t)kFDTok, p.nt - tile * kFDTok);
-#pragma unroll 4
-    for (int tt = warp; tt < ntok; tt += 8) {
-      const uint32_t bi = (uint32_t)(tt * w * 32 + lane * w);
-      const uint32_t* wp = iw + (bi >> 5);
-      uint32_t idx = __funnelshift_r(wp[0], wp[1], bi & 31) & imask;
-      const uint32_t bq = (uint32_t)(tt * br * 32 + lane * br);
-      const uint32_t* qp = rw + (bq >> 5);
-      const uint32_t q = __funnelshift_r(qp[0], qp[1], bq & 31) & rmask;
-      if (idx >= (uint32_t)ncw) {
-        atomicOr(p.err, HQMQ_DEVERR_INDEX_RANGE);
-        idx = 0;
-      }
-      const float rad = ((float)q * __half2float(__ushort_as_half(sc[tt]))) * rtop;
-      const float4 cw = tab[idx];
-      OutT* o = out + ((row * p.nt + tile * kFDTok + tt) * 128 + 4 * lane);
-      if constexpr (sizeof(OutT) == 4) {
-        *reinterpret_cast<float4*>(o) = make_float4(rad * cw.x, rad * cw.y, rad * cw.z, rad * cw.w);
-      } else {
-        OutT t4[4] = {Out<OutT>::cvt(rad * cw.x), Out<OutT>::cvt(rad * cw.y),
-                      Out<OutT>::cvt(rad * cw.z), Out<OutT>::cvt(rad * cw.w)};
-        *reinterpret_cast<uint2*>(o) = *reinterpret_cast<const uint2*>(t4);
-      }
+    OutT* orow = out + (row * p.nt + tile * kFDTok) * 128 + 4 * lane;
+    if (ntok == kFDTok) {
+      // full tile: warp w decodes tokens w, w+8, ..., w+56 (fully unrolled)
+      const uint32_t* iww = iw + warp * w;
+      const uint32_t* rww = rw + warp * br;
+      const uint16_t* scw = sc + warp;
+      OutT* ow = orow + warp * 128;
+#pragma unroll
+      for (int i = 0; i < kFDTok / 8; ++i)
+        decode_token_fast<OutT, W, BR>(p, iww, rww, scw, tab, 8 * i, ow + 8 * i * 128, lane,
+                                       (uint32_t)ncw, rtop, bad);
+    } else {
+      for (int tt = warp; tt < ntok; tt += 8)
+        decode_token_fast<OutT, W, BR>(p, iw, rw, sc, tab, tt, orow + tt * 128, lane,
+                                       (uint32_t)ncw, rtop, bad);
     }
     __syncthreads();  // every warp is done with this stage
     if (tid == 0) {
@@ -252,6 +303,7 @@ __global__ void __launch_bounds__(256) decode_fast_kernel(DecParams p) {
       if (nxt < ntile) issue(nxt, stage);
     }
   }
+  if (bad) atomicOr(p.err, HQMQ_DEVERR_INDEX_RANGE);
 }
 
 // Bit-exact fp64 decode: ((q * sigma_w) / top) * codeword (codec.py:315-320).
@@ -411,17 +463,21 @@ int launch_decode(DecParams& p, const hqmq_decode_args* a, cudaStream_t st) {
   if (fast) {
     const FastDecodeGeom g = fd_geom(p.w, p.br);
     const size_t fsmem = smem + (size_t)kFDStages * g.stage_bytes;
-    static thread_local bool fset = false;
-    if (!fset) {
-      cudaFuncSetAttribute(decode_fast_kernel<OutT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           200 * 1024);
-      fset = true;
+    // (index_bits, radius_bits) instances with compile-time stream geometry
+    void (*kern)(DecParams) = decode_fast_kernel<OutT, 0, 0>;
+    switch (p.w * 16 + p.br) {
+      case 9 * 16 + 4: kern = decode_fast_kernel<OutT, 9, 4>; break;    // S = 16
+      case 11 * 16 + 4: kern = decode_fast_kernel<OutT, 11, 4>; break;  // S = 64
+      case 13 * 16 + 4: kern = decode_fast_kernel<OutT, 13, 4>; break;  // S = 256
+      case 11 * 16 + 6: kern = decode_fast_kernel<OutT, 11, 6>; break;  // Qwen b_r 6
+      default: break;
     }
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     const int64_t ntile = ceil_div(p.nt, kFDTok);
     const int per_sm = std::max<int>(1, std::min<int>(8, (int)((200 * 1024) / fsmem)));
     const int64_t want = std::max<int64_t>(1, ceil_div((int64_t)148 * per_sm, rows));
     const int64_t bx = std::max<int64_t>(1, std::min<int64_t>(want, ntile));
-    decode_fast_kernel<OutT><<<dim3((unsigned)bx, (unsigned)rows), 256, fsmem, st>>>(p);
+    kern<<<dim3((unsigned)bx, (unsigned)rows), 256, fsmem, st>>>(p);
     return check();
   }
   const int64_t nck = p.nt * p.C;
