@@ -138,6 +138,27 @@ __device__ __forceinline__ Dir2 fast_dir(const InT (&v)[4], const double (&x)[4]
   return d;
 }
 
+// fast_dir for the search-only pass: the exact norm is computed only on the
+// (rare) slow path, where the fp32 sum of squares leaves its safe range.
+template <typename InT>
+__device__ __forceinline__ Dir2 fast_dir_lazy_norm(const InT (&v)[4], double (&x)[4]) {
+  const float x0 = In<InT>::f(v[0]), x1 = In<InT>::f(v[1]);
+  const float x2 = In<InT>::f(v[2]), x3 = In<InT>::f(v[3]);
+  const float ss = fmaf(x3, x3, fmaf(x2, x2, fmaf(x1, x1, x0 * x0)));
+  if (ss >= 1e-30f && ss <= 1e30f) {
+    const float inv = rsqrtf(ss);
+    Dir2 d;
+    d.a = make_float2(x0 * inv, x0 * inv);
+    d.b = make_float2(x1 * inv, x1 * inv);
+    d.c = make_float2(x2 * inv, x2 * inv);
+    d.d = make_float2(x3 * inv, x3 * inv);
+    return d;
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) x[i] = In<InT>::d(v[i]);
+  return fast_dir(v, x, exact_norm(x));
+}
+
 // Closed-form primary index of the best element of a coset and the runner-up
 // score inside that coset (hurwitz.py:10-14,28-36 canonical order).
 __device__ __forceinline__ void coset_resolve(float2 wx, float2 yz, int& p, float& top,
@@ -481,8 +502,13 @@ __device__ __forceinline__ double warp_max_f64(double v) {
   return v;
 }
 
-template <typename InT, int kWT, int kMinB>
+// kMode: 0 = fused (one pass), 1 = prep only (exact norms / flags / scales /
+// quanta / radius stream / payloads), 2 = search only (fp32 directions from
+// the input, S-loop, certification + exact fixup, index stream).  The split
+// form keeps the FMA-bound search kernel free of the latency-bound fp64 work.
+template <typename InT, int kWT, int kMinB, int kMode>
 __global__ void __launch_bounds__(kWThreads, kMinB) encode_warp_kernel(EncParams p) {
+  constexpr bool kPrep = kMode != 2, kSearch = kMode != 1;
   extern __shared__ float4 tab_s[];  // [S][4]
   __shared__ uint32_t stage_i[kWWarps][kWT * 32 + 2];
   __shared__ uint32_t stage_r[kWWarps][kWT * 8 + 2];
@@ -493,7 +519,8 @@ __global__ void __launch_bounds__(kWThreads, kMinB) encode_warp_kernel(EncParams
   const int S = p.S, w = p.w, br = p.br;
   const float4* __restrict__ rot = p.rot + (int64_t)h * S * 4;
   const double* __restrict__ joint = p.joint + (int64_t)h * kGroupOrder * S * 4;
-  for (int i = threadIdx.x; i < S * 4; i += kWThreads) tab_s[i] = __ldg(rot + i);
+  if (kSearch)
+    for (int i = threadIdx.x; i < S * 4; i += kWThreads) tab_s[i] = __ldg(rot + i);
   for (int i = lane; i < kWT * 32 + 2; i += 32) stage_i[warp][i] = 0u;
   for (int i = lane; i < kWT * 8 + 2; i += 32) stage_r[warp][i] = 0u;
   __syncthreads();
@@ -529,56 +556,80 @@ __global__ void __launch_bounds__(kWThreads, kMinB) encode_warp_kernel(EncParams
     const int64_t tok0 = row * p.T + t0;
     const uint64_t P0 = ext ? (uint64_t)p.tokoff[tok0] : (uint64_t)tok0 * 32;
 
-    // ---- exact fp64 prologue: norms, flags, scales, quanta, payloads, fp32 dirs
     uint32_t fmask[kWT];
     uint32_t qpack = 0, livebits = 0, coded_run = 0;
     float4 u4[kWT];
+    if constexpr (!kPrep) {
+      // ---- search-only prologue: flags from the prep pass, fp32 directions
 #pragma unroll
-    for (int j = 0; j < kWT; ++j) {
-      const InT* v = reinterpret_cast<const InT*>(&raw[j]);
-      InT vv[4] = {v[0], v[1], v[2], v[3]};
-      double x[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) x[i] = In<InT>::d(vv[i]);
-      const double r = exact_norm(x);
-      const bool valid = j < ntok;
-      const bool fl = valid && r > thr;
-      fmask[j] = __ballot_sync(0xffffffffu, fl);
-      const bool live = valid && !fl && r > 0.0;
-      double sg = warp_max_f64(fl ? 0.0 : r);
-      if (!(sg > 0.0)) sg = 1.0;
-      const __half hs = __double2half(sg);
-      const double sw = (double)__half2float(hs);
-      if (valid && lane == j) {
-        p.scales[tok0 + j] = __half_as_ushort(hs);
-        if (!(sw > 0.0)) atomicOr(p.err, HQMQ_DEVERR_SIGMA_NONPOSITIVE);
-      }
-      if (valid && !fl) qpack |= exact_quantum(r, sw, top) << (8 * j);
-      livebits |= (live ? 1u : 0u) << j;
-      u4[j] = make_float4(0.f, 0.f, 0.f, 0.f);
-      if (live) {
-        const Dir2 d = fast_dir(vv, x, r);
-        u4[j] = make_float4(d.a.x, d.b.x, d.c.x, d.d.x);
-      }
-      if (ext && valid) {
-        if (fl) {
-          const uint64_t rel = coded_run + __popc(~fmask[j] & lanemask_lt);
-          const uint64_t prow = (uint64_t)(tok0 + j) * 32 + lane - (P0 + rel);
-          if (prow < (uint64_t)p.payload_capacity) {
-            ushort4 hv;
-            hv.x = __half_as_ushort(__double2half(x[0]));
-            hv.y = __half_as_ushort(__double2half(x[1]));
-            hv.z = __half_as_ushort(__double2half(x[2]));
-            hv.w = __half_as_ushort(__double2half(x[3]));
-            reinterpret_cast<ushort4*>(p.payloads)[prow] = hv;
-          }
+      for (int j = 0; j < kWT; ++j) {
+        const InT* v = reinterpret_cast<const InT*>(&raw[j]);
+        InT vv[4] = {v[0], v[1], v[2], v[3]};
+        const bool valid = j < ntok;
+        fmask[j] = (ext && valid) ? __ldg(p.flagw + tok0 + j) : 0u;
+        const bool fl = (fmask[j] >> lane) & 1u;
+        const bool nz = (raw[j].x | raw[j].y) & 0x7fff7fffu;  // any nonzero element
+        const bool live = valid && !fl && nz;
+        livebits |= (live ? 1u : 0u) << j;
+        u4[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (live) {
+          double x[4] = {0.0, 0.0, 0.0, 0.0};
+          const Dir2 d = fast_dir_lazy_norm(vv, x);
+          u4[j] = make_float4(d.a.x, d.b.x, d.c.x, d.d.x);
         }
-        if (lane == j) p.flagw[tok0 + j] = fmask[j];
-        coded_run += __popc(~fmask[j]);
       }
+    } else {
+      // ---- exact fp64 prologue: norms, flags, scales, quanta, payloads, fp32 dirs
+  #pragma unroll
+      for (int j = 0; j < kWT; ++j) {
+        const InT* v = reinterpret_cast<const InT*>(&raw[j]);
+        InT vv[4] = {v[0], v[1], v[2], v[3]};
+        double x[4];
+  #pragma unroll
+        for (int i = 0; i < 4; ++i) x[i] = In<InT>::d(vv[i]);
+        const double r = exact_norm(x);
+        const bool valid = j < ntok;
+        const bool fl = valid && r > thr;
+        fmask[j] = __ballot_sync(0xffffffffu, fl);
+        const bool live = valid && !fl && r > 0.0;
+        double sg = warp_max_f64(fl ? 0.0 : r);
+        if (!(sg > 0.0)) sg = 1.0;
+        const __half hs = __double2half(sg);
+        const double sw = (double)__half2float(hs);
+        if (valid && lane == j) {
+          p.scales[tok0 + j] = __half_as_ushort(hs);
+          if (!(sw > 0.0)) atomicOr(p.err, HQMQ_DEVERR_SIGMA_NONPOSITIVE);
+        }
+        if (valid && !fl) qpack |= exact_quantum(r, sw, top) << (8 * j);
+        livebits |= (live ? 1u : 0u) << j;
+        u4[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (kSearch && live) {
+          const Dir2 d = fast_dir(vv, x, r);
+          u4[j] = make_float4(d.a.x, d.b.x, d.c.x, d.d.x);
+        }
+        if (ext && valid) {
+          if (fl) {
+            const uint64_t rel = coded_run + __popc(~fmask[j] & lanemask_lt);
+            const uint64_t prow = (uint64_t)(tok0 + j) * 32 + lane - (P0 + rel);
+            if (prow < (uint64_t)p.payload_capacity) {
+              ushort4 hv;
+              hv.x = __half_as_ushort(__double2half(x[0]));
+              hv.y = __half_as_ushort(__double2half(x[1]));
+              hv.z = __half_as_ushort(__double2half(x[2]));
+              hv.w = __half_as_ushort(__double2half(x[3]));
+              reinterpret_cast<ushort4*>(p.payloads)[prow] = hv;
+            }
+          }
+          if (lane == j) p.flagw[tok0 + j] = fmask[j];
+          coded_run += __popc(~fmask[j]);
+        }
+      }
+
     }
 
     // ---- fp32 closed-form search over the S cosets (table broadcast from smem)
+    int idx[kWT];
+    if constexpr (kSearch) {
     float best[kWT], second[kWT];
     int bs[kWT];
 #pragma unroll
@@ -609,7 +660,6 @@ __global__ void __launch_bounds__(kWThreads, kMinB) encode_warp_kernel(EncParams
     }
 
     // ---- certification + warp-cooperative exact fixup (input re-read from L2)
-    int idx[kWT];
 #pragma unroll
     for (int j = 0; j < kWT; ++j) {
       idx[j] = 0;
@@ -648,6 +698,7 @@ __global__ void __launch_bounds__(kWThreads, kMinB) encode_warp_kernel(EncParams
         if (lane == L) idx[j] = ex;
       }
     }
+    }
 
     // ---- pack the index / radius streams
     uint32_t coded_before = 0;
@@ -659,13 +710,13 @@ __global__ void __launch_bounds__(kWThreads, kMinB) encode_warp_kernel(EncParams
       const bool fl = (fmask[j] >> lane) & 1u;
       const uint32_t rel = coded_before + __popc(~fmask[j] & lanemask_lt);
       if (!fl) {
-        stage_bits(st_i, (uint64_t)lbi + (uint64_t)rel * w, (uint32_t)idx[j], w);
-        stage_bits(st_r, (uint64_t)lbr + (uint64_t)rel * br, (qpack >> (8 * j)) & 0xffu, br);
+        if constexpr (kSearch) stage_bits(st_i, (uint64_t)lbi + (uint64_t)rel * w, (uint32_t)idx[j], w);
+        if constexpr (kPrep) stage_bits(st_r, (uint64_t)lbr + (uint64_t)rel * br, (qpack >> (8 * j)) & 0xffu, br);
       }
       coded_before += __popc(~fmask[j]);
     }
     __syncwarp();
-    {
+    if constexpr (kSearch) {
       // no extraction: words are token-aligned and fully owned -> plain stores;
       // with extraction the two edge words may be shared with neighbours -> OR.
       const uint64_t end = lbi + (uint64_t)coded_before * w;
@@ -679,7 +730,7 @@ __global__ void __launch_bounds__(kWThreads, kMinB) encode_warp_kernel(EncParams
         st_i[i] = 0u;
       }
     }
-    {
+    if constexpr (kPrep) {
       const uint64_t end = lbr + (uint64_t)coded_before * br;
       const uint32_t nw = (uint32_t)((end + 31) >> 5);
       const uint64_t gw0 = (P0 * (uint64_t)br) >> 5;
@@ -1155,10 +1206,21 @@ int launch_encode(const hqmq_encode_args* a, const Layout& L, cudaStream_t st) {
         kern<<<dim3((unsigned)bx, (unsigned)L.rows), kWThreads, smem, st>>>(p);
       };
       switch (variant) {
-        case 1: launch(encode_warp_kernel<InT, 4, 3>, 4, 3); break;
-        case 2: launch(encode_warp_kernel<InT, 8, 2>, 8, 2); break;
-        case 3: launch(encode_warp_kernel<InT, 8, 1>, 8, 1); break;
-        default: launch(encode_warp_kernel<InT, 4, 2>, 4, 2); break;
+        case 1:  // fused single pass
+          launch(encode_warp_kernel<InT, 4, 2, 0>, 4, 2);
+          break;
+        case 2:  // split, search at 3 CTAs/SM
+          launch(encode_warp_kernel<InT, 4, 4, 1>, 4, 4);
+          launch(encode_warp_kernel<InT, 4, 3, 2>, 4, 3);
+          break;
+        case 3:  // split, search kWT 8
+          launch(encode_warp_kernel<InT, 4, 4, 1>, 4, 4);
+          launch(encode_warp_kernel<InT, 8, 2, 2>, 8, 2);
+          break;
+        default:  // split: prep pass, then the FMA-bound search pass
+          launch(encode_warp_kernel<InT, 4, 4, 1>, 4, 4);
+          launch(encode_warp_kernel<InT, 4, 2, 2>, 4, 2);
+          break;
       }
       e = cudaGetLastError();
       return e == cudaSuccess ? HQMQ_OK : cuda_fail(e);
