@@ -155,6 +155,8 @@ typedef struct {
   const double* joint_f64;
   void* out;
   uint32_t* error_word;
+  const uint16_t* joint_f16; /* optional [heads][24*S][4] fp16 copy of the table
+                                for 16-bit outputs (NULL: converted in-kernel) */
 } hqmq_decode_args;
 
 int hqmq_decode(const hqmq_decode_args* args, void* stream);
@@ -201,7 +203,8 @@ typedef struct {
   const uint32_t* flag_words;
   const uint16_t* payloads;
   const uint32_t* token_offsets;
-  const float* joint_f32; /* [kv_heads][24*S][4] */
+  const float* joint_f32;  /* [kv_heads][24*S][4] */
+  const uint16_t* joint_f16; /* optional fp16 copy (NULL: converted in-kernel) */
 } hqmq_packed_view;
 
 typedef struct {

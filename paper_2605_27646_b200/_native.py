@@ -55,6 +55,7 @@ class DecodeArgs(ctypes.Structure):
         ("flag_words", c_vp), ("payloads", c_vp), ("token_offsets", c_vp),
         ("joint_f32", c_vp), ("joint_f64", c_vp),
         ("out", c_vp), ("error_word", c_vp),
+        ("joint_f16", c_vp),
     ]
 
 
@@ -63,6 +64,7 @@ class PackedView(ctypes.Structure):
         ("scales", c_vp), ("index_words", c_vp), ("radius_words", c_vp),
         ("flag_words", c_vp), ("payloads", c_vp), ("token_offsets", c_vp),
         ("joint_f32", c_vp),
+        ("joint_f16", c_vp),
     ]
 
 

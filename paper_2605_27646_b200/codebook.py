@@ -20,7 +20,9 @@ them resident in HBM:
 * rot_f32   (S, 16) fp32 — conj(secondary) as 8 float2 pairs for the FFMA2
   rotation v = u (x) conj(q_s) of the encode search;
 * joint_f64 (24S, 4) fp64 — the reference table, for exact fixup / fp64 decode;
-* joint_f32 (24S, 4) fp32 — the same rounded to fp32, for decode / attention.
+* joint_f32 (24S, 4) fp32 — the same rounded to fp32, for decode / attention;
+* joint_f16 (24S, 4) fp16 — for 16-bit decode outputs and the tensor-core
+  attention (8-byte smem gathers).
 """
 
 from __future__ import annotations
@@ -213,6 +215,7 @@ class CodebookBank:
                 "rot_f32": torch.from_numpy(np.ascontiguousarray(rot)).to(device),
                 "joint_f64": torch.from_numpy(np.ascontiguousarray(j64)).to(device),
                 "joint_f32": torch.from_numpy(np.ascontiguousarray(j64.astype(np.float32))).to(device),
+                "joint_f16": torch.from_numpy(np.ascontiguousarray(j64.astype(np.float16))).to(device),
             }
             self._dev[key] = found
         return found

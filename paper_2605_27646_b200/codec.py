@@ -207,7 +207,7 @@ class QuantizedTensor:
         return self._unpack()[2].clone()
 
     # ----------------------------------------------------------- kernels
-    def _decode_args(self, start, stop, out_dtype, out, err, j32, j64):
+    def _decode_args(self, start, stop, out_dtype, out, err, j32, j64, j16=None):
         s, c = self.shape, self.config
         a = nat.DecodeArgs()
         a.batch, a.heads, a.tokens, a.head_dim = s.batch, s.heads, s.tokens, s.head_dim
@@ -222,6 +222,7 @@ class QuantizedTensor:
         a.token_offsets = self.token_offsets.data_ptr() if self.token_offsets is not None else None
         a.joint_f32 = j32.data_ptr() if j32 is not None else None
         a.joint_f64 = j64.data_ptr() if j64 is not None else None
+        a.joint_f16 = j16.data_ptr() if j16 is not None else None
         a.out = out.data_ptr() if out is not None else None
         a.error_word = err.data_ptr() if err is not None else None
         return a
@@ -237,6 +238,7 @@ class QuantizedTensor:
         v.payloads = self._payload_buf.data_ptr() if self.flag_words is not None else None
         v.token_offsets = self.token_offsets.data_ptr() if self.token_offsets is not None else None
         v.joint_f32 = tabs["joint_f32"].data_ptr()
+        v.joint_f16 = tabs["joint_f16"].data_ptr()
         return v
 
     # ---------------------------------------------------------- sections
@@ -444,7 +446,7 @@ def decode_token_range(packed: QuantizedTensor, bank: CodebookBank, start: int, 
     tabs = bank.device_tables(packed.layer, packed.head_base, s.heads, packed.role, dev)
     err = torch.zeros(1, dtype=torch.int32, device=dev)
     args = packed._decode_args(start, stop, code, out, err,
-                               tabs["joint_f32"], tabs["joint_f64"])
+                               tabs["joint_f32"], tabs["joint_f64"], tabs["joint_f16"])
     nat.check(nat.lib().hqmq_decode(ctypes.byref(args), nat.stream_handle(dev)), "hqmq_decode")
     if check and int(err.item()) & nat.DEVERR_INDEX:
         raise CorruptData("codeword index out of range")

@@ -37,6 +37,7 @@ struct AttView {
   const uint16_t* payloads;
   const uint32_t* tokoff;
   const float4* table;  // [Hkv][24S]
+  const uint2* table16;  // optional fp16 copy [Hkv][24S]
 };
 
 struct AttParams {
@@ -361,10 +362,12 @@ template <int W, int BR>
 __global__ void __launch_bounds__(kMThreads, 2) attention_mma_kernel(AttParams p) {
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ __align__(8) uint64_t full[kMStages];
+  __shared__ __align__(8) uint64_t tab_bar;
   __shared__ unsigned int released[kMStages];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ncw = kGroupOrder * p.S;
   constexpr int w = W, br = BR;
+  const bool tab_tma = p.k.table16 != nullptr && p.v.table16 != nullptr;
   const RingGeom gm = ring_geom(w, br);
   uint2* ktab = reinterpret_cast<uint2*>(sm);
   uint2* vtab = ktab + ncw;
@@ -382,6 +385,7 @@ __global__ void __launch_bounds__(kMThreads, 2) attention_mma_kernel(AttParams p
       mbar_init(&full[s], 1);
       released[s] = 0u;
     }
+    mbar_init(&tab_bar, 1);
     fence_mbar_init();
   }
   __syncthreads();
@@ -410,16 +414,28 @@ __global__ void __launch_bounds__(kMThreads, 2) attention_mma_kernel(AttParams p
     }
   };
   // the first tiles stream in while the joint tables are converted to fp16
-  if (tid == 0)
+  if (tid == 0) {
+    if (tab_tma) {  // fp16 tables by TMA, beside the first tiles
+      const uint32_t tb = (uint32_t)ncw * 8u;
+      fence_proxy_async();
+      mbar_arrive_expect_tx(&tab_bar, 2 * tb);
+      bulk_g2s(ktab, p.k.table16 + hkv * ncw, tb, &tab_bar);
+      bulk_g2s(vtab, p.v.table16 + hkv * ncw, tb, &tab_bar);
+    }
     for (int s = 0; s < kMStages && s < ntile; ++s) issue(s, s);
-  const float4* gk = p.k.table + hkv * ncw;
-  const float4* gv = p.v.table + hkv * ncw;
-  for (int i = tid; i < ncw; i += kMThreads) {
-    const float4 a = __ldg(gk + i), c = __ldg(gv + i);
-    ktab[i] = make_uint2(pack_half2(a.x, a.y), pack_half2(a.z, a.w));
-    vtab[i] = make_uint2(pack_half2(c.x, c.y), pack_half2(c.z, c.w));
   }
-  __syncthreads();
+  if (tab_tma) {
+    mbar_wait(&tab_bar, 0u);
+  } else {
+    const float4* gk = p.k.table + hkv * ncw;
+    const float4* gv = p.v.table + hkv * ncw;
+    for (int i = tid; i < ncw; i += kMThreads) {
+      const float4 a = __ldg(gk + i), c = __ldg(gv + i);
+      ktab[i] = make_uint2(pack_half2(a.x, a.y), pack_half2(a.z, a.w));
+      vtab[i] = make_uint2(pack_half2(c.x, c.y), pack_half2(c.z, c.w));
+    }
+    __syncthreads();
+  }
 
   const int g4 = lane >> 2, t4 = lane & 3;  // mma fragment coordinates
   const uint32_t cwmax = (uint32_t)ncw - 1u;
@@ -691,6 +707,7 @@ int hqmq_attention_decode(const hqmq_attention_args* a, void* stream) {
     o.scales = v.scales; o.idxw = v.index_words; o.radw = v.radius_words; o.flagw = v.flag_words;
     o.payloads = v.payloads; o.tokoff = v.token_offsets;
     o.table = reinterpret_cast<const float4*>(v.joint_f32);
+    o.table16 = reinterpret_cast<const uint2*>(v.joint_f16);
     return o;
   };
   p.k = view(a->k);

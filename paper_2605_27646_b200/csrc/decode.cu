@@ -53,6 +53,7 @@ struct DecParams {
   const uint16_t* payloads;
   const uint32_t* tokoff;
   const void* table;  // float4 [H][24S] or double [H][24S][4]
+  const uint2* table16;  // optional fp16 [H][24S] (16-bit outputs)
   void* out;
   uint32_t* err;
 };
@@ -223,6 +224,8 @@ template <typename OutT, int W, int BR>
 __global__ void __launch_bounds__(256) decode_fast_kernel(DecParams p) {
   extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ __align__(8) uint64_t full[kFDStages];
+  __shared__ __align__(8) uint64_t tab_bar;
+  __shared__ unsigned int released[kFDStages];
   const int64_t row = blockIdx.y;
   const int h = (int)(row % p.H);
   const int ncw = kGroupOrder * p.S;
@@ -234,6 +237,8 @@ __global__ void __launch_bounds__(256) decode_fast_kernel(DecParams p) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t ntile = ceil_div(p.nt, kFDTok);
   const int64_t tok_base = row * p.T + p.t0;  // first token of the range in this row
+  constexpr bool k16 = sizeof(OutT) == 2;
+  const bool tab_tma = k16 && p.table16 != nullptr;
 
   auto issue = [&](int64_t tile, int stage) {
     const int64_t t = tok_base + tile * kFDTok;
@@ -248,26 +253,39 @@ __global__ void __launch_bounds__(256) decode_fast_kernel(DecParams p) {
   };
 
   if (tid == 0) {
-    for (int s = 0; s < kFDStages; ++s) mbar_init(&full[s], 1);
+    for (int s = 0; s < kFDStages; ++s) {
+      mbar_init(&full[s], 1);
+      released[s] = 0u;
+    }
+    mbar_init(&tab_bar, 1);
     fence_mbar_init();
   }
   __syncthreads();
   if (tid == 0) {
+    if (tab_tma) {  // the fp16 table arrives by TMA beside the first tiles
+      const uint32_t tb = (uint32_t)ncw * 8u;
+      fence_proxy_async();
+      mbar_arrive_expect_tx(&tab_bar, tb);
+      bulk_g2s(tab, p.table16 + (int64_t)h * ncw, tb, &tab_bar);
+    }
     int s = 0;
     for (int64_t tile = blockIdx.x; tile < ntile && s < kFDStages; tile += gridDim.x, ++s)
       issue(tile, s);
   }
-  if constexpr (sizeof(OutT) == 4) {
+  if constexpr (!k16) {
     for (int i = tid; i < ncw; i += 256) tab[i] = __ldg(gtab + i);
-  } else {
+    __syncthreads();
+  } else if (!tab_tma) {
     uint2* t16 = reinterpret_cast<uint2*>(tab);
     for (int i = tid; i < ncw; i += 256) {
       const float4 c = __ldg(gtab + i);
       const __half2 a = __floats2half2_rn(c.x, c.y), b = __floats2half2_rn(c.z, c.w);
       t16[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b));
     }
+    __syncthreads();
+  } else {
+    mbar_wait(&tab_bar, 0u);
   }
-  __syncthreads();
 
   const float rtop = 1.0f / (float)((1 << br) - 1);
   OutT* __restrict__ out = reinterpret_cast<OutT*>(p.out);
@@ -297,10 +315,15 @@ __global__ void __launch_bounds__(256) decode_fast_kernel(DecParams p) {
         decode_token_fast<OutT, W, BR>(p, iw, rw, sc, tab, tt, orow + tt * 128, lane,
                                        (uint32_t)ncw, rtop, bad);
     }
-    __syncthreads();  // every warp is done with this stage
-    if (tid == 0) {
-      const int64_t nxt = tile + (int64_t)kFDStages * gridDim.x;
-      if (nxt < ntile) issue(nxt, stage);
+    // release the stage without a block barrier: the last warp done with it
+    // issues the tile kFDStages ahead into it
+    __syncwarp();
+    if (lane == 0) {
+      if (atomicAdd(&released[stage], 1u) == 7u) {
+        released[stage] = 0u;
+        const int64_t nxt = tile + (int64_t)kFDStages * gridDim.x;
+        if (nxt < ntile) issue(nxt, stage);
+      }
     }
   }
   if (bad) atomicOr(p.err, HQMQ_DEVERR_INDEX_RANGE);
@@ -446,6 +469,7 @@ bool fill(const hqmq_decode_args* a, DecParams& p, bool need_range) {
   p.scales = a->scales; p.idxw = a->index_words; p.radw = a->radius_words;
   p.flagw = a->flag_words; p.payloads = a->payloads; p.tokoff = a->token_offsets;
   p.out = a->out; p.err = a->error_word;
+  p.table16 = reinterpret_cast<const uint2*>(a->joint_f16);
   return true;
 }
 

@@ -54,8 +54,8 @@ def test_struct_layouts_match_header():
     assert ctypes.sizeof(_native.EncodeArgs) == 200
     assert _native.EncodeArgs.outlier_multiplier.offset == 48
     assert _native.EncodeArgs.data.offset == 64
-    assert ctypes.sizeof(_native.DecodeArgs) == 144
-    assert ctypes.sizeof(_native.PackedView) == 56
+    assert ctypes.sizeof(_native.DecodeArgs) == 152
+    assert ctypes.sizeof(_native.PackedView) == 64
     assert _native.AttentionArgs.q.offset == 72
 
 
