@@ -329,6 +329,112 @@ __global__ void __launch_bounds__(256) decode_fast_kernel(DecParams p) {
   if (bad) atomicOr(p.err, HQMQ_DEVERR_INDEX_RANGE);
 }
 
+// Med3x layout (head_dim 128, flag bitmap present): a token's 32 chunks own
+// exactly flag word `tok`, and its coded chunks start at token_offsets[tok]
+// in the index / radius streams.  Warp = token, lane = chunk; the warp's code
+// reads hit one contiguous ~w-word span (L1), flagged lanes read their fp16
+// payload row instead.  kU tokens per warp iteration for memory parallelism.
+template <typename OutT>
+__global__ void __launch_bounds__(256) decode_flag_kernel(DecParams p) {
+  extern __shared__ __align__(128) unsigned char dsm[];
+  __shared__ __align__(8) uint64_t tab_bar;
+  constexpr int kU = 4;
+  const int64_t row = blockIdx.y;
+  const int h = (int)(row % p.H);
+  const int ncw = kGroupOrder * p.S;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr bool k16 = sizeof(OutT) == 2;
+  float4* tab = reinterpret_cast<float4*>(dsm);
+  const float4* __restrict__ gtab = reinterpret_cast<const float4*>(p.table) + (int64_t)h * ncw;
+  const bool tab_tma = k16 && p.table16 != nullptr;
+  if (tid == 0) {
+    mbar_init(&tab_bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tab_tma) {
+    if (tid == 0) {
+      const uint32_t tb = (uint32_t)ncw * 8u;
+      fence_proxy_async();
+      mbar_arrive_expect_tx(&tab_bar, tb);
+      bulk_g2s(tab, p.table16 + (int64_t)h * ncw, tb, &tab_bar);
+    }
+    mbar_wait(&tab_bar, 0u);
+  } else if constexpr (k16) {
+    uint2* t16 = reinterpret_cast<uint2*>(tab);
+    for (int i = tid; i < ncw; i += 256) {
+      const float4 c = __ldg(gtab + i);
+      const __half2 a = __floats2half2_rn(c.x, c.y), b = __floats2half2_rn(c.z, c.w);
+      t16[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b));
+    }
+    __syncthreads();
+  } else {
+    for (int i = tid; i < ncw; i += 256) tab[i] = __ldg(gtab + i);
+    __syncthreads();
+  }
+  const int w = p.w, br = p.br;
+  const uint32_t imask = w == 32 ? 0xffffffffu : ((1u << w) - 1u);
+  const uint32_t rmask = (1u << br) - 1u;
+  const float rtop = 1.0f / (float)((1 << br) - 1);
+  const uint32_t lt = (1u << lane) - 1u;
+  OutT* __restrict__ out = reinterpret_cast<OutT*>(p.out);
+  bool bad = false;
+  const int64_t stride = (int64_t)gridDim.x * 8 * kU;
+  for (int64_t t0 = ((int64_t)blockIdx.x * 8 + warp) * kU; t0 < p.nt; t0 += stride) {
+    uint32_t fw[kU], off[kU];
+    uint16_t scl[kU];
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t tt = min(t0 + u, p.nt - 1);
+      const int64_t tok = row * p.T + p.t0 + tt;
+      fw[u] = __ldg(p.flagw + tok);
+      off[u] = __ldg(p.tokoff + tok);
+      scl[u] = __ldg(p.scales + tok);
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      const int64_t tt = t0 + u;
+      if (tt >= p.nt) break;
+      const int64_t tok = row * p.T + p.t0 + tt;
+      const bool fl = (fw[u] >> lane) & 1u;
+      const uint64_t pos = (uint64_t)off[u] + __popc(~fw[u] & lt);
+      float v[4];
+      if (!fl) {
+        uint32_t idx = read_bits(p.idxw, pos * (uint64_t)w, w) & imask;
+        const uint32_t q = read_bits(p.radw, pos * (uint64_t)br, br) & rmask;
+        bad |= idx >= (uint32_t)ncw;
+        idx = idx < (uint32_t)ncw ? idx : 0u;
+        const float rad = (float)q * (__half2float(__ushort_as_half(scl[u])) * rtop);
+        if constexpr (k16) {
+          const uint2 cw = reinterpret_cast<const uint2*>(tab)[idx];
+          const float2 c01 = __half22float2(*reinterpret_cast<const __half2*>(&cw.x));
+          const float2 c23 = __half22float2(*reinterpret_cast<const __half2*>(&cw.y));
+          v[0] = rad * c01.x; v[1] = rad * c01.y; v[2] = rad * c23.x; v[3] = rad * c23.y;
+        } else {
+          const float4 cw = tab[idx];
+          v[0] = rad * cw.x; v[1] = rad * cw.y; v[2] = rad * cw.z; v[3] = rad * cw.w;
+        }
+      } else {
+        const uint64_t prow = (uint64_t)tok * 32 + lane - pos;
+        const ushort4 hv = __ldg(reinterpret_cast<const ushort4*>(p.payloads) + prow);
+        v[0] = __half2float(__ushort_as_half(hv.x));
+        v[1] = __half2float(__ushort_as_half(hv.y));
+        v[2] = __half2float(__ushort_as_half(hv.z));
+        v[3] = __half2float(__ushort_as_half(hv.w));
+      }
+      OutT* o = out + (row * p.nt + tt) * 128 + 4 * lane;
+      if constexpr (sizeof(OutT) == 4) {
+        *reinterpret_cast<float4*>(o) = make_float4(v[0], v[1], v[2], v[3]);
+      } else {
+        OutT t4[4] = {Out<OutT>::cvt(v[0]), Out<OutT>::cvt(v[1]), Out<OutT>::cvt(v[2]),
+                      Out<OutT>::cvt(v[3])};
+        *reinterpret_cast<uint2*>(o) = *reinterpret_cast<const uint2*>(t4);
+      }
+    }
+  }
+  if (bad) atomicOr(p.err, HQMQ_DEVERR_INDEX_RANGE);
+}
+
 // Bit-exact fp64 decode: ((q * sigma_w) / top) * codeword (codec.py:315-320).
 __global__ void __launch_bounds__(kDecThreads) decode_f64_kernel(DecParams p) {
   const int64_t row = blockIdx.y;
@@ -481,6 +587,15 @@ int launch_decode(DecParams& p, const hqmq_decode_args* a, cudaStream_t st) {
   p.table = a->joint_f32;
   p.aligned4 = (p.D % 4 == 0) && (reinterpret_cast<uintptr_t>(a->out) % (4 * sizeof(OutT)) == 0);
   auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  if (p.D == 128 && p.flagw && p.tokoff && p.payloads && use_smem && p.aligned4) {
+    const int64_t nwt = ceil_div(p.nt, 32);  // 8 warps x 4 tokens per CTA step
+    const int64_t want = std::max<int64_t>(1, ceil_div((int64_t)148 * 4, rows));
+    const int64_t bx = std::max<int64_t>(1, std::min<int64_t>(want, nwt));
+    cudaFuncSetAttribute(decode_flag_kernel<OutT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kDecSmemLimit);
+    decode_flag_kernel<OutT><<<dim3((unsigned)bx, (unsigned)rows), 256, smem, st>>>(p);
+    return check();
+  }
   const bool fast = p.D == 128 && !p.flagw && use_smem && p.aligned4 && p.T % 8 == 0 &&
                     p.t0 % 8 == 0 && p.nt % 8 == 0 && al16(p.idxw) && al16(p.radw) &&
                     al16(p.scales);

@@ -43,6 +43,17 @@ constexpr int kSBlock = 512;                      // secondaries per smem stage
 // unit directions, SURVEY.md §7 hard part 1) with a further 3x safety factor.
 constexpr float kDelta = 6e-6f;
 
+// r > thr for r = sqrt_rn(s), decided on s away from thr^2 and exactly near it
+// (sqrt_rn is monotone, so the reference's r-comparisons are s-comparisons
+// except within rounding distance of the boundary).
+__device__ __forceinline__ bool sqrt_gt(double s, double thr) {
+  const double t2 = __dmul_rn(thr, thr);
+  if (s > t2 * (1.0 + 1e-9)) return true;
+  if (s < t2 * (1.0 - 1e-9)) return false;
+  return __dsqrt_rn(s) > thr;
+}
+
+
 constexpr int kDigitBits = 13;
 constexpr int kBins = 1 << kDigitBits;  // 8192
 constexpr int kPasses = 5;              // lo bits: 50, 37, 24, 11, 0
@@ -760,8 +771,8 @@ __global__ void token_coded_norms_kernel(const double* __restrict__ norms,
     uint32_t c = 0;
 #pragma unroll
     for (int k = 0; k < 16; ++k) {
-      const double2 v = nr[k];
-      c += (v.x > thr ? 0u : 1u) + (v.y > thr ? 0u : 1u);
+      const double2 v = nr[k];  // squared norms
+      c += (sqrt_gt(v.x, thr) ? 0u : 1u) + (sqrt_gt(v.y, thr) ? 0u : 1u);
     }
     cnt[t] = c;
   }
@@ -769,12 +780,15 @@ __global__ void token_coded_norms_kernel(const double* __restrict__ norms,
 
 // ------------------------------------------------------ Med3x radix select
 // Exact lower median (rank (n-1)//2, outliers.py:50-55) of the fp64 chunk
-// norms of every pooling group: non-negative doubles order like their uint64
-// bit patterns, so 5 histogram passes over 13/13/13/13/11-bit digits of bits
-// [62:0] pin the element.  Passes 0-2 stream the whole call (pass 0 computes
-// and stores the exact norms from the input); pass 2 also compacts the
-// elements still matching the 26-bit prefix into per-group candidate lists,
-// so passes 3-4 touch only those.  Each pass's last CTA selects the digit.
+// norms of every pooling group.  The select runs on the squared norms s (the
+// reference's r = sqrt_rn(s) is monotone in s, so median(r) =
+// sqrt_rn(median(s)) and no per-chunk sqrt is needed): non-negative doubles
+// order like their uint64 bit patterns, so 5 histogram passes over
+// 13/13/13/13/11-bit digits of bits [62:0] pin the element.  Passes 0-2 stream
+// the whole call (pass 0 computes and stores s from the input); pass 2 also
+// compacts the elements still matching the 26-bit prefix into per-group
+// candidate lists, so passes 3-4 touch only those.  Each pass's last CTA
+// selects the digit; the threshold is C * sqrt_rn(median s).
 struct RadixParams {
   int64_t B, H, T, D;
   int C;
@@ -792,6 +806,13 @@ struct RadixParams {
   unsigned int* done;
   int G;
 };
+
+// Pass 0 digits (sign/exponent + top mantissa bits) concentrate in a few bins:
+// aggregate equal bins across the warp first; later passes spread over all
+// 8192 bins, where plain shared atomics are cheaper than the match.
+__device__ __forceinline__ void hist_add_sparse(uint32_t* hs, uint32_t bin, bool active) {
+  if (active) atomicAdd(hs + bin, 1u);
+}
 
 __device__ __forceinline__ void hist_add(uint32_t* hs, uint32_t bin, bool active) {
   const unsigned m = __match_any_sync(0xffffffffu, active ? bin : 0xffffffffu);
@@ -824,7 +845,7 @@ __device__ void radix_select_last(RadixParams& p) {
       p.groups[g].prefix |= ((unsigned long long)bin) << lo;
       p.groups[g].rank = k - acc;
       if (p.pass == kPasses - 1) {
-        const double med = __longlong_as_double((long long)p.groups[g].prefix);
+        const double med = __dsqrt_rn(__longlong_as_double((long long)p.groups[g].prefix));
         p.groups[g].threshold = __dmul_rn(p.multiplier, med);
       }
     }
@@ -878,7 +899,12 @@ __global__ void __launch_bounds__(kHistThreads) radix_hist_kernel(RadixParams p)
             double x[4];
 #pragma unroll
             for (int k = 0; k < 4; ++k) x[k] = In<InT>::d(v[j][k]);
-            rr[j] = exact_norm(x);
+            // the select runs on s = r^2: rank statistics commute with the
+            // monotone sqrt_rn, so median(r) = sqrt_rn(median(s)) exactly
+            double sq = __dmul_rn(x[0], x[0]);
+            sq = __dadd_rn(sq, __dmul_rn(x[1], x[1]));
+            sq = __dadd_rn(sq, __dmul_rn(x[2], x[2]));
+            rr[j] = __dadd_rn(sq, __dmul_rn(x[3], x[3]));
             nrow[i] = rr[j];
           }
         }
@@ -907,8 +933,10 @@ __global__ void __launch_bounds__(kHistThreads) radix_hist_kernel(RadixParams p)
               p.cand[(unsigned long long)g * p.n_per_group + base +
                      __popc(m & ((1u << lane) - 1u))] = rr[j];
           }
-        } else {
+        } else if (p.pass == 0) {
           hist_add(hs, bin, active);
+        } else {
+          hist_add_sparse(hs, bin, active);
         }
       }
     }
@@ -982,7 +1010,8 @@ __global__ void __launch_bounds__(kTailThreads) radix_tail_kernel(RadixParams p)
   if (threadIdx.x == 0) {
     p.groups[g].prefix = s_pref;
     p.groups[g].rank = s_rank;
-    p.groups[g].threshold = __dmul_rn(p.multiplier, __longlong_as_double((long long)s_pref));
+    p.groups[g].threshold =
+        __dmul_rn(p.multiplier, __dsqrt_rn(__longlong_as_double((long long)s_pref)));
   }
 }
 
@@ -1010,7 +1039,7 @@ __global__ void tile_count_kernel(const double* __restrict__ norms, const RadixG
   const int nck = ntok * C;
   const double* nr = norms + (row * T + t0) * C;
   uint32_t cnt = 0;
-  for (int k = threadIdx.x; k < nck; k += blockDim.x) cnt += nr[k] > thr ? 0u : 1u;
+  for (int k = threadIdx.x; k < nck; k += blockDim.x) cnt += sqrt_gt(nr[k], thr) ? 0u : 1u;
   typedef cub::BlockReduce<uint32_t, 256> BR;
   __shared__ typename BR::TempStorage tmp;
   const uint32_t total = BR(tmp).Sum(cnt);
