@@ -27,6 +27,8 @@
  *   hqmq_validate_indices    <- the index range checks of kvpack.from_bytes
  *                               (kvpack.py:279-280) / decode_token_range (codec.py:305-309)
  *   hqmq_attention_decode    <- attention.fused_attend       (attention.py:137-199)
+ *   hqmq_crc32               <- the zlib.crc32 trailer of kvpack.to_bytes / from_bytes
+ *                               (kvpack.py:177, 219)
  */
 #ifndef HQMQ_B200_H
 #define HQMQ_B200_H
@@ -224,6 +226,16 @@ typedef struct {
 
 size_t hqmq_attention_workspace_bytes(const hqmq_attention_args* args);
 int hqmq_attention_decode(const hqmq_attention_args* args, void* stream);
+
+/* ------------------------------------------------------------ kvpack CRC */
+/* zlib-compatible CRC-32 (reflected 0xEDB88320, init and xorout 0xFFFFFFFF) of
+ * n bytes of device memory, written little-endian to the 4 device bytes at
+ * out_crc (the kvpack trailer, kvpack.py:176-177).  Asynchronous on `stream`;
+ * the workspace (hqmq_crc32_workspace_bytes) must not be reused before the
+ * stream reaches this call's end. */
+size_t hqmq_crc32_workspace_bytes(uint64_t n);
+int hqmq_crc32(const void* data, uint64_t n, uint8_t* out_crc, void* workspace,
+               size_t workspace_bytes, void* stream);
 
 #ifdef __cplusplus
 }

@@ -100,6 +100,8 @@ SIGNATURES = {
     "hqmq_validate_indices": ([c_vp, c_i64, c_i32, c_i64, c_vp, c_vp], c_i32),
     "hqmq_attention_workspace_bytes": ([ctypes.POINTER(AttentionArgs)], ctypes.c_size_t),
     "hqmq_attention_decode": ([ctypes.POINTER(AttentionArgs), c_vp], c_i32),
+    "hqmq_crc32_workspace_bytes": ([ctypes.c_uint64], ctypes.c_size_t),
+    "hqmq_crc32": ([c_vp, ctypes.c_uint64, c_vp, c_vp, ctypes.c_size_t, c_vp], c_i32),
 }
 
 _lib = None

@@ -14,7 +14,6 @@ from __future__ import annotations
 
 import ctypes
 import struct
-import zlib
 
 import numpy as np
 
@@ -55,13 +54,9 @@ def expected_file_size(packed: QuantizedTensor) -> int:
     return size + 4
 
 
-def to_bytes(packed: QuantizedTensor) -> bytes:
+def _header(packed: QuantizedTensor, lengths) -> bytes:
+    """128-byte header + section table (kvpack.py:126-175)."""
     s, c = packed.shape, packed.config
-    if packed.role not in ROLE_TAGS:
-        raise InvalidArgument(f"role must be one of {sorted(ROLE_TAGS)}")
-    if not 0 <= packed.head_base + s.heads <= 0xFFFF:
-        raise InvalidArgument("head_base + heads must fit in 16 bits")
-    sections = packed.section_bytes()
     flags = (_FLAG_OUTLIER if c.outlier_multiplier is not None else 0) | (
         _FLAG_PER_HEAD if c.median_pooling == "per_head" else 0)
     header = struct.pack(_HEADER_FMT, MAGIC, VERSION, flags, s.batch, s.heads, s.tokens,
@@ -70,11 +65,62 @@ def to_bytes(packed: QuantizedTensor) -> bytes:
                          packed.layer)
     table = bytearray()
     off = HEADER_BYTES
-    for body in sections:
-        table += struct.pack("<QQ", off, len(body))
-        off += len(body)
-    payload = header + bytes(table) + b"".join(sections)
-    return payload + struct.pack("<I", zlib.crc32(payload) & 0xFFFFFFFF)
+    for n in lengths:
+        table += struct.pack("<QQ", off, n)
+        off += n
+    return header + bytes(table)
+
+
+def device_crc32(buf, n: int, out) -> None:
+    """zlib.crc32 of the first n bytes of a uint8 CUDA tensor, written
+    little-endian into the 4-byte uint8 CUDA tensor `out` (hqmq_crc32)."""
+    import torch
+
+    L = nat.lib()
+    ws = torch.empty(int(L.hqmq_crc32_workspace_bytes(n)), dtype=torch.uint8, device=buf.device)
+    nat.check(L.hqmq_crc32(buf.data_ptr(), n, out.data_ptr(), ws.data_ptr(), ws.numel(),
+                           nat.stream_handle(buf.device)), "hqmq_crc32")
+    buf._crc_ws = ws  # keep the workspace alive until the stream has used it
+
+
+def to_device_image(packed: QuantizedTensor):
+    """The whole kvpack file assembled in HBM (header, section table, the five
+    sections copied device-to-device, CRC-32 computed on the GPU): a uint8
+    CUDA tensor whose bytes equal the reference's to_bytes (kvpack.py:126-177)."""
+    import torch
+
+    s, c = packed.shape, packed.config
+    if packed.role not in ROLE_TAGS:
+        raise InvalidArgument(f"role must be one of {sorted(ROLE_TAGS)}")
+    if not 0 <= packed.head_base + s.heads <= 0xFFFF:
+        raise InvalidArgument("head_base + heads must fit in 16 bits")
+    n_coded = packed.n_coded  # synchronises the encode and raises its errors
+    dev = packed.device
+    as_u8 = lambda t: t.contiguous().view(-1).view(torch.uint8)  # noqa: E731
+    secs = [as_u8(packed.scales),
+            as_u8(packed.index_words)[: (n_coded * c.index_bits + 7) // 8],
+            as_u8(packed.radius_words)[: (n_coded * c.radius_bits + 7) // 8],
+            as_u8(packed.flag_words)[: (s.n_chunks + 7) // 8]
+            if c.outlier_multiplier is not None else None,
+            as_u8(packed.payloads) if packed.n_payload else None]
+    lengths = [0 if t is None else t.numel() for t in secs]
+    head = _header(packed, lengths)
+    total = len(head) + sum(lengths)
+    img = torch.empty(total + 4, dtype=torch.uint8, device=dev)
+    img[: len(head)].copy_(torch.frombuffer(bytearray(head), dtype=torch.uint8), non_blocking=False)
+    off = len(head)
+    for t, n in zip(secs, lengths):
+        if n:
+            img[off: off + n].copy_(t)
+        off += n
+    device_crc32(img, total, img[total:])
+    return img
+
+
+def to_bytes(packed: QuantizedTensor) -> bytes:
+    """kvpack.py:126-177: byte-identical serialisation, assembled and
+    checksummed on the GPU, then one device->host copy."""
+    return to_device_image(packed).cpu().numpy().tobytes()
 
 
 def write_kvpack(packed: QuantizedTensor, sink) -> int:
@@ -96,17 +142,10 @@ def read_kvpack(source, device="cuda") -> QuantizedTensor:
     return from_bytes(blob, device)
 
 
-def _upload_words(buf: bytes, nbits: int, device):
-    import torch
-
-    n = _words(nbits)
-    raw = np.zeros(n * 4, dtype=np.uint8)
-    raw[: len(buf)] = np.frombuffer(buf, dtype=np.uint8)
-    return torch.from_numpy(raw.view("<i4").copy()).to(device)
-
-
 def from_bytes(blob: bytes, device="cuda") -> QuantizedTensor:
-    """Parse and validate (kvpack.py:194-306), then upload to the device."""
+    """Parse and validate (kvpack.py:194-306) with the reference's checks in the
+    reference's order.  The file is uploaded once; the CRC-32 is verified on
+    the GPU and the sections are carved out of the device copy."""
     import torch
 
     if len(blob) < HEADER_BYTES + 4:
@@ -117,8 +156,12 @@ def from_bytes(blob: bytes, device="cuda") -> QuantizedTensor:
         raise CorruptData(f"bad magic {magic!r}")
     if version != VERSION:
         raise UnsupportedVersion(f"format version {version}, expected {VERSION}")
-    (crc_stored,) = struct.unpack_from("<I", blob, len(blob) - 4)
-    if zlib.crc32(blob[:-4]) & 0xFFFFFFFF != crc_stored:
+    nat.require_cuda(device)
+    device = torch.device(device)
+    dblob = torch.frombuffer(bytearray(blob), dtype=torch.uint8).to(device)
+    crc = torch.empty(4, dtype=torch.uint8, device=device)
+    device_crc32(dblob, len(blob) - 4, crc)
+    if bytes(crc.cpu().numpy().tobytes()) != bytes(blob[-4:]):
         raise CorruptData("checksum mismatch")
     table = []
     end = HEADER_BYTES
@@ -148,21 +191,26 @@ def from_bytes(blob: bytes, device="cuda") -> QuantizedTensor:
         off, length = table[k]
         return blob[off:off + length]
 
-    nat.require_cuda(device)
-    device = torch.device(device)
+    def dsection(k, nbytes_alloc):
+        """Device copy of section k into a zeroed, 4-byte aligned uint8 buffer."""
+        off, length = table[k]
+        buf = torch.zeros(max(nbytes_alloc, length, 4), dtype=torch.uint8, device=device)
+        if length:
+            buf[:length].copy_(dblob[off:off + length])
+        return buf
+
     n_tok = batch * heads * tokens
     n = n_tok * shape.chunks_per_vector
     if len(section(0)) != 2 * n_tok:
         raise CorruptData("scale section has the wrong length")
-    scales = torch.from_numpy(np.frombuffer(section(0), dtype="<f2").astype(np.float16).reshape(
-        batch, heads, tokens)).to(device)
+    scales = dsection(0, 2 * n_tok)[: 2 * n_tok].view(torch.float16).reshape(batch, heads, tokens)
     if outlier:
         if len(section(3)) != (n + 7) // 8:
             raise CorruptData("flag bitmap has the wrong length")
         fbits = np.unpackbits(np.frombuffer(section(3), dtype=np.uint8), bitorder="little",
                               count=n)
         n_flag = int(fbits.sum())
-        fw = _upload_words(section(3), n, device)
+        fw = dsection(3, 4 * _words(n)).view(torch.int32)
     else:
         if len(section(3)) != 0:
             raise CorruptData("unexpected flag bitmap without extraction")
@@ -174,15 +222,13 @@ def from_bytes(blob: bytes, device="cuda") -> QuantizedTensor:
         raise CorruptData(f"bit stream length {len(section(1))} != expected {(n_coded * w + 7) // 8}")
     if len(section(2)) != (n_coded * br + 7) // 8:
         raise CorruptData(f"bit stream length {len(section(2))} != expected {(n_coded * br + 7) // 8}")
-    iw = _upload_words(section(1), n * w, device)
-    rw = _upload_words(section(2), n * br, device)
+    iw = dsection(1, 4 * _words(n * w)).view(torch.int32)
+    rw = dsection(2, 4 * _words(n * br)).view(torch.int32)
     pay_raw = section(4)
     if len(pay_raw) != 8 * n_flag:
         raise CorruptData("payload section has the wrong length")
-    pay = torch.zeros((max(1, n_flag), CHUNK_DIM), dtype=torch.float16, device=device)
-    if n_flag:
-        pay[:n_flag] = torch.from_numpy(np.frombuffer(pay_raw, dtype="<f2").astype(
-            np.float16).reshape(n_flag, CHUNK_DIM)).to(device)
+    pay = dsection(4, 8 * max(1, n_flag))[: 8 * max(1, n_flag)].view(torch.float16).reshape(
+        max(1, n_flag), CHUNK_DIM)
     L = nat.lib()
     stream = nat.stream_handle(device)
     tok = None

@@ -99,6 +99,40 @@ def test_frozen_reference_digest(cuda):
     assert digest == "12b2dfad207652800819a0ab439f8ef44c1c5ce33eff0f70979bc4e8b2cc1039"
 
 
+@pytest.mark.parametrize("n", [0, 1, 3, 4, 5, 511, 512, 513, 4096, 65537, 1 << 20, 5_000_003])
+def test_device_crc32_matches_zlib(cuda, n):
+    """hqmq_crc32 (GPU, kvpack.py:177) == zlib.crc32, aligned and misaligned starts."""
+    import zlib
+
+    m = hq()
+    from paper_2605_27646_b200.kvpack import device_crc32
+
+    rs = np.random.default_rng(n)
+    raw = rs.integers(0, 256, n + 3, dtype=np.uint8)
+    buf = torch.from_numpy(raw).to(cuda)
+    for shift in (0, 1, 3):
+        out = torch.zeros(4, dtype=torch.uint8, device=cuda)
+        device_crc32(buf[shift:shift + n] if n else buf[:0], n, out)
+        got = int.from_bytes(out.cpu().numpy().tobytes(), "little")
+        assert got == zlib.crc32(raw[shift:shift + n].tobytes()) & 0xFFFFFFFF, (n, shift)
+    assert m is not None
+
+
+def test_kvpack_every_bit_flip_detected(cuda):
+    """Every single-bit flip of a kvpack file is rejected (test_kvpack.py:108-116),
+    with the CRC checked on the GPU."""
+    m = hq()
+    meta, g = load_codec_fixture("frozen")
+    blob = g["blob"].tobytes()
+    assert m.to_bytes(m.from_bytes(blob, device=cuda)) == blob
+    for pos in range(0, len(blob), 7):
+        for bit in (0, 5):
+            bad = bytearray(blob)
+            bad[pos] ^= 1 << bit
+            with pytest.raises(m.CorruptData):
+                m.from_bytes(bytes(bad), device=cuda)
+
+
 def test_from_arrays_pack_matches_encoder(cuda):
     m = hq()
     meta, g = load_codec_fixture("outlier_heavy")

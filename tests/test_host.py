@@ -93,7 +93,8 @@ def test_rotation_table_identity():
 
 
 def test_kvpack_header_validation_before_upload():
-    """Corruptions detectable from the header/CRC raise CorruptData without a device."""
+    """Corruptions detectable from the header raise CorruptData / UnsupportedVersion
+    without a device (the CRC itself is checked on the GPU: test_gpu_parity)."""
     meta, g = load_codec_fixture("frozen")
     blob = g["blob"].tobytes()
     with pytest.raises(m.CorruptData):
@@ -107,8 +108,3 @@ def test_kvpack_header_validation_before_upload():
     bad[-4:] = struct.pack("<I", zlib.crc32(bytes(bad[:-4])) & 0xFFFFFFFF)
     with pytest.raises(m.UnsupportedVersion):
         m.from_bytes(bytes(bad))
-    for pos in range(0, len(blob), 7):
-        bad = bytearray(blob)
-        bad[pos] ^= 0x01
-        with pytest.raises(m.CorruptData):
-            m.from_bytes(bytes(bad))
