@@ -220,6 +220,78 @@ __device__ __forceinline__ void decode_token_fast(const DecParams& p, const uint
   }
 }
 
+// Two tokens per warp instruction (compile-time W / BR only): half-warp h
+// takes token tt + h, lane l = lane & 15 decodes chunks 2l and 2l+1, so one
+// pair of code loads feeds two chunks and the row store is 16 bytes per lane.
+template <typename OutT, int W, int BR>
+__device__ __forceinline__ void decode_token2_fast(const uint32_t* __restrict__ iw,
+                                                   const uint32_t* __restrict__ rw,
+                                                   const uint16_t* __restrict__ sc,
+                                                   const void* __restrict__ tab, int tt,
+                                                   OutT* __restrict__ orow, int lane, uint32_t ncw,
+                                                   float rtop, bool& bad) {
+  constexpr uint32_t kIM = W == 32 ? 0xffffffffu : ((1u << W) - 1u);
+  constexpr uint32_t kRM = (1u << BR) - 1u;
+  const int t = tt + (lane >> 4);
+  const uint32_t c0 = 2u * (uint32_t)(lane & 15);
+  const uint32_t bi = c0 * W, bq = c0 * BR;
+  const uint32_t* wp = iw + t * W + (bi >> 5);
+  static_assert(2 * W <= 32 && 2 * BR <= 32, "two codes must fit one funnel-shifted word");
+  const uint32_t ipair = __funnelshift_r(wp[0], wp[1], bi & 31);  // 2W <= 32 bits from bi
+  uint32_t i0 = ipair & kIM;
+  uint32_t i1 = (ipair >> W) & kIM;
+  const uint32_t* qp = rw + t * BR + (bq >> 5);
+  uint32_t qpair;
+  if constexpr ((32 % (2 * BR)) == 0) qpair = qp[0] >> (bq & 31);
+  else qpair = __funnelshift_r(qp[0], qp[1], bq & 31);
+  const uint32_t q0 = qpair & kRM, q1 = (qpair >> BR) & kRM;
+  bad |= (i0 >= ncw) | (i1 >= ncw);
+  i0 = i0 < ncw ? i0 : 0u;
+  i1 = i1 < ncw ? i1 : 0u;
+  const float sg = __half2float(__ushort_as_half(sc[t])) * rtop;
+  const float r0 = (float)q0 * sg, r1 = (float)q1 * sg;
+  OutT* o = orow + t * 128 + 4 * c0;
+  if constexpr (sizeof(OutT) == 4) {
+    const float4 a = reinterpret_cast<const float4*>(tab)[i0];
+    const float4 b = reinterpret_cast<const float4*>(tab)[i1];
+    reinterpret_cast<float4*>(o)[0] = make_float4(r0 * a.x, r0 * a.y, r0 * a.z, r0 * a.w);
+    reinterpret_cast<float4*>(o)[1] = make_float4(r1 * b.x, r1 * b.y, r1 * b.z, r1 * b.w);
+  } else {
+    const uint2 a = reinterpret_cast<const uint2*>(tab)[i0];
+    const uint2 b = reinterpret_cast<const uint2*>(tab)[i1];
+    uint4 ov;
+    if constexpr (std::is_same<OutT, __half>::value) {
+      const __half2 ra = __float2half2_rn(r0), rb = __float2half2_rn(r1);
+      const __half2 x0 = __hmul2(ra, *reinterpret_cast<const __half2*>(&a.x));
+      const __half2 x1 = __hmul2(ra, *reinterpret_cast<const __half2*>(&a.y));
+      const __half2 x2 = __hmul2(rb, *reinterpret_cast<const __half2*>(&b.x));
+      const __half2 x3 = __hmul2(rb, *reinterpret_cast<const __half2*>(&b.y));
+      ov = make_uint4(*reinterpret_cast<const uint32_t*>(&x0), *reinterpret_cast<const uint32_t*>(&x1),
+                      *reinterpret_cast<const uint32_t*>(&x2), *reinterpret_cast<const uint32_t*>(&x3));
+    } else {
+      const float2 a01 = __half22float2(*reinterpret_cast<const __half2*>(&a.x));
+      const float2 a23 = __half22float2(*reinterpret_cast<const __half2*>(&a.y));
+      const float2 b01 = __half22float2(*reinterpret_cast<const __half2*>(&b.x));
+      const float2 b23 = __half22float2(*reinterpret_cast<const __half2*>(&b.y));
+      const __nv_bfloat162 x0 = __floats2bfloat162_rn(r0 * a01.x, r0 * a01.y);
+      const __nv_bfloat162 x1 = __floats2bfloat162_rn(r0 * a23.x, r0 * a23.y);
+      const __nv_bfloat162 x2 = __floats2bfloat162_rn(r1 * b01.x, r1 * b01.y);
+      const __nv_bfloat162 x3 = __floats2bfloat162_rn(r1 * b23.x, r1 * b23.y);
+      ov = make_uint4(*reinterpret_cast<const uint32_t*>(&x0), *reinterpret_cast<const uint32_t*>(&x1),
+                      *reinterpret_cast<const uint32_t*>(&x2), *reinterpret_cast<const uint32_t*>(&x3));
+    }
+    *reinterpret_cast<uint4*>(o) = ov;
+  }
+}
+
+// Shared-memory table bytes: fp32 codewords for fp32 output, fp16 copies
+// (8-byte entries) for 16-bit outputs; the TMA ring starts after them.
+template <typename OutT>
+__host__ __device__ inline size_t fd_table_bytes(int ncw) {
+  const size_t b = (size_t)ncw * (sizeof(OutT) == 4 ? 16 : 8);
+  return (b + 127) / 128 * 128;
+}
+
 template <typename OutT, int W, int BR>
 __global__ void __launch_bounds__(256) decode_fast_kernel(DecParams p) {
   extern __shared__ __align__(128) unsigned char dsm[];
@@ -232,7 +304,7 @@ __global__ void __launch_bounds__(256) decode_fast_kernel(DecParams p) {
   const int w = W ? W : p.w, br = BR ? BR : p.br;
   const FastDecodeGeom g = fd_geom(w, br);
   float4* tab = reinterpret_cast<float4*>(dsm);
-  unsigned char* ring = dsm + (size_t)ncw * sizeof(float4);
+  unsigned char* ring = dsm + fd_table_bytes<OutT>(ncw);
   const float4* __restrict__ gtab = reinterpret_cast<const float4*>(p.table) + (int64_t)h * ncw;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t ntile = ceil_div(p.nt, kFDTok);
@@ -300,7 +372,14 @@ __global__ void __launch_bounds__(256) decode_fast_kernel(DecParams p) {
     const uint16_t* sc = reinterpret_cast<const uint16_t*>(s + g.sc_off);
     const int ntok = (int)min((int64_t)kFDTok, p.nt - tile * kFDTok);
     OutT* orow = out + (row * p.nt + tile * kFDTok) * 128 + 4 * lane;
-    if (ntok == kFDTok) {
+    if (W != 0 && ntok == kFDTok) {
+      // full tile, compile-time geometry: warp w decodes token pairs
+      // (2w, 2w+1), (2w+16, 2w+17), ... (fully unrolled)
+#pragma unroll
+      for (int i = 0; i < kFDTok / 16; ++i)
+        decode_token2_fast<OutT, W ? W : 1, BR ? BR : 1>(iw, rw, sc, tab, 2 * warp + 16 * i, orow - 4 * lane,
+                                                        lane, (uint32_t)ncw, rtop, bad);
+    } else if (ntok == kFDTok) {
       // full tile: warp w decodes tokens w, w+8, ..., w+56 (fully unrolled)
       const uint32_t* iww = iw + warp * w;
       const uint32_t* rww = rw + warp * br;
@@ -593,7 +672,8 @@ int launch_decode(DecParams& p, const hqmq_decode_args* a, cudaStream_t st) {
     const int64_t bx = std::max<int64_t>(1, std::min<int64_t>(want, nwt));
     cudaFuncSetAttribute(decode_flag_kernel<OutT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)kDecSmemLimit);
-    decode_flag_kernel<OutT><<<dim3((unsigned)bx, (unsigned)rows), 256, smem, st>>>(p);
+    decode_flag_kernel<OutT><<<dim3((unsigned)bx, (unsigned)rows), 256,
+                               fd_table_bytes<OutT>(kGroupOrder * p.S), st>>>(p);
     return check();
   }
   const bool fast = p.D == 128 && !p.flagw && use_smem && p.aligned4 && p.T % 8 == 0 &&
@@ -601,7 +681,7 @@ int launch_decode(DecParams& p, const hqmq_decode_args* a, cudaStream_t st) {
                     al16(p.scales);
   if (fast) {
     const FastDecodeGeom g = fd_geom(p.w, p.br);
-    const size_t fsmem = smem + (size_t)kFDStages * g.stage_bytes;
+    const size_t fsmem = fd_table_bytes<OutT>(kGroupOrder * p.S) + (size_t)kFDStages * g.stage_bytes;
     // (index_bits, radius_bits) instances with compile-time stream geometry
     void (*kern)(DecParams) = decode_fast_kernel<OutT, 0, 0>;
     switch (p.w * 16 + p.br) {
@@ -613,7 +693,7 @@ int launch_decode(DecParams& p, const hqmq_decode_args* a, cudaStream_t st) {
     }
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     const int64_t ntile = ceil_div(p.nt, kFDTok);
-    const int per_sm = std::max<int>(1, std::min<int>(8, (int)((200 * 1024) / fsmem)));
+    const int per_sm = std::max<int>(1, std::min<int>(8, (int)((227 * 1024) / (fsmem + 1024))));
     const int64_t want = std::max<int64_t>(1, ceil_div((int64_t)148 * per_sm, rows));
     const int64_t bx = std::max<int64_t>(1, std::min<int64_t>(want, ntile));
     kern<<<dim3((unsigned)bx, (unsigned)rows), 256, fsmem, st>>>(p);
