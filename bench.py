@@ -375,11 +375,24 @@ def run_ours(args, wl, world, rank, local):
             result["decode_attn"] = bench_attention(args, torch, hq, dev)
         except Exception as exc:  # report, never hide
             result["decode_attn"] = {"error": repr(exc)[:300]}
-    if rank == 0 and not args.no_e2e and world == 1:
+    if not args.no_e2e:
+        # every rank runs its own units through the public API with host
+        # buffers; whole-job bytes over the slowest rank's time
         try:
-            result["e2e"] = bench_e2e(args, torch, hq, wl, dev, cfg, bank, units)
+            e2e = bench_e2e(args, torch, hq, wl, dev, cfg, bank, units)
         except Exception as exc:
-            result["e2e"] = {"error": repr(exc)[:300]}
+            e2e = {"error": repr(exc)[:300]}
+        if world > 1 and "ms_per_step" in e2e:
+            t = torch.tensor([e2e["ms_per_step"]], dtype=torch.float64, device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            nb = torch.tensor([e2e["h2d_bytes_per_step"], e2e["d2h_bytes_per_step"]],
+                              dtype=torch.float64, device=dev)
+            dist.all_reduce(nb)
+            ms = float(t.item())
+            e2e.update(ms_per_step=round(ms, 3), h2d_bytes_per_step=int(nb[0].item()),
+                       d2h_bytes_per_step=int(nb[1].item()),
+                       value=round(nb[0].item() / (ms * 1e-3) / 1e9, 3))
+        result["e2e"] = e2e
     if rank == 0 and world == 1 and not args.no_cpu:
         result["cpu_baseline"] = cpu_baseline(wl, args.cpu_seconds)
     if rank == 0:

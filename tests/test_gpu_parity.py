@@ -246,6 +246,38 @@ def test_full_size_c2_unit_sampled(cuda, oracle):
     assert rel < 0.2
 
 
+def test_full_size_c5_unit_sampled(cuda, oracle):
+    """Llama-3-70B 128k unit at full size (1, 8, 131072, 128), S=256 (C5): sampled
+    token slices bit-exact against the oracle, plus size-independent properties
+    over the whole unit (decode of the fp64 path reproduces the fp32 path to
+    1e-6, the round-trip error is bounded, the kvpack image round-trips)."""
+    m = hq()
+    g = torch.Generator(device=cuda).manual_seed(70)
+    x = torch.randn((1, 8, 131072, 128), generator=g, device=cuda).to(torch.float16)
+    cfg = m.CodecConfig(codebook_size=256, radius_bits=4)
+    bank = m.CodebookBank(0, 256)
+    qt = m.encode_tensor(x, cfg, layer=79, role="K", bank=bank)
+    rs = np.random.default_rng(5)
+    toks = np.sort(rs.choice(131072, 96, replace=False))
+    xs = x[:, :, toks].to(torch.float64).cpu().numpy()
+    ref = _oracle_encode(oracle, xs, cfg, 79, "K")
+    np.testing.assert_array_equal(qt.indices.cpu().numpy()[:, :, toks], ref.indices)
+    np.testing.assert_array_equal(qt.quanta.cpu().numpy()[:, :, toks], ref.quanta)
+    np.testing.assert_array_equal(qt.scales.cpu().numpy()[:, :, toks].view(np.uint16),
+                                  ref.scales.view(np.uint16))
+    d64 = m.decode_tensor(qt, bank, dtype=torch.float64)
+    np.testing.assert_array_equal(d64[:, :, toks].cpu().numpy(), oracle.decode(ref))
+    d32 = m.decode_tensor(qt, bank)
+    rel = torch.max(torch.abs(d32.double() - d64) / (torch.abs(d64) + 1e-30)).item()
+    assert rel <= 1e-6
+    err = (torch.linalg.vector_norm(d32 - x.float()) / torch.linalg.vector_norm(x.float())).item()
+    assert err < 0.2
+    blob = m.to_bytes(qt)
+    back = m.from_bytes(blob, device=cuda)
+    assert torch.equal(back.index_words[: qt.index_words.numel()], qt.index_words)
+    assert len(blob) == m.expected_file_size(qt)
+
+
 def test_full_size_c3_unit(cuda, oracle):
     """Qwen2.5-7B unit at full size (1, 4, 32768, 128), outlier-heavy, S=64,
     b_r=6, Med3x over the whole call: compared exactly against the oracle."""
