@@ -759,6 +759,271 @@ __global__ void __launch_bounds__(kWThreads, kMinB) encode_warp_kernel(EncParams
   }
 }
 
+// ------------------------------------------- tcgen05 search (tensor cores)
+// The S-loop's rotations v_s = u (x) conj(q_s) for all secondaries are one
+// GEMM, V[chunk][4s+c] = sum_i u_i R_s[i][c], with contraction 4.  On sm_100a
+// it runs on the 5th-gen tensor cores at fp32-level accuracy by splitting both
+// operands into two fp16 parts (u = u1 + u2, R = R1 + R2) and stacking the
+// three significant cross terms along K:
+//   A row (chunk) = [u1 | u1 | u2 | 0],  B column (4s+c) = [R1 | R2 | R1 | 0]
+// so one tcgen05.mma (M=128 chunks, N=128 = 32 secondaries x 4, K=16) gives
+// V = u1.R1 + u1.R2 + u2.R1 (the dropped u2.R2 is < 2^-22) in fp32 TMEM
+// (measured |err| <= 2.8e-7 vs fp64, tools/ubench_umma.cu).  CUDA cores then
+// only score the 24-element cosets from TMEM (tcgen05.ld) and track the top
+// two; the certification margin and the exact fp64 fixup are unchanged, with
+// the margin widened to cover the split-operand error.
+//
+// CTA = 8 warps = 2 groups of 4; a group owns a tile of 4 tokens (128 chunks:
+// warp = token, lane = chunk = TMEM lane) and 128 TMEM columns, so two groups
+// (and two CTAs per SM) overlap one another's MMA waits with scoring.
+constexpr int kTcWarps = 8;
+constexpr int kTcThreads = kTcWarps * 32;
+constexpr int kTcBlk = 32;                 // secondaries per MMA (N = 128)
+constexpr int kTcN = 4 * kTcBlk;
+constexpr uint32_t kTcLBO = 128, kTcSBO = 256;  // K-major SWIZZLE_NONE core-matrix strides
+constexpr float kDeltaTc = 1e-5f;          // certification margin (split-fp16 rotation)
+
+__device__ __forceinline__ uint32_t tc_kmaj(int r, int k) {
+  return (r >> 3) * kTcSBO + (k >> 3) * kTcLBO + (r & 7) * 16 + (k & 7) * 2;
+}
+__device__ __forceinline__ uint64_t tc_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)(kTcLBO >> 4) << 16) |
+         ((uint64_t)(kTcSBO >> 4) << 32) | ((uint64_t)1 << 46);
+}
+__host__ __device__ constexpr uint32_t tc_idesc(int M, int N) {
+  return (1u << 4) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);  // f16 x f16 -> f32
+}
+__device__ __forceinline__ void tc_ld32(uint32_t addr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]),
+        "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]),
+        "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(addr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ uint32_t pack2h(float lo, float hi) {
+  const __half2 h = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
+
+template <typename InT>
+__global__ void __launch_bounds__(kTcThreads, 2) encode_tc_kernel(EncParams p) {
+  extern __shared__ __align__(1024) unsigned char tsm[];
+  __shared__ uint32_t stage_i[kTcWarps][34];
+  __shared__ __align__(8) uint64_t mbar[2];
+  __shared__ uint32_t tmem_slot;
+  const int S = p.S, w = p.w;
+  const int nblk = S / kTcBlk;
+  // smem: A tiles (2 x 4 KB) | B operand (S/32 blocks x 4 KB) | fp32 rotation table
+  unsigned char* asm_base = tsm;
+  unsigned char* bsm = tsm + 2 * 4096;
+  float4* tab_s = reinterpret_cast<float4*>(bsm + (size_t)nblk * 4096);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int grp = warp >> 2, wl = warp & 3;
+  const int64_t row = blockIdx.y;
+  const int h = (int)(row % p.H);
+  const float4* __restrict__ rot = p.rot + (int64_t)h * S * 4;
+  const double* __restrict__ joint = p.joint + (int64_t)h * kGroupOrder * S * 4;
+
+  // ---- one-time setup: fp32 table, split-fp16 B operand, TMEM, barriers
+  for (int i = tid; i < S * 4; i += kTcThreads) tab_s[i] = __ldg(rot + i);
+  for (int n = tid; n < S * 4; n += kTcThreads) {
+    const int s = n >> 2, c = n & 3, blk = s / kTcBlk, nn = n - blk * kTcN;
+    const float* f = reinterpret_cast<const float*>(rot + 4 * s);
+    unsigned char* bb = bsm + (size_t)blk * 4096;
+    uint32_t hi[2], lo[2];
+#pragma unroll
+    for (int i = 0; i < 4; i += 2) {
+      const float r0 = __ldg(f + (c >> 1) * 8 + (i >> 1) * 4 + (c & 1));
+      const float r1 = __ldg(f + (c >> 1) * 8 + ((i + 1) >> 1) * 4 + 2 + (c & 1));
+      const __half a0 = __float2half_rn(r0), a1 = __float2half_rn(r1);
+      hi[i >> 1] = pack2h(__half2float(a0), __half2float(a1));
+      lo[i >> 1] = pack2h(r0 - __half2float(a0), r1 - __half2float(a1));
+    }
+    // k 0..3 = R1, 4..7 = R2, 8..11 = R1, 12..15 = 0
+    *reinterpret_cast<uint4*>(bb + tc_kmaj(nn, 0)) = make_uint4(hi[0], hi[1], lo[0], lo[1]);
+    *reinterpret_cast<uint4*>(bb + tc_kmaj(nn, 8)) = make_uint4(hi[0], hi[1], 0u, 0u);
+  }
+  for (int i = lane; i < 34; i += 32) stage_i[warp][i] = 0u;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_slot)),
+                 "n"(2 * kTcN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    mbar_init(&mbar[0], 1);
+    mbar_init(&mbar[1], 1);
+    fence_mbar_init();
+  }
+  fence_proxy_async();
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_slot + (uint32_t)(grp * kTcN) + ((uint32_t)(wl * 32) << 16);
+  const uint32_t tmem_grp = tmem_slot + (uint32_t)(grp * kTcN);
+  unsigned char* at = asm_base + grp * 4096;
+  const uint32_t a_saddr = smem_u32(at), b_saddr = smem_u32(bsm);
+  uint32_t phase = 0;
+
+  const InT* __restrict__ data = reinterpret_cast<const InT*>(p.data);
+  const int64_t ntiles = ceil_div(p.T, 4);
+  const int64_t stride = (int64_t)gridDim.x * 2;
+  const uint32_t lanemask_lt = (1u << lane) - 1u;
+  uint32_t* __restrict__ st_i = stage_i[warp];
+  const bool ext = p.tokoff != nullptr;
+  const bool leader = wl == 0 && lane == 0;
+
+  int64_t tile = (int64_t)blockIdx.x * 2 + grp;
+  uint2 raw = make_uint2(0u, 0u);
+  auto load = [&](int64_t t4) {
+    const int64_t t = t4 * 4 + wl;
+    return (t4 < ntiles && t < p.T)
+               ? __ldg(reinterpret_cast<const uint2*>(data + (row * p.T + t) * 128) + lane)
+               : make_uint2(0u, 0u);
+  };
+  raw = load(tile);
+  for (; tile < ntiles; tile += stride) {
+    const uint2 nxt = load(tile + stride);
+    const int64_t t = tile * 4 + wl;  // this warp's token
+    const bool valid = t < p.T;
+    const int64_t tok = row * p.T + t;
+    // ---- direction, liveness, A row (m = 32 wl + lane)
+    const uint32_t fmask = (ext && valid) ? __ldg(p.flagw + tok) : 0u;
+    const bool fl = (fmask >> lane) & 1u;
+    const InT* v = reinterpret_cast<const InT*>(&raw);
+    InT vv[4] = {v[0], v[1], v[2], v[3]};
+    const bool nz = (raw.x | raw.y) & 0x7fff7fffu;
+    const bool live = valid && !fl && nz;
+    float4 u4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (live) {
+      double x[4] = {0.0, 0.0, 0.0, 0.0};
+      const Dir2 d = fast_dir_lazy_norm(vv, x);
+      u4 = make_float4(d.a.x, d.b.x, d.c.x, d.d.x);
+    }
+    {
+      const __half h0 = __float2half_rn(u4.x), h1 = __float2half_rn(u4.y);
+      const __half h2 = __float2half_rn(u4.z), h3 = __float2half_rn(u4.w);
+      const uint32_t u1a = pack2h(__half2float(h0), __half2float(h1));
+      const uint32_t u1b = pack2h(__half2float(h2), __half2float(h3));
+      const uint32_t u2a = pack2h(u4.x - __half2float(h0), u4.y - __half2float(h1));
+      const uint32_t u2b = pack2h(u4.z - __half2float(h2), u4.w - __half2float(h3));
+      const int m = wl * 32 + lane;
+      *reinterpret_cast<uint4*>(at + tc_kmaj(m, 0)) = make_uint4(u1a, u1b, u1a, u1b);
+      *reinterpret_cast<uint4*>(at + tc_kmaj(m, 8)) = make_uint4(u2a, u2b, 0u, 0u);
+    }
+    fence_proxy_async();
+    asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
+    // ---- per block of 32 secondaries: MMA into TMEM, then score from TMEM
+    float best = -1.f, second = -1.f;
+    int bs = 0;
+    for (int blk = 0; blk < nblk; ++blk) {
+      if (leader) {
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint64_t da = tc_desc(a_saddr), db = tc_desc(b_saddr + (uint32_t)blk * 4096u);
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_grp),
+            "l"(da), "l"(db), "r"(tc_idesc(128, kTcN)), "r"(0));
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+            smem_u32(&mbar[grp])));
+      }
+      mbar_wait(&mbar[grp], phase);
+      phase ^= 1u;
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+      for (int q = 0; q < kTcN / 32; ++q) {
+        float vals[32];
+        tc_ld32(tmem + (uint32_t)(q * 32), vals);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float2 wx = make_float2(vals[4 * j], vals[4 * j + 1]);
+          const float2 yz = make_float2(vals[4 * j + 2], vals[4 * j + 3]);
+          const float sc = coset_score(wx, yz);
+          const int s = blk * kTcBlk + q * 8 + j;
+          const bool gt = sc > best;
+          second = fmaxf(second, fminf(sc, best));
+          best = fmaxf(best, sc);
+          bs = gt ? s : bs;
+        }
+      }
+      // TMEM reads done before the next MMA (or the next tile's) overwrites it
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
+    }
+    // ---- certification (exact fp32 rotation of the chosen secondary) + fixup
+    int idx = 0;
+    bool unsure = false;
+    if (live) {
+      Dir2 d;
+      d.a = make_float2(u4.x, u4.x);
+      d.b = make_float2(u4.y, u4.y);
+      d.c = make_float2(u4.z, u4.z);
+      d.d = make_float2(u4.w, u4.w);
+      float2 wx, yz;
+      rotate(d, tab_s[4 * bs], tab_s[4 * bs + 1], tab_s[4 * bs + 2], tab_s[4 * bs + 3], wx, yz);
+      int pidx;
+      float top32, within;
+      coset_resolve(wx, yz, pidx, top32, within);
+      idx = pidx * S + bs;
+      // every other secondary's score is known to within the split-operand
+      // error (TMEM), the chosen one's exactly in fp32 (top32): if the TMEM
+      // argmax were wrong, second >= top32 - (both errors) and this fails
+      unsure = !(top32 - fmaxf(second, within) > kDeltaTc);
+    }
+    uint32_t um = __ballot_sync(0xffffffffu, unsure);
+    if (um && lane == 0)
+      atomicAdd(reinterpret_cast<unsigned long long*>(p.counters + 2), (unsigned long long)__popc(um));
+    while (um) {
+      const int L = __ffs(um) - 1;
+      um &= um - 1;
+      const uint2 rw = __ldg(reinterpret_cast<const uint2*>(data + tok * 128) + L);
+      const InT* vr = reinterpret_cast<const InT*>(&rw);
+      InT vx[4] = {vr[0], vr[1], vr[2], vr[3]};
+      double x[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) x[i] = In<InT>::d(vx[i]);
+      const double rl = exact_norm(x);
+      const Dir2 ud = fast_dir(vx, x, rl);
+      const int ex = warp_exact_index(x, rl, ud, tab_s, joint, S, lane);
+      if (lane == L) idx = ex;
+    }
+    // ---- pack this token's index codes
+    if (valid) {
+      const uint64_t P0 = ext ? (uint64_t)__ldg(p.tokoff + tok) : (uint64_t)tok * 32;
+      const uint32_t lbi = (uint32_t)((P0 * (uint64_t)w) & 31);
+      const uint32_t rel = __popc(~fmask & lanemask_lt);
+      if (!fl) stage_bits(st_i, (uint64_t)lbi + (uint64_t)rel * w, (uint32_t)idx, w);
+      __syncwarp();
+      const uint32_t coded = __popc(~fmask);
+      const uint64_t end = lbi + (uint64_t)coded * w;
+      const uint32_t nw = (uint32_t)((end + 31) >> 5);
+      const uint64_t gw0 = (P0 * (uint64_t)w) >> 5;
+      for (uint32_t i = lane; i < nw; i += 32) {
+        const uint32_t word = st_i[i];
+        const bool owned = (i > 0 || lbi == 0) && (i + 1 < nw || (end & 31) == 0);
+        if (owned) p.idxw[gw0 + i] = word;
+        else if (word) atomicOr(p.idxw + gw0 + i, word);
+        st_i[i] = 0u;
+      }
+      __syncwarp();
+    }
+    raw = nxt;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_slot),
+                 "n"(2 * kTcN));
+}
+
 // Per-token coded (unflagged) chunk count from the stored norms (C = 32).
 __global__ void token_coded_norms_kernel(const double* __restrict__ norms,
                                          const RadixGroup* groups, int64_t H, int64_t T,
@@ -1246,9 +1511,24 @@ int launch_encode(const hqmq_encode_args* a, const Layout& L, cudaStream_t st) {
           launch(encode_warp_kernel<InT, 4, 4, 1>, 4, 4);
           launch(encode_warp_kernel<InT, 8, 2, 2>, 8, 2);
           break;
-        default:  // split: prep pass, then the FMA-bound search pass
+        case 5:  // split: prep pass, then the FFMA2 search pass
           launch(encode_warp_kernel<InT, 4, 4, 1>, 4, 4);
           launch(encode_warp_kernel<InT, 4, 2, 2>, 4, 2);
+          break;
+        default:  // split: prep pass, then the tensor-core search pass (S % 32 == 0)
+          launch(encode_warp_kernel<InT, 4, 4, 1>, 4, 4);
+          if (a->codebook_size % kTcBlk == 0) {
+            const size_t tsmem = 2 * 4096 + (size_t)(a->codebook_size / kTcBlk) * 4096 +
+                                 (size_t)a->codebook_size * 64;
+            cudaFuncSetAttribute(encode_tc_kernel<InT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)tsmem);
+            const int64_t ntiles = ceil_div(a->tokens, 4);
+            const int64_t want = std::max<int64_t>(1, ceil_div((int64_t)148 * 2, L.rows));
+            const int64_t bx = std::max<int64_t>(1, std::min<int64_t>(want, ceil_div(ntiles, 2)));
+            encode_tc_kernel<InT><<<dim3((unsigned)bx, (unsigned)L.rows), kTcThreads, tsmem, st>>>(p);
+          } else {
+            launch(encode_warp_kernel<InT, 4, 2, 2>, 4, 2);
+          }
           break;
       }
       e = cudaGetLastError();
