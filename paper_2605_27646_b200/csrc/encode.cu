@@ -813,18 +813,20 @@ __device__ __forceinline__ uint32_t pack2h(float lo, float hi) {
   return *reinterpret_cast<const uint32_t*>(&h);
 }
 
-template <typename InT>
-__global__ void __launch_bounds__(kTcThreads, 2) encode_tc_kernel(EncParams p) {
+template <typename InT, int kBlk = kTcBlk, int kMinB = 2>
+__global__ void __launch_bounds__(kTcThreads, kMinB) encode_tc_kernel(EncParams p) {
+  constexpr int kN = 4 * kBlk;           // MMA N (columns per group)
+  constexpr uint32_t kBB = kN * 32;      // bytes of one B block
   extern __shared__ __align__(1024) unsigned char tsm[];
   __shared__ uint32_t stage_i[kTcWarps][34];
   __shared__ __align__(8) uint64_t mbar[2];
   __shared__ uint32_t tmem_slot;
   const int S = p.S, w = p.w;
-  const int nblk = S / kTcBlk;
+  const int nblk = S / kBlk;
   // smem: A tiles (2 x 4 KB) | B operand (S/32 blocks x 4 KB) | fp32 rotation table
   unsigned char* asm_base = tsm;
   unsigned char* bsm = tsm + 2 * 4096;
-  float4* tab_s = reinterpret_cast<float4*>(bsm + (size_t)nblk * 4096);
+  float4* tab_s = reinterpret_cast<float4*>(bsm + (size_t)nblk * kBB);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int grp = warp >> 2, wl = warp & 3;
   const int64_t row = blockIdx.y;
@@ -835,9 +837,9 @@ __global__ void __launch_bounds__(kTcThreads, 2) encode_tc_kernel(EncParams p) {
   // ---- one-time setup: fp32 table, split-fp16 B operand, TMEM, barriers
   for (int i = tid; i < S * 4; i += kTcThreads) tab_s[i] = __ldg(rot + i);
   for (int n = tid; n < S * 4; n += kTcThreads) {
-    const int s = n >> 2, c = n & 3, blk = s / kTcBlk, nn = n - blk * kTcN;
+    const int s = n >> 2, c = n & 3, blk = s / kBlk, nn = n - blk * kN;
     const float* f = reinterpret_cast<const float*>(rot + 4 * s);
-    unsigned char* bb = bsm + (size_t)blk * 4096;
+    unsigned char* bb = bsm + (size_t)blk * kBB;
     uint32_t hi[2], lo[2];
 #pragma unroll
     for (int i = 0; i < 4; i += 2) {
@@ -855,7 +857,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) encode_tc_kernel(EncParams p) {
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&tmem_slot)),
-                 "n"(2 * kTcN));
+                 "n"(2 * kN));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
@@ -867,8 +869,8 @@ __global__ void __launch_bounds__(kTcThreads, 2) encode_tc_kernel(EncParams p) {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem = tmem_slot + (uint32_t)(grp * kTcN) + ((uint32_t)(wl * 32) << 16);
-  const uint32_t tmem_grp = tmem_slot + (uint32_t)(grp * kTcN);
+  const uint32_t tmem = tmem_slot + (uint32_t)(grp * kN) + ((uint32_t)(wl * 32) << 16);
+  const uint32_t tmem_grp = tmem_slot + (uint32_t)(grp * kN);
   unsigned char* at = asm_base + grp * 4096;
   const uint32_t a_saddr = smem_u32(at), b_saddr = smem_u32(bsm);
   uint32_t phase = 0;
@@ -927,11 +929,11 @@ __global__ void __launch_bounds__(kTcThreads, 2) encode_tc_kernel(EncParams p) {
     for (int blk = 0; blk < nblk; ++blk) {
       if (leader) {
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint64_t da = tc_desc(a_saddr), db = tc_desc(b_saddr + (uint32_t)blk * 4096u);
+        const uint64_t da = tc_desc(a_saddr), db = tc_desc(b_saddr + (uint32_t)blk * kBB);
         asm volatile(
             "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
             "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_grp),
-            "l"(da), "l"(db), "r"(tc_idesc(128, kTcN)), "r"(0));
+            "l"(da), "l"(db), "r"(tc_idesc(128, kN)), "r"(0));
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
             smem_u32(&mbar[grp])));
       }
@@ -939,7 +941,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) encode_tc_kernel(EncParams p) {
       phase ^= 1u;
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-      for (int q = 0; q < kTcN / 32; ++q) {
+      for (int q = 0; q < kN / 32; ++q) {
         float vals[32];
         tc_ld32(tmem + (uint32_t)(q * 32), vals);
 #pragma unroll
@@ -947,7 +949,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) encode_tc_kernel(EncParams p) {
           const float2 wx = make_float2(vals[4 * j], vals[4 * j + 1]);
           const float2 yz = make_float2(vals[4 * j + 2], vals[4 * j + 3]);
           const float sc = coset_score(wx, yz);
-          const int s = blk * kTcBlk + q * 8 + j;
+          const int s = blk * kBlk + q * 8 + j;
           const bool gt = sc > best;
           second = fmaxf(second, fminf(sc, best));
           best = fmaxf(best, sc);
@@ -1021,7 +1023,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) encode_tc_kernel(EncParams p) {
   __syncthreads();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_slot),
-                 "n"(2 * kTcN));
+                 "n"(2 * kN));
 }
 
 // Per-token coded (unflagged) chunk count from the stored norms (C = 32).
@@ -1515,21 +1517,26 @@ int launch_encode(const hqmq_encode_args* a, const Layout& L, cudaStream_t st) {
           launch(encode_warp_kernel<InT, 4, 4, 1>, 4, 4);
           launch(encode_warp_kernel<InT, 4, 2, 2>, 4, 2);
           break;
-        default:  // split: prep pass, then the tensor-core search pass (S % 32 == 0)
+        default: {  // split: prep pass, then the tensor-core search pass
           launch(encode_warp_kernel<InT, 4, 4, 1>, 4, 4);
-          if (a->codebook_size % kTcBlk == 0) {
-            const size_t tsmem = 2 * 4096 + (size_t)(a->codebook_size / kTcBlk) * 4096 +
+          auto tc = [&](auto kern, int blk, int minb) {
+            const size_t tsmem = 2 * 4096 + (size_t)a->codebook_size * 4 * 32 +
                                  (size_t)a->codebook_size * 64;
-            cudaFuncSetAttribute(encode_tc_kernel<InT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)tsmem);
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
             const int64_t ntiles = ceil_div(a->tokens, 4);
-            const int64_t want = std::max<int64_t>(1, ceil_div((int64_t)148 * 2, L.rows));
+            const int64_t want = std::max<int64_t>(1, ceil_div((int64_t)148 * minb, L.rows));
             const int64_t bx = std::max<int64_t>(1, std::min<int64_t>(want, ceil_div(ntiles, 2)));
-            encode_tc_kernel<InT><<<dim3((unsigned)bx, (unsigned)L.rows), kTcThreads, tsmem, st>>>(p);
+            kern<<<dim3((unsigned)bx, (unsigned)L.rows), kTcThreads, tsmem, st>>>(p);
+            (void)blk;
+          };
+          // (64-secondary blocks at 1 CTA/SM measured 2x slower: occupancy wins)
+          if (a->codebook_size % kTcBlk == 0) {
+            tc(encode_tc_kernel<InT, kTcBlk, 2>, kTcBlk, 2);
           } else {
             launch(encode_warp_kernel<InT, 4, 2, 2>, 4, 2);
           }
           break;
+        }
       }
       e = cudaGetLastError();
       return e == cudaSuccess ? HQMQ_OK : cuda_fail(e);
