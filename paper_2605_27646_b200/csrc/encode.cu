@@ -590,6 +590,74 @@ __global__ void __launch_bounds__(kWThreads, kMinB) encode_warp_kernel(EncParams
         }
       }
     } else {
+      if constexpr (kMode == 1) {
+      // ---- prep pass: only the squared norms are exact fp64 per chunk; the
+      // decisions that depend on r = sqrt_rn(s) use fp32 where provably on
+      // the same side as the exact value and replay exactly otherwise:
+      //   flag   r > thr        -> sqrt_gt (s vs thr^2 with a margin)
+      //   sigma  max_c r_c       =  sqrt_rn(max_c s_c): one sqrt per token
+      //   q      floor(r*top/sigma_w + 0.5) from fp32 unless near a boundary
+      const float ftop = (float)top;
+      const float qm = 4.0e-6f * (ftop + 1.0f);
+      double sq[kWT];
+      double sig_l = 0.0;  // lane j (< kWT) collects token j's max s
+  #pragma unroll
+      for (int j = 0; j < kWT; ++j) {
+        const InT* v = reinterpret_cast<const InT*>(&raw[j]);
+        double x[4];
+  #pragma unroll
+        for (int i = 0; i < 4; ++i) x[i] = In<InT>::d(v[i]);
+        double q2 = __dmul_rn(x[0], x[0]);
+        q2 = __dadd_rn(q2, __dmul_rn(x[1], x[1]));
+        q2 = __dadd_rn(q2, __dmul_rn(x[2], x[2]));
+        sq[j] = __dadd_rn(q2, __dmul_rn(x[3], x[3]));
+        const bool valid = j < ntok;
+        const bool fl = ext && valid && sqrt_gt(sq[j], thr);
+        fmask[j] = __ballot_sync(0xffffffffu, fl);
+        const double m = warp_max_f64(fl ? 0.0 : sq[j]);
+        sig_l = (lane % kWT) == j ? m : sig_l;
+      }
+      sig_l = __dsqrt_rn(sig_l);
+  #pragma unroll
+      for (int j = 0; j < kWT; ++j) {
+        const bool valid = j < ntok;
+        const bool fl = (fmask[j] >> lane) & 1u;
+        double sg = __shfl_sync(0xffffffffu, sig_l, j);
+        if (!(sg > 0.0)) sg = 1.0;
+        const __half hs = __double2half(sg);
+        const double sw = (double)__half2float(hs);
+        if (valid && lane == j) {
+          p.scales[tok0 + j] = __half_as_ushort(hs);
+          if (!(sw > 0.0)) atomicOr(p.err, HQMQ_DEVERR_SIGMA_NONPOSITIVE);
+        }
+        if (valid && !fl && sq[j] > 0.0) {
+          const float s32 = (float)sq[j];
+          uint32_t q;
+          const float vq = (s32 * rsqrtf(s32)) * __fdividef(ftop, (float)sw) + 0.5f;
+          const float fq = floorf(vq), fr = vq - fq;
+          if (s32 > 1e-30f && fr >= qm && fr <= 1.0f - qm) q = (uint32_t)fminf(fmaxf(fq, 0.f), ftop);
+          else q = exact_quantum(__dsqrt_rn(sq[j]), sw, top);
+          qpack |= q << (8 * j);
+        }
+        if (ext && valid) {
+          if (fl) {
+            const InT* v = reinterpret_cast<const InT*>(&raw[j]);
+            const uint64_t rel = coded_run + __popc(~fmask[j] & lanemask_lt);
+            const uint64_t prow = (uint64_t)(tok0 + j) * 32 + lane - (P0 + rel);
+            if (prow < (uint64_t)p.payload_capacity) {
+              ushort4 hv;
+              hv.x = __half_as_ushort(__double2half(In<InT>::d(v[0])));
+              hv.y = __half_as_ushort(__double2half(In<InT>::d(v[1])));
+              hv.z = __half_as_ushort(__double2half(In<InT>::d(v[2])));
+              hv.w = __half_as_ushort(__double2half(In<InT>::d(v[3])));
+              reinterpret_cast<ushort4*>(p.payloads)[prow] = hv;
+            }
+          }
+          if (lane == j) p.flagw[tok0 + j] = fmask[j];
+          coded_run += __popc(~fmask[j]);
+        }
+      }
+      } else {
       // ---- exact fp64 prologue: norms, flags, scales, quanta, payloads, fp32 dirs
   #pragma unroll
       for (int j = 0; j < kWT; ++j) {
@@ -635,7 +703,7 @@ __global__ void __launch_bounds__(kWThreads, kMinB) encode_warp_kernel(EncParams
           coded_run += __popc(~fmask[j]);
         }
       }
-
+      }
     }
 
     // ---- fp32 closed-form search over the S cosets (table broadcast from smem)
