@@ -1600,6 +1600,10 @@ int launch_encode(const hqmq_encode_args* a, const Layout& L, cudaStream_t st) {
           // (64-secondary blocks at 1 CTA/SM measured 2x slower: occupancy wins)
           if (a->codebook_size % kTcBlk == 0) {
             tc(encode_tc_kernel<InT, kTcBlk, 2>, kTcBlk, 2);
+          } else if (a->codebook_size % 16 == 0 && a->codebook_size >= 48) {
+            // e.g. S = 48: N = 64 blocks (at S = 16 the per-tile MMA round trip
+            // outweighs the work: measured 0.52 vs 0.47 ms, FFMA2 kept)
+            tc(encode_tc_kernel<InT, 16, 2>, 16, 2);
           } else {
             launch(encode_warp_kernel<InT, 4, 2, 2>, 4, 2);
           }
