@@ -108,8 +108,9 @@ def _dtype_code(dt) -> int:
 
 
 def _words(bits: int) -> int:
-    # +2 padding words: the bit reader always loads the word after the target.
-    return (bits + 31) // 32 + 2
+    # +4 padding words: the bit reader loads the word after the target and the
+    # Med3x TMA decode rounds its bulk copies up to 16 bytes.
+    return (bits + 31) // 32 + 4
 
 
 class QuantizedTensor:

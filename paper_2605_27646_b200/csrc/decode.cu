@@ -514,6 +514,182 @@ __global__ void __launch_bounds__(256) decode_flag_kernel(DecParams p) {
   if (bad) atomicOr(p.err, HQMQ_DEVERR_INDEX_RANGE);
 }
 
+// Med3x layout through the TMA ring (head_dim 128): a 64-token tile's coded
+// chunks are one contiguous run of the index / radius streams, [off[t0],
+// off[t0+63] + coded(t0+63)), so the producer bulk-copies that run (16-byte
+// aligned, with its base word recorded per stage) together with the tile's
+// flag words, token offsets and scales; warps then decode like the fast path
+// (warp = token, lane = chunk, coded position = token offset + ballot popc),
+// flagged lanes reading their fp16 payload row from global.
+constexpr int kFlTok = 64;
+constexpr int kFlStages = 4;
+
+struct FlagGeom {
+  uint32_t idx_off, rad_off, fl_off, to_off, sc_off, stage_bytes;
+};
+__host__ __device__ inline FlagGeom fl_geom(int w, int br) {
+  auto up = [](uint32_t x) { return (x + 127u) / 128u * 128u; };
+  FlagGeom g;
+  uint32_t o = 0;
+  g.idx_off = o; o += up((kFlTok * w + 8) * 4);
+  g.rad_off = o; o += up((kFlTok * br + 8) * 4);
+  g.fl_off = o; o += up(kFlTok * 4);
+  g.to_off = o; o += up(kFlTok * 4);
+  g.sc_off = o; o += up(kFlTok * 2);
+  g.stage_bytes = o;
+  return g;
+}
+
+template <typename OutT>
+__global__ void __launch_bounds__(256) decode_flag_tma_kernel(DecParams p) {
+  extern __shared__ __align__(128) unsigned char dsm[];
+  __shared__ __align__(8) uint64_t full[kFlStages];
+  __shared__ __align__(8) uint64_t tab_bar;
+  __shared__ unsigned int released[kFlStages];
+  __shared__ uint32_t base_w[kFlStages][2];  // first index / radius word of the stage
+  const int64_t row = blockIdx.y;
+  const int h = (int)(row % p.H);
+  const int ncw = kGroupOrder * p.S;
+  const int w = p.w, br = p.br;
+  const FlagGeom g = fl_geom(w, br);
+  constexpr bool k16 = sizeof(OutT) == 2;
+  float4* tab = reinterpret_cast<float4*>(dsm);
+  const size_t tbytes = ((size_t)ncw * (k16 ? 8 : 16) + 127) / 128 * 128;
+  unsigned char* ring = dsm + tbytes;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t ntile = ceil_div(p.nt, kFlTok);
+  const int64_t tok_base = row * p.T + p.t0;
+  const bool tab_tma = k16 && p.table16 != nullptr;
+
+  auto issue = [&](int64_t tile, int stage) {
+    const int64_t t = tok_base + tile * kFlTok;
+    const int ntok = (int)min((int64_t)kFlTok, p.nt - tile * kFlTok);
+    unsigned char* s = ring + (size_t)stage * g.stage_bytes;
+    const uint64_t c0 = __ldg(p.tokoff + t);
+    const uint64_t c1 = (uint64_t)__ldg(p.tokoff + t + ntok - 1) +
+                        (uint64_t)__popc(~__ldg(p.flagw + t + ntok - 1));
+    const uint64_t iw0 = ((c0 * (uint64_t)w) >> 5) & ~3ull;
+    const uint64_t iw1 = (((c1 * (uint64_t)w + 31) >> 5) + 3) & ~3ull;
+    const uint64_t rw0 = ((c0 * (uint64_t)br) >> 5) & ~3ull;
+    const uint64_t rw1 = (((c1 * (uint64_t)br + 31) >> 5) + 3) & ~3ull;
+    base_w[stage][0] = (uint32_t)iw0;  // low 32 bits suffice for relative offsets
+    base_w[stage][1] = (uint32_t)rw0;
+    const uint32_t ib = (uint32_t)(iw1 - iw0) * 4, rb = (uint32_t)(rw1 - rw0) * 4;
+    const uint32_t fb = ntok * 4, sb = ntok * 2;
+    fence_proxy_async();
+    mbar_arrive_expect_tx(&full[stage], ib + rb + 2 * fb + sb);
+    if (ib) bulk_g2s(s + g.idx_off, p.idxw + iw0, ib, &full[stage]);
+    if (rb) bulk_g2s(s + g.rad_off, p.radw + rw0, rb, &full[stage]);
+    bulk_g2s(s + g.fl_off, p.flagw + t, fb, &full[stage]);
+    bulk_g2s(s + g.to_off, p.tokoff + t, fb, &full[stage]);
+    bulk_g2s(s + g.sc_off, p.scales + t, sb, &full[stage]);
+  };
+
+  if (tid == 0) {
+    for (int st = 0; st < kFlStages; ++st) {
+      mbar_init(&full[st], 1);
+      released[st] = 0u;
+    }
+    mbar_init(&tab_bar, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  const float4* __restrict__ gtab = reinterpret_cast<const float4*>(p.table) + (int64_t)h * ncw;
+  if (tid == 0) {
+    if (tab_tma) {
+      const uint32_t tb = (uint32_t)ncw * 8u;
+      fence_proxy_async();
+      mbar_arrive_expect_tx(&tab_bar, tb);
+      bulk_g2s(tab, p.table16 + (int64_t)h * ncw, tb, &tab_bar);
+    }
+    int st = 0;
+    for (int64_t tile = blockIdx.x; tile < ntile && st < kFlStages; tile += gridDim.x, ++st)
+      issue(tile, st);
+  }
+  if constexpr (!k16) {
+    for (int i = tid; i < ncw; i += 256) tab[i] = __ldg(gtab + i);
+    __syncthreads();
+  } else if (!tab_tma) {
+    uint2* t16 = reinterpret_cast<uint2*>(tab);
+    for (int i = tid; i < ncw; i += 256) {
+      const float4 c = __ldg(gtab + i);
+      const __half2 a = __floats2half2_rn(c.x, c.y), b = __floats2half2_rn(c.z, c.w);
+      t16[i] = make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b));
+    }
+    __syncthreads();
+  } else {
+    mbar_wait(&tab_bar, 0u);
+  }
+  const uint32_t imask = w == 32 ? 0xffffffffu : ((1u << w) - 1u);
+  const uint32_t rmask = (1u << br) - 1u;
+  const float rtop = 1.0f / (float)((1 << br) - 1);
+  const uint32_t lt = (1u << lane) - 1u;
+  OutT* __restrict__ out = reinterpret_cast<OutT*>(p.out);
+  bool bad = false;
+  int k = 0;
+  for (int64_t tile = blockIdx.x; tile < ntile; tile += gridDim.x, ++k) {
+    const int stage = k % kFlStages;
+    mbar_wait(&full[stage], (uint32_t)((k / kFlStages) & 1));
+    const unsigned char* s = ring + (size_t)stage * g.stage_bytes;
+    const uint32_t* iw = reinterpret_cast<const uint32_t*>(s + g.idx_off);
+    const uint32_t* rw = reinterpret_cast<const uint32_t*>(s + g.rad_off);
+    const uint32_t* fls = reinterpret_cast<const uint32_t*>(s + g.fl_off);
+    const uint32_t* tos = reinterpret_cast<const uint32_t*>(s + g.to_off);
+    const uint16_t* scs = reinterpret_cast<const uint16_t*>(s + g.sc_off);
+    const uint32_t bi0 = base_w[stage][0], br0 = base_w[stage][1];
+    const int ntok = (int)min((int64_t)kFlTok, p.nt - tile * kFlTok);
+    for (int tt = warp; tt < ntok; tt += 8) {
+      const int64_t tok = tok_base + tile * kFlTok + tt;
+      const uint32_t fw = fls[tt];
+      const bool fl = (fw >> lane) & 1u;
+      const uint64_t pos = (uint64_t)tos[tt] + __popc(~fw & lt);
+      float v[4];
+      if (!fl) {
+        const uint32_t ib = (uint32_t)(pos * (uint64_t)w - (uint64_t)bi0 * 32u);
+        uint32_t idx = __funnelshift_r(iw[ib >> 5], iw[(ib >> 5) + 1], ib & 31) & imask;
+        const uint32_t rbit = (uint32_t)(pos * (uint64_t)br - (uint64_t)br0 * 32u);
+        const uint32_t q = __funnelshift_r(rw[rbit >> 5], rw[(rbit >> 5) + 1], rbit & 31) & rmask;
+        bad |= idx >= (uint32_t)ncw;
+        idx = idx < (uint32_t)ncw ? idx : 0u;
+        const float rad = (float)q * (__half2float(__ushort_as_half(scs[tt])) * rtop);
+        if constexpr (k16) {
+          const uint2 cw = reinterpret_cast<const uint2*>(tab)[idx];
+          const float2 c01 = __half22float2(*reinterpret_cast<const __half2*>(&cw.x));
+          const float2 c23 = __half22float2(*reinterpret_cast<const __half2*>(&cw.y));
+          v[0] = rad * c01.x; v[1] = rad * c01.y; v[2] = rad * c23.x; v[3] = rad * c23.y;
+        } else {
+          const float4 cw = tab[idx];
+          v[0] = rad * cw.x; v[1] = rad * cw.y; v[2] = rad * cw.z; v[3] = rad * cw.w;
+        }
+      } else {
+        const uint64_t prow = (uint64_t)tok * 32 + lane - pos;
+        const ushort4 hv = __ldg(reinterpret_cast<const ushort4*>(p.payloads) + prow);
+        v[0] = __half2float(__ushort_as_half(hv.x));
+        v[1] = __half2float(__ushort_as_half(hv.y));
+        v[2] = __half2float(__ushort_as_half(hv.z));
+        v[3] = __half2float(__ushort_as_half(hv.w));
+      }
+      OutT* o = out + (row * p.nt + tile * kFlTok + tt) * 128 + 4 * lane;
+      if constexpr (sizeof(OutT) == 4) {
+        *reinterpret_cast<float4*>(o) = make_float4(v[0], v[1], v[2], v[3]);
+      } else {
+        OutT t4[4] = {Out<OutT>::cvt(v[0]), Out<OutT>::cvt(v[1]), Out<OutT>::cvt(v[2]),
+                      Out<OutT>::cvt(v[3])};
+        *reinterpret_cast<uint2*>(o) = *reinterpret_cast<const uint2*>(t4);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      if (atomicAdd(&released[stage], 1u) == 7u) {
+        released[stage] = 0u;
+        const int64_t nxt = tile + (int64_t)kFlStages * gridDim.x;
+        if (nxt < ntile) issue(nxt, stage);
+      }
+    }
+  }
+  if (bad) atomicOr(p.err, HQMQ_DEVERR_INDEX_RANGE);
+}
+
 // Bit-exact fp64 decode: ((q * sigma_w) / top) * codeword (codec.py:315-320).
 __global__ void __launch_bounds__(kDecThreads) decode_f64_kernel(DecParams p) {
   const int64_t row = blockIdx.y;
@@ -666,6 +842,20 @@ int launch_decode(DecParams& p, const hqmq_decode_args* a, cudaStream_t st) {
   p.table = a->joint_f32;
   p.aligned4 = (p.D % 4 == 0) && (reinterpret_cast<uintptr_t>(a->out) % (4 * sizeof(OutT)) == 0);
   auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  if (p.D == 128 && p.flagw && p.tokoff && p.payloads && use_smem && p.aligned4 &&
+      p.T % 8 == 0 && p.t0 % 8 == 0 && p.nt % 8 == 0 && al16(p.idxw) && al16(p.radw) &&
+      al16(p.scales) && al16(p.flagw) && al16(p.tokoff)) {
+    const FlagGeom g = fl_geom(p.w, p.br);
+    const size_t fsmem = fd_table_bytes<OutT>(kGroupOrder * p.S) + (size_t)kFlStages * g.stage_bytes;
+    cudaFuncSetAttribute(decode_flag_tma_kernel<OutT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         200 * 1024);
+    const int64_t ntile = ceil_div(p.nt, kFlTok);
+    const int per_sm = std::max<int>(1, std::min<int>(8, (int)((227 * 1024) / (fsmem + 1024))));
+    const int64_t want = std::max<int64_t>(1, ceil_div((int64_t)148 * per_sm, rows));
+    const int64_t bx = std::max<int64_t>(1, std::min<int64_t>(want, ntile));
+    decode_flag_tma_kernel<OutT><<<dim3((unsigned)bx, (unsigned)rows), 256, fsmem, st>>>(p);
+    return check();
+  }
   if (p.D == 128 && p.flagw && p.tokoff && p.payloads && use_smem && p.aligned4) {
     const int64_t nwt = ceil_div(p.nt, 32);  // 8 warps x 4 tokens per CTA step
     const int64_t want = std::max<int64_t>(1, ceil_div((int64_t)148 * 4, rows));
