@@ -293,6 +293,28 @@ def test_full_size_c3_unit(cuda, oracle):
     assert m.to_bytes(qt) == oracle.to_bytes(ref)
 
 
+@pytest.mark.parametrize("C", [None, 3.0])
+def test_decode_token_ranges_fast_paths(cuda, C):
+    """Token-range decode through the TMA fast paths (head_dim 128, 8-aligned
+    ranges; Med3x and plain layouts) and the general path (unaligned ranges),
+    fp32 within 1e-6 of the bit-exact fp64 decode, fp16/bf16 within 1e-2."""
+    m = hq()
+    g = torch.Generator(device=cuda).manual_seed(11)
+    x = torch.randn((2, 4, 1024, 128), generator=g, device=cuda).half()
+    x[:, :, ::37, 8:12] *= 40.0  # outliers for Med3x
+    cfg = m.CodecConfig(64, 6 if C else 4, outlier_multiplier=C)
+    bank = m.CodebookBank(0, 64)
+    qt = m.encode_tensor(x, cfg, layer=2, role="V", bank=bank)
+    full64 = m.decode_tensor(qt, bank, dtype=torch.float64).cpu().numpy()
+    for a, b in ((0, 1024), (64, 512), (8, 16), (1016, 1024), (3, 77), (500, 501)):
+        want = full64[:, :, a:b]
+        got32 = m.decode_token_range(qt, bank, a, b, dtype=torch.float32).cpu().numpy()
+        assert_fp32_close(got32, want)
+        for dt in (torch.float16, torch.bfloat16):
+            got = m.decode_token_range(qt, bank, a, b, dtype=dt).double().cpu().numpy()
+            assert np.max(np.abs(got - want) / (np.abs(want) + 1e-2)) < 1e-2, (a, b, dt)
+
+
 def test_edge_cases(cuda):
     m = hq()
     cfg = m.CodecConfig(codebook_size=24, radius_bits=3, outlier_multiplier=3.0)
