@@ -888,6 +888,10 @@ __global__ void __launch_bounds__(kPThreads, 1) attention_prefill_kernel(AttPara
   }
 }
 
+size_t prefill_tc_workspace(const hqmq_attention_args* a);
+bool prefill_tc_applicable(const hqmq_attention_args* a);
+int launch_prefill_tc(const hqmq_attention_args* a, cudaStream_t st);
+
 namespace {
 
 struct AttPlan {
@@ -929,6 +933,7 @@ bool plan_att(const hqmq_attention_args* a, AttPlan& pl) {
   pl.splits = (int)ceil_div(a->kv_tokens, pl.keys_per_split);
   const int64_t parts = a->batch * a->kv_heads * nrows * pl.splits;
   pl.ws = pl.splits > 1 ? (size_t)parts * (a->head_dim + 2) * sizeof(float) + 256 : 0;
+  if (prefill_tc_applicable(a)) pl.ws = std::max(pl.ws, prefill_tc_workspace(a));
   return true;
 }
 
@@ -1000,6 +1005,11 @@ int hqmq_attention_decode(const hqmq_attention_args* a, void* stream) {
     case 12 * 16 + 3: mk = attention_mma_kernel<12, 3>; break;
     default: break;
   }
+  static const int prefill_variant = [] {
+    const char* v = getenv("HQMQ_PREFILL_VARIANT");  // 1: fused mma.sync prefill
+    return v ? atoi(v) : 0;
+  }();
+  if (prefill_variant == 0 && prefill_tc_applicable(a)) return launch_prefill_tc(a, st);
   const size_t psmem = prefill_smem_bytes(a->codebook_size);
   const bool prefill = a->head_dim == 128 && p.nrows > 8 && kPR % p.g == 0 && !a->precise &&
                        psmem <= 200 * 1024;
