@@ -144,7 +144,7 @@ __global__ void __launch_bounds__(kFaThreads, 2) attention_fa_tc_kernel(FaParams
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tm = tmem_slot;                  // S: cols [0, 64), O: cols [64, 192)
+  const uint32_t tm = tmem_slot;  // S(t & 1): cols [0, 64) / [64, 128), O: cols [128, 256)
   const uint32_t tm_row = tm + ((uint32_t)(warp * 32) << 16);
   const uint32_t q_sa = smem_u32(qs), p_sa = smem_u32(psm);
 
@@ -154,112 +154,139 @@ __global__ void __launch_bounds__(kFaThreads, 2) attention_fa_tc_kernel(FaParams
   const __half* vbase = p.v + bh * p.Tkv * kFaD;
   float m_run = -INFINITY, l_run = 0.f;
   uint32_t ph_s = 0, ph_o = 0;
-  int ntile = 0;
-  // K (K-major B: row = key) and V (MN-major B: n = dim, k = key) tiles of
-  // keys [k0, k0 + 64) into buffer b, asynchronously (zero-filled past kend)
-  auto load_tile = [&](int64_t k0, int bsel) {
-    unsigned char* ks = kvbuf + bsel * 2 * kKBytes;
-    unsigned char* vs = ks + kKBytes;
-    for (int i = tid; i < kFaKeys * (kFaD / 8); i += kFaThreads) {
-      const int key = i >> 4, dg = i & 15;
-      const bool ok = k0 + key < kend;
-      const int64_t kr = ok ? k0 + key : 0;
-      cp_async16(ks + (key >> 3) * kSboQK + dg * 128 + (key & 7) * 16,
-                 reinterpret_cast<const uint4*>(kbase + kr * kFaD) + dg, ok);
-      cp_async16(vs + dg * kSboV + (key >> 3) * 128 + (key & 7) * 16,
-                 reinterpret_cast<const uint4*>(vbase + kr * kFaD) + dg, ok);
+  const int ntiles = (int)((kend + kFaKeys - 1) / kFaKeys);
+  // K tiles run two ahead (K-major B: row = key), V tiles one ahead (MN-major
+  // B: n = dim, k = key), each double-buffered and zero-filled past kend; every
+  // call commits one cp.async group so the group count stays uniform
+  auto load_k = [&](int t) {
+    if (t < ntiles) {
+      unsigned char* ks = kvbuf + (t & 1) * kKBytes;
+      const int64_t k0 = (int64_t)t * kFaKeys;
+      for (int i = tid; i < kFaKeys * (kFaD / 8); i += kFaThreads) {
+        const int key = i >> 4, dg = i & 15;
+        const bool ok = k0 + key < kend;
+        cp_async16(ks + (key >> 3) * kSboQK + dg * 128 + (key & 7) * 16,
+                   reinterpret_cast<const uint4*>(kbase + (ok ? k0 + key : 0) * kFaD) + dg, ok);
+      }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
   };
-  if (kend > 0) load_tile(0, 0);
-  for (int64_t k0 = 0; k0 < kend; k0 += kFaKeys, ++ntile) {
-    const int nk = (int)std::min((int64_t)kFaKeys, kend - k0);
-    const int bsel = ntile & 1;
-    if (ntile > 0) {  // previous PV done with P and with the other K / V buffer
-      mbar_wait(&bar_o, ph_o);
-      ph_o ^= 1u;
+  auto load_v = [&](int t) {
+    if (t < ntiles) {
+      unsigned char* vs = kvbuf + (2 + (t & 1)) * kKBytes;
+      const int64_t k0 = (int64_t)t * kFaKeys;
+      for (int i = tid; i < kFaKeys * (kFaD / 8); i += kFaThreads) {
+        const int key = i >> 4, dg = i & 15;
+        const bool ok = k0 + key < kend;
+        cp_async16(vs + dg * kSboV + (key >> 3) * 128 + (key & 7) * 16,
+                   reinterpret_cast<const uint4*>(vbase + (ok ? k0 + key : 0) * kFaD) + dg, ok);
+      }
     }
-    if (k0 + kFaKeys < kend) {
-      load_tile(k0 + kFaKeys, bsel ^ 1);
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
-    } else {
-      asm volatile("cp.async.wait_group 0;" ::: "memory");
-    }
-    const uint32_t k_sa = smem_u32(kvbuf + bsel * 2 * kKBytes), v_sa = k_sa + kKBytes;
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  const uint32_t kv_sa = smem_u32(kvbuf);
+  auto issue_s = [&](int t) {  // S(t) = Q K(t)^T into TMEM columns (t & 1) * 64
+#pragma unroll
+    for (int kk = 0; kk < kFaD / 16; ++kk)
+      fa_mma(tm + (uint32_t)(t & 1) * 64, fa_desc(q_sa + kk * 256, kSboQK),
+             fa_desc(kv_sa + (t & 1) * kKBytes + kk * 256, kSboQK), fa_idesc(kFaRows, kFaKeys, 0),
+             kk > 0);
+    fa_commit(&bar_s);
+  };
+  if (ntiles > 0) {
+    load_k(0);
+    load_k(1);
+    load_v(0);
+    asm volatile("cp.async.wait_group 2;" ::: "memory");
     fence_proxy_async();
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (tid == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#pragma unroll
-      for (int kk = 0; kk < kFaD / 16; ++kk)
-        fa_mma(tm, fa_desc(q_sa + kk * 256, kSboQK), fa_desc(k_sa + kk * 256, kSboQK),
-               fa_idesc(kFaRows, kFaKeys, 0), kk > 0);
-      fa_commit(&bar_s);
+      issue_s(0);
     }
+  }
+  for (int t = 0; t < ntiles; ++t) {
+    const int64_t k0 = (int64_t)t * kFaKeys;
+    const int nk = (int)std::min((int64_t)kFaKeys, kend - k0);
+    // 1. scores of tile t
     mbar_wait(&bar_s, ph_s);
     ph_s ^= 1u;
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    // ---- this row's 64 scores: mask, online softmax, P -> smem
     uint32_t sr[64];
-    FA_LD32(tm_row, sr);
-    FA_LD32(tm_row + 32, (sr + 32));
+    FA_LD32(tm_row + (uint32_t)(t & 1) * 64, sr);
+    FA_LD32(tm_row + (uint32_t)(t & 1) * 64 + 32, (sr + 32));
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    // 2. K(t) is consumed: its buffer takes K(t+2)
+    load_k(t + 2);
+    // 3. online softmax (log2 domain), P in registers
     float mx = -INFINITY;
 #pragma unroll
     for (int j = 0; j < 64; ++j) {
       const int64_t key = k0 + j;
-      float s = __uint_as_float(sr[j]);
-      s = (rvalid && j < nk && key < vis) ? s : -INFINITY;
-      sr[j] = __float_as_uint(s);
-      mx = fmaxf(mx, s);
+      float sv = __uint_as_float(sr[j]);
+      sv = (rvalid && j < nk && key < vis) ? sv : -INFINITY;
+      sr[j] = __float_as_uint(sv);
+      mx = fmaxf(mx, sv);
     }
     const float m_new = fmaxf(m_run, mx);
     const float alpha = (m_new == -INFINITY) ? 1.f : exp2f(m_run - m_new);
     float psum = 0.f;
+    uint32_t hw[32];
 #pragma unroll
-    for (int kg = 0; kg < 8; ++kg) {
-      uint32_t hw[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float s0 = __uint_as_float(sr[kg * 8 + 2 * e]), s1 = __uint_as_float(sr[kg * 8 + 2 * e + 1]);
-        const float e0 = m_new == -INFINITY ? 0.f : exp2f(s0 - m_new);
-        const float e1 = m_new == -INFINITY ? 0.f : exp2f(s1 - m_new);
-        psum += e0 + e1;
-        const __half2 h = __floats2half2_rn(e0, e1);
-        hw[e] = *reinterpret_cast<const uint32_t*>(&h);
-      }
-      *reinterpret_cast<uint4*>(psm + (tid >> 3) * kSboP + kg * 128 + (tid & 7) * 16) =
-          make_uint4(hw[0], hw[1], hw[2], hw[3]);
+    for (int e = 0; e < 32; ++e) {
+      const float s0 = __uint_as_float(sr[2 * e]), s1 = __uint_as_float(sr[2 * e + 1]);
+      const float e0 = m_new == -INFINITY ? 0.f : exp2f(s0 - m_new);
+      const float e1 = m_new == -INFINITY ? 0.f : exp2f(s1 - m_new);
+      psum += e0 + e1;
+      const __half2 h = __floats2half2_rn(e0, e1);
+      hw[e] = *reinterpret_cast<const uint32_t*>(&h);
     }
     l_run = l_run * alpha + psum;
     m_run = m_new;
-    // rescale the O accumulator in TMEM when some row's running max moved
-    // (warp-uniform: tcgen05.ld / st are .sync.aligned; other rows scale by 1)
-    if (ntile > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+    // 4. PV(t-1) done: P smem, V buffer (t-1) & 1 and the O accumulator are free
+    if (t > 0) {
+      mbar_wait(&bar_o, ph_o);
+      ph_o ^= 1u;
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+    // 5. V(t+1) into the freed V buffer
+    load_v(t + 1);
+    // 6. rescale O in TMEM when some row's max moved (warp-uniform), write P(t)
+    if (t > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         uint32_t orr[32];
-        FA_LD32(tm_row + 64 + c * 32, orr);
+        FA_LD32(tm_row + 128 + c * 32, orr);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
         for (int j = 0; j < 32; ++j) orr[j] = __float_as_uint(__uint_as_float(orr[j]) * alpha);
-        FA_ST32(tm_row + 64 + c * 32, orr);
+        FA_ST32(tm_row + 128 + c * 32, orr);
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
     }
+#pragma unroll
+    for (int kg = 0; kg < 8; ++kg)
+      *reinterpret_cast<uint4*>(psm + (tid >> 3) * kSboP + kg * 128 + (tid & 7) * 16) =
+          make_uint4(hw[4 * kg], hw[4 * kg + 1], hw[4 * kg + 2], hw[4 * kg + 3]);
+    // 7. K(t+1) and V(t) have landed (the two newest groups may still fly)
+    asm volatile("cp.async.wait_group 2;" ::: "memory");
     fence_proxy_async();
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
+    // 8. O += P(t) V(t); then S(t+1)
     if (tid == 0) {
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
       for (int kk = 0; kk < kFaKeys / 16; ++kk)
-        fa_mma(tm + 64, fa_desc(p_sa + kk * 256, kSboP), fa_desc(v_sa + kk * 256, kSboV),
-               fa_idesc(kFaRows, kFaD, 1), (ntile > 0 || kk > 0) ? 1u : 0u);
+        fa_mma(tm + 128, fa_desc(p_sa + kk * 256, kSboP),
+               fa_desc(kv_sa + (2 + (t & 1)) * kKBytes + kk * 256, kSboV),
+               fa_idesc(kFaRows, kFaD, 1), (t > 0 || kk > 0) ? 1u : 0u);
       fa_commit(&bar_o);
+      if (t + 1 < ntiles) issue_s(t + 1);
     }
   }
+  const int ntile = ntiles;
   if (ntile > 0) {
     mbar_wait(&bar_o, ph_o);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -272,7 +299,7 @@ __global__ void __launch_bounds__(kFaThreads, 2) attention_fa_tc_kernel(FaParams
     for (int c = 0; c < 4; ++c) {
       uint32_t orr[32];
       if (ntile > 0) {
-        FA_LD32(tm_row + 64 + c * 32, orr);
+        FA_LD32(tm_row + 128 + c * 32, orr);
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
       } else {
 #pragma unroll
