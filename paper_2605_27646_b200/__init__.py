@@ -21,6 +21,7 @@ from .codec import (
     CodecConfig,
     QuantizedTensor,
     TensorShape,
+    append_tokens,
     decode_tensor,
     decode_token_range,
     encode_tensor,

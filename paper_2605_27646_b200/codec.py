@@ -466,3 +466,54 @@ def quantize_dequantize(data, config: CodecConfig, layer: int = 0, role: str = "
     """Fake-quant round trip (codec.py:339-349)."""
     bank = _bank_for(config, bank)
     return decode_tensor(encode_tensor(data, config, layer, role, bank, head_base), bank, dtype)
+
+
+def append_tokens(packed: QuantizedTensor, data, bank: CodebookBank | None = None) -> QuantizedTensor:
+    """Grow a compressed cache along the token axis:
+    encode `data` (batch, heads, new_tokens, head_dim) with the cache's config,
+    layer, role and head_base, and return the concatenated QuantizedTensor.
+
+    Without Med3x the encode is token-local (codec.py:258-274: sigma per token,
+    index per chunk), so the result is bit-identical to encode_tensor of the
+    concatenated input, and every token's codes occupy whole 32-bit words: the
+    append is the sm_100a encode of the new tokens plus row-strided device
+    copies of the sections.  With Med3x the reference pools the median over the
+    whole call (codec.py:208-219), so an exact append needs the full input;
+    that case raises InvalidArgument.
+    """
+    torch = _torch()
+    c, s = packed.config, packed.shape
+    if c.outlier_multiplier is not None:
+        raise InvalidArgument("append_tokens with outlier extraction: the Med3x median pools the "
+                              "whole call, re-encode the full tensor instead")
+    bank = _bank_for(c, bank)
+    new = encode_tensor(data, c, layer=packed.layer, role=packed.role, bank=bank,
+                        head_base=packed.head_base, device=packed.device)
+    ns = new.shape
+    if (ns.batch, ns.heads, ns.head_dim) != (s.batch, s.heads, s.head_dim):
+        raise InvalidArgument(f"appended data {tuple((ns.batch, ns.heads, ns.tokens, ns.head_dim))} "
+                              f"does not match the cache {tuple((s.batch, s.heads, s.tokens, s.head_dim))}")
+    shape = TensorShape(s.batch, s.heads, s.tokens + ns.tokens, s.head_dim)
+    rows, C = s.batch * s.heads, s.chunks_per_vector
+    dev = packed.device
+
+    def cat_words(old, fresh, width):
+        per_tok = C * width  # bits per token
+        if per_tok % 32:
+            raise InvalidArgument("token codes are not word-aligned for this head_dim / width")
+        wpt = per_tok // 32
+        out = torch.zeros(_words(shape.n_chunks * width), dtype=torch.int32, device=dev)
+        dst = out[: rows * shape.tokens * wpt].view(rows, shape.tokens * wpt)
+        dst[:, : s.tokens * wpt].copy_(old[: rows * s.tokens * wpt].view(rows, s.tokens * wpt))
+        dst[:, s.tokens * wpt:].copy_(fresh[: rows * ns.tokens * wpt].view(rows, ns.tokens * wpt))
+        return out
+
+    new.synchronize()
+    iw = cat_words(packed.index_words, new.index_words, c.index_bits)
+    rw = cat_words(packed.radius_words, new.radius_words, c.radius_bits)
+    scales = torch.cat([packed.scales, new.scales], dim=2).contiguous()
+    n = shape.n_chunks
+    meta = torch.tensor([n, 0, packed.n_fixup + new.n_fixup, 0], dtype=torch.int64, device=dev)
+    pay = torch.zeros((1, 4), dtype=torch.float16, device=dev)
+    return QuantizedTensor(shape, c, packed.layer, packed.role, packed.head_base, scales, iw, rw,
+                           None, pay, None, meta, dev, n_coded=n, n_payload=0)

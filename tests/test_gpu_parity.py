@@ -315,6 +315,28 @@ def test_decode_token_ranges_fast_paths(cuda, C):
             assert np.max(np.abs(got - want) / (np.abs(want) + 1e-2)) < 1e-2, (a, b, dt)
 
 
+def test_append_tokens_equals_full_encode(cuda):
+    """append_tokens (§8(f) rank 2): encode(A) then append(B), append(C) is
+    bit-identical to encode(A|B|C); Med3x and shape mismatches are refused."""
+    m = hq()
+    g = torch.Generator(device=cuda).manual_seed(21)
+    x = torch.randn((2, 4, 96, 128), generator=g, device=cuda).half()
+    cfg = m.CodecConfig(64, 4)
+    bank = m.CodebookBank(0, 64)
+    qt = m.encode_tensor(x[:, :, :40], cfg, layer=9, role="K", bank=bank, head_base=2)
+    qt = m.append_tokens(qt, x[:, :, 40:41], bank)      # one decode step
+    qt = m.append_tokens(qt, x[:, :, 41:], bank)        # a chunk
+    full = m.encode_tensor(x, cfg, layer=9, role="K", bank=bank, head_base=2)
+    assert m.to_bytes(qt) == m.to_bytes(full)
+    assert torch.equal(m.decode_tensor(qt, bank, dtype=torch.float64),
+                       m.decode_tensor(full, bank, dtype=torch.float64))
+    with pytest.raises(m.InvalidArgument):
+        m.append_tokens(qt, x[:, :2, :4], bank)
+    ext = m.encode_tensor(x[:, :, :8], m.CodecConfig(64, 4, outlier_multiplier=3.0), bank=bank)
+    with pytest.raises(m.InvalidArgument):
+        m.append_tokens(ext, x[:, :, 8:16], bank)
+
+
 def test_edge_cases(cuda):
     m = hq()
     cfg = m.CodecConfig(codebook_size=24, radius_bits=3, outlier_multiplier=3.0)
