@@ -35,7 +35,15 @@ from .errors import (
     NativeLibraryMissing,
     UnsupportedVersion,
 )
-from .kvpack import expected_file_size, from_bytes, read_kvpack, to_bytes, write_kvpack
+from .kvpack import (
+    expected_file_size,
+    from_bytes,
+    read_kvpack,
+    read_raw,
+    to_bytes,
+    write_kvpack,
+    write_raw,
+)
 from .scan import nearest_scan
 
 __version__ = "0.1.0"

@@ -247,3 +247,57 @@ def from_bytes(blob: bytes, device="cuda") -> QuantizedTensor:
     meta = torch.tensor([n_coded, n_flag, 0, 0], dtype=torch.int64, device=device)
     return QuantizedTensor(shape, config, layer, roles[role_tag], head_base, scales, iw, rw, fw,
                            pay, tok, meta, device, n_coded=n_coded, n_payload=n_flag)
+
+
+# ------------------------------------------------------------ raw tensors
+RAW_MAGIC = b"KVRW"
+_RAW_FMT = "<4sBIIII"
+_RAW_DTYPES = {0: np.float32, 1: np.float16}
+
+
+def write_raw(data, sink, dtype: str = "f32") -> int:
+    """Dense (batch, heads, tokens, head_dim) tensor file (kvpack.py:309-325):
+    header <4sBIIII> (magic, dtype code 0=f32 / 1=f16, shape), row-major body."""
+    codes = {"f32": 0, "f16": 1}
+    if dtype not in codes:
+        raise InvalidArgument(f"dtype must be f32 or f16, got {dtype!r}")
+    try:
+        import torch
+
+        if torch.is_tensor(data):
+            data = data.detach().cpu().numpy()
+    except ImportError:  # pragma: no cover
+        pass
+    data = np.asarray(data)
+    if data.ndim != 4:
+        raise InvalidArgument("raw tensors must be 4-d (batch, heads, tokens, head_dim)")
+    blob = struct.pack(_RAW_FMT, RAW_MAGIC, codes[dtype], *data.shape) + np.ascontiguousarray(
+        data.astype(np.dtype(_RAW_DTYPES[codes[dtype]]).newbyteorder("<"))).tobytes()
+    if hasattr(sink, "write"):
+        sink.write(blob)
+    else:
+        with open(sink, "wb") as f:
+            f.write(blob)
+    return len(blob)
+
+
+def read_raw(source) -> np.ndarray:
+    """kvpack.py:328-347, same validation and exceptions."""
+    if hasattr(source, "read"):
+        blob = source.read()
+    else:
+        with open(source, "rb") as f:
+            blob = f.read()
+    head = struct.calcsize(_RAW_FMT)
+    if len(blob) < head:
+        raise CorruptData("raw tensor file too short")
+    magic, code, b, h, t, d = struct.unpack_from(_RAW_FMT, blob, 0)
+    if magic != RAW_MAGIC:
+        raise CorruptData(f"bad raw magic {magic!r}")
+    if code not in _RAW_DTYPES:
+        raise CorruptData(f"unknown raw dtype code {code}")
+    dt = np.dtype(_RAW_DTYPES[code]).newbyteorder("<")
+    expected = head + b * h * t * d * dt.itemsize
+    if len(blob) != expected:
+        raise CorruptData(f"raw length {len(blob)} != expected {expected}")
+    return np.frombuffer(blob[head:], dtype=dt).reshape(b, h, t, d).copy()

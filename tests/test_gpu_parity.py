@@ -337,6 +337,25 @@ def test_append_tokens_equals_full_encode(cuda):
         m.append_tokens(ext, x[:, :, 8:16], bank)
 
 
+def test_cli_quantize_dequantize_vs_oracle(cuda, oracle, tmp_path):
+    """CLI front end (cli.py:151-173 of the reference): raw -> kvpack bytes equal
+    the oracle's serialisation of the same data; dequantize returns the decode."""
+    m = hq()
+    from paper_2605_27646_b200 import cli
+
+    x = oracle.gen_gaussian((1, 2, 48, 128), seed=5).astype(np.float32)
+    raw, pk, back = tmp_path / "x.raw", tmp_path / "x.kvpack", tmp_path / "y.raw"
+    m.write_raw(x, raw)
+    assert cli.main(["quantize", str(raw), str(pk), "--S", "64", "--br", "4", "--outlier-c", "3",
+                     "--role", "V", "--layer", "7", "--head", "1"]) == 0
+    ref = oracle.encode(x.astype(np.float64), 64, 4, multiplier=3.0, layer=7, role="V",
+                        head_base=1, threads=os.cpu_count() or 1)
+    assert pk.read_bytes() == oracle.to_bytes(ref)
+    assert cli.main(["dequantize", str(pk), str(back)]) == 0
+    np.testing.assert_array_equal(m.read_raw(back), oracle.decode(ref).astype(np.float32))
+    assert cli.main(["dequantize", str(raw), str(back)]) == 3  # not a kvpack file
+
+
 def test_edge_cases(cuda):
     m = hq()
     cfg = m.CodecConfig(codebook_size=24, radius_bits=3, outlier_multiplier=3.0)

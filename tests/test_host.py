@@ -108,3 +108,42 @@ def test_kvpack_header_validation_before_upload():
     bad[-4:] = struct.pack("<I", zlib.crc32(bytes(bad[:-4])) & 0xFFFFFFFF)
     with pytest.raises(m.UnsupportedVersion):
         m.from_bytes(bytes(bad))
+
+
+def test_raw_tensor_round_trip_and_validation(tmp_path):
+    """KVRW raw files (kvpack.py:309-347): host-side format, same checks."""
+    import numpy as np
+
+    x = np.arange(2 * 3 * 4 * 8, dtype=np.float32).reshape(2, 3, 4, 8) / 7.0
+    p = tmp_path / "x.raw"
+    n = m.write_raw(x, p)
+    assert n == struct.calcsize("<4sBIIII") + x.nbytes
+    np.testing.assert_array_equal(m.read_raw(p), x)
+    m.write_raw(x, p, dtype="f16")
+    np.testing.assert_array_equal(m.read_raw(p), x.astype(np.float16))
+    with pytest.raises(m.InvalidArgument):
+        m.write_raw(x, p, dtype="f64")
+    with pytest.raises(m.InvalidArgument):
+        m.write_raw(x[0], p)
+    blob = bytearray(p.read_bytes())
+    blob[0] ^= 1
+    p.write_bytes(bytes(blob))
+    with pytest.raises(m.CorruptData):
+        m.read_raw(p)
+    p.write_bytes(bytes(blob[:10]))
+    with pytest.raises(m.CorruptData):
+        m.read_raw(p)
+
+
+def test_cli_parser_matches_reference_options():
+    from paper_2605_27646_b200 import cli
+
+    a = cli.build_parser().parse_args(["quantize", "i", "o", "--S", "64", "--br", "4", "--outlier-c",
+                                       "3", "--per-head-median", "--role", "V", "--layer", "5",
+                                       "--head", "2"])
+    assert (a.S, a.br, a.outlier_c, a.per_head_median, a.role, a.layer, a.head) == (
+        64, 4, 3.0, True, "V", 5, 2)
+    a = cli.build_parser().parse_args(["dequantize", "i", "o", "--dtype", "f16"])
+    assert a.dtype == "f16"
+    with pytest.raises(SystemExit):
+        cli.build_parser().parse_args(["quantize", "i", "o"])
