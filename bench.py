@@ -453,6 +453,17 @@ def _attention_one(torch, hq, dev, T):
            "tok_per_s": round(B / (t_hq * 1e-3 * 32), 1),
            "tok_per_s_definition": "batch / (32 layers x per-layer decode-attention time)",
            "hqmq_compressed_gbs": round(nbytes / (t_hq * 1e-3) / 1e9, 1)}
+    # the same cache in 128-token pages handed out in random order (serving layout)
+    try:
+        cache = hq.PagedKVCache(cfgc, B, HKV, T, bank=bank, page_order_seed=0, device=dev)
+        cache.append(k, v)
+        out_pg = torch.empty_like(q)
+        t_pg = timeit(lambda: cache.attend(q, out=out_pg))
+        res["hqmq_paged_ms_per_layer"] = round(t_pg, 4)
+        res["hqmq_paged_max_abs_diff_vs_contiguous"] = float((out_pg - out).abs().max())
+        del cache
+    except Exception as exc:
+        res["hqmq_paged_error"] = repr(exc)[:200]
     # fp16 dense comparator: torch SDPA (cuDNN/flash backends) with GQA
     try:
         import torch.nn.functional as F

@@ -27,6 +27,8 @@
  *   hqmq_validate_indices    <- the index range checks of kvpack.from_bytes
  *                               (kvpack.py:279-280) / decode_token_range (codec.py:305-309)
  *   hqmq_attention_decode    <- attention.fused_attend       (attention.py:137-199)
+ *   hqmq_attention_decode_paged <- attention.fused_attend over a paged cache
+ *                               (the serving layout; the reference has no paging)
  *   hqmq_crc32               <- the zlib.crc32 trailer of kvpack.to_bytes / from_bytes
  *                               (kvpack.py:177, 219)
  */
@@ -226,6 +228,42 @@ typedef struct {
 
 size_t hqmq_attention_workspace_bytes(const hqmq_attention_args* args);
 int hqmq_attention_decode(const hqmq_attention_args* args, void* stream);
+
+/* ------------------------------------------------------ paged attention */
+/* Decode-step attention over a PAGED compressed cache (the serving layout;
+ * SURVEY.md §8(f) rank 2): a page holds page_tokens (= 128) consecutive tokens
+ * of ONE (sequence, kv head) row in the token-aligned stream format (no Med3x):
+ * page_tokens*index_bits index words, page_tokens*radius_bits radius words,
+ * page_tokens fp16 scales.  block_table[(b*kv_heads + h)*max_pages + i] is the
+ * page id holding tokens [128 i, 128 i + 128) of row (b, h); kv_lens[b] is
+ * sequence b's cache length (<= max_kv_tokens).  One query token per
+ * sequence; all cached keys visible.  Same numerics as hqmq_attention_decode. */
+typedef struct {
+  const uint32_t* index_pages;  /* [num_pages][page_tokens*index_bits] */
+  const uint32_t* radius_pages; /* [num_pages][page_tokens*radius_bits] */
+  const uint16_t* scale_pages;  /* [num_pages][page_tokens] */
+  const float* joint_f32;       /* [kv_heads][24*S][4] */
+  const uint16_t* joint_f16;    /* optional fp16 copy */
+} hqmq_paged_view;
+
+typedef struct {
+  int64_t batch, q_heads, kv_heads, head_dim;
+  int32_t codebook_size, radius_bits, index_bits, page_tokens;
+  int32_t max_pages, max_kv_tokens;
+  double scale;
+  const int32_t* kv_lens;     /* [batch], device */
+  const int32_t* block_table; /* [batch][kv_heads][max_pages], device */
+  const float* q;             /* (batch, q_heads, 1, head_dim) fp32 */
+  hqmq_paged_view k, v;
+  float* out;                 /* (batch, q_heads, 1, head_dim) fp32 */
+  int32_t num_splits;         /* 0 = choose automatically */
+  int32_t _pad;
+  void* workspace;
+  size_t workspace_bytes;
+} hqmq_paged_attention_args;
+
+size_t hqmq_paged_attention_workspace_bytes(const hqmq_paged_attention_args* args);
+int hqmq_attention_decode_paged(const hqmq_paged_attention_args* args, void* stream);
 
 /* ------------------------------------------------------------ kvpack CRC */
 /* zlib-compatible CRC-32 (reflected 0xEDB88320, init and xorout 0xFFFFFFFF) of

@@ -44,6 +44,7 @@ from .kvpack import (
     write_kvpack,
     write_raw,
 )
+from .paged import PagedKVCache
 from .scan import nearest_scan
 
 __version__ = "0.1.0"

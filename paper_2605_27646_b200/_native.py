@@ -81,6 +81,27 @@ class AttentionArgs(ctypes.Structure):
     ]
 
 
+class PagedView(ctypes.Structure):
+    _fields_ = [
+        ("index_pages", c_vp), ("radius_pages", c_vp), ("scale_pages", c_vp),
+        ("joint_f32", c_vp), ("joint_f16", c_vp),
+    ]
+
+
+class PagedAttentionArgs(ctypes.Structure):
+    _fields_ = [
+        ("batch", c_i64), ("q_heads", c_i64), ("kv_heads", c_i64), ("head_dim", c_i64),
+        ("codebook_size", c_i32), ("radius_bits", c_i32), ("index_bits", c_i32),
+        ("page_tokens", c_i32),
+        ("max_pages", c_i32), ("max_kv_tokens", c_i32),
+        ("scale", ctypes.c_double),
+        ("kv_lens", c_vp), ("block_table", c_vp), ("q", c_vp),
+        ("k", PagedView), ("v", PagedView), ("out", c_vp),
+        ("num_splits", c_i32), ("_pad", c_i32),
+        ("workspace", c_vp), ("workspace_bytes", ctypes.c_size_t),
+    ]
+
+
 # Every symbol include/hqmq_b200.h declares, with its ctypes signature.
 SIGNATURES = {
     "hqmq_version": ([], ctypes.c_char_p),
@@ -100,6 +121,8 @@ SIGNATURES = {
     "hqmq_validate_indices": ([c_vp, c_i64, c_i32, c_i64, c_vp, c_vp], c_i32),
     "hqmq_attention_workspace_bytes": ([ctypes.POINTER(AttentionArgs)], ctypes.c_size_t),
     "hqmq_attention_decode": ([ctypes.POINTER(AttentionArgs), c_vp], c_i32),
+    "hqmq_paged_attention_workspace_bytes": ([ctypes.POINTER(PagedAttentionArgs)], ctypes.c_size_t),
+    "hqmq_attention_decode_paged": ([ctypes.POINTER(PagedAttentionArgs), c_vp], c_i32),
     "hqmq_crc32_workspace_bytes": ([ctypes.c_uint64], ctypes.c_size_t),
     "hqmq_crc32": ([c_vp, ctypes.c_uint64, c_vp, c_vp, ctypes.c_size_t, c_vp], c_i32),
 }

@@ -52,6 +52,11 @@ struct AttParams {
   float* out;
   float* part_o;   // [B*Hkv][rows][splits][D]
   float* part_ml;  // [B*Hkv][rows][splits][2]
+  // paged cache (decode serving layout): per-sequence lengths and the block
+  // table of 128-token pages per (sequence, kv head) row
+  const int32_t* kv_lens;
+  const int32_t* block_table;
+  int max_pages;
 };
 
 __device__ __forceinline__ float4 decode_chunk(const AttView& v, const float4* tab, int64_t tok,
@@ -358,7 +363,7 @@ struct CodeRun {
   }
 };
 
-template <int W, int BR>
+template <int W, int BR, bool kPaged = false>
 __global__ void __launch_bounds__(kMThreads, 2) attention_mma_kernel(AttParams p) {
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ __align__(8) uint64_t full[kMStages];
@@ -376,7 +381,8 @@ __global__ void __launch_bounds__(kMThreads, 2) attention_mma_kernel(AttParams p
   const int64_t bh = blockIdx.y;
   const int64_t b = bh / p.Hkv, hkv = bh % p.Hkv;
   const int64_t kbeg = (int64_t)blockIdx.x * p.keys_per_split;
-  const int64_t kend = min(p.Tkv, kbeg + p.keys_per_split);
+  const int64_t tkv = kPaged ? (int64_t)__ldg(p.kv_lens + b) : p.Tkv;  // this sequence's keys
+  const int64_t kend = min(tkv, kbeg + p.keys_per_split);
   const int64_t ntile = kend > kbeg ? ceil_div(kend - kbeg, kMT) : 0;
   const int64_t tokrow = bh * p.Tkv;
 
@@ -391,8 +397,12 @@ __global__ void __launch_bounds__(kMThreads, 2) attention_mma_kernel(AttParams p
   __syncthreads();
 
   auto issue = [&](int64_t k, int stage) {
-    const int64_t t = tokrow + kbeg + k * kMT;
-    const int ntok = (int)min((int64_t)kMT, kend - (kbeg + k * kMT));
+    int64_t t = tokrow + kbeg + k * kMT;
+    int ntok = (int)min((int64_t)kMT, kend - (kbeg + k * kMT));
+    if constexpr (kPaged) {  // tile = one whole page (keys past kend are masked)
+      t = (int64_t)__ldg(p.block_table + bh * p.max_pages + (kbeg + k * kMT) / kMT) * kMT;
+      ntok = kMT;
+    }
     unsigned char* s = ring + (size_t)stage * gm.bytes;
     const uint32_t ib = ntok * w * 4, rb = ntok * br * 4, sb = ntok * 2;
     fence_proxy_async();
@@ -462,8 +472,8 @@ __global__ void __launch_bounds__(kMThreads, 2) attention_mma_kernel(AttParams p
       qa[ks][1] = pack_half2(v.z * p.scale_log2, v.w * p.scale_log2);
     }
   }
-  int64_t vis = p.Tkv;  // keys j < vis are visible to row g4
-  if (row_valid && p.causal) vis = (g4 % (int)p.Tq) + (p.Tkv - p.Tq) + 1;
+  int64_t vis = tkv;  // keys j < vis are visible to row g4
+  if (row_valid && p.causal) vis = (g4 % (int)p.Tq) + (tkv - p.Tq) + 1;
   const float rtop = 1.0f / (float)((1 << br) - 1);
 
   for (int64_t k = 0; k < ntile; ++k) {
@@ -966,6 +976,7 @@ int hqmq_attention_decode(const hqmq_attention_args* a, void* stream) {
   p.scale_log2 = (float)(a->scale * 1.4426950408889634);
   p.splits = pl.splits; p.keys_per_split = pl.keys_per_split;
   p.nrows = (int)(p.g * a->q_tokens);
+  p.kv_lens = nullptr; p.block_table = nullptr; p.max_pages = 0;
   p.q = a->q;
   auto view = [](const hqmq_packed_view& v) {
     AttView o;
@@ -1044,6 +1055,101 @@ int hqmq_attention_decode(const hqmq_attention_args* a, void* stream) {
   } else {
     attention_split_kernel<false><<<grid, kAttThreads, 0, st>>>(p);
   }
+  int rc = check_launch();
+  if (rc != HQMQ_OK) return rc;
+  if (pl.splits > 1) {
+    combine_kernel<<<dim3((unsigned)(a->batch * a->kv_heads), (unsigned)p.nrows), 128, 0, st>>>(p);
+    rc = check_launch();
+  }
+  return rc;
+}
+
+namespace {
+struct PagedPlan {
+  int splits;
+  int64_t keys_per_split;
+  size_t ws;
+};
+bool plan_paged(const hqmq_paged_attention_args* a, PagedPlan& pl) {
+  using namespace hqmq;
+  if (!a || a->batch < 1 || a->q_heads < 1 || a->kv_heads < 1 || a->head_dim != 128) return false;
+  if (a->q_heads % a->kv_heads || a->q_heads / a->kv_heads > 8) return false;
+  if (a->page_tokens != kMT || a->max_pages < 1 || a->max_kv_tokens < 1) return false;
+  if ((int64_t)a->max_kv_tokens > (int64_t)a->max_pages * kMT) return false;
+  const int64_t ctas = a->batch * a->kv_heads;
+  int splits = a->num_splits;
+  if (splits <= 0) {  // same per-SM load model as the contiguous path
+    int64_t best = INT64_MAX;
+    splits = 1;
+    const int64_t max_s = std::max<int64_t>(1, std::min<int64_t>(64, ceil_div(a->max_kv_tokens, 256)));
+    for (int64_t s = 1; s <= max_s; ++s) {
+      const int64_t tiles = ceil_div(ceil_div(a->max_kv_tokens, s), kMT);
+      const int64_t cost = ceil_div(ctas * s, 148) * (tiles + 3);
+      if (cost < best) {
+        best = cost;
+        splits = (int)s;
+      }
+    }
+  }
+  pl.keys_per_split = ceil_div(ceil_div(a->max_kv_tokens, splits), kMT) * kMT;
+  pl.splits = (int)ceil_div(a->max_kv_tokens, pl.keys_per_split);
+  const int64_t nrows = a->q_heads / a->kv_heads;
+  pl.ws = pl.splits > 1 ? (size_t)ctas * nrows * pl.splits * (128 + 2) * sizeof(float) + 256 : 0;
+  return true;
+}
+}  // namespace
+
+size_t hqmq_paged_attention_workspace_bytes(const hqmq_paged_attention_args* a) {
+  PagedPlan pl;
+  return plan_paged(a, pl) ? pl.ws : 0;
+}
+
+int hqmq_attention_decode_paged(const hqmq_paged_attention_args* a, void* stream) {
+  using namespace hqmq;
+  PagedPlan pl;
+  if (!plan_paged(a, pl)) return HQMQ_ERR_INVALID_ARGUMENT;
+  if (a->workspace_bytes < pl.ws) return HQMQ_ERR_WORKSPACE;
+  auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  if (!al16(a->k.index_pages) || !al16(a->k.radius_pages) || !al16(a->k.scale_pages) ||
+      !al16(a->v.index_pages) || !al16(a->v.radius_pages) || !al16(a->v.scale_pages))
+    return HQMQ_ERR_INVALID_ARGUMENT;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  AttParams p;
+  p.B = a->batch; p.Hq = a->q_heads; p.Hkv = a->kv_heads; p.Tq = 1; p.Tkv = a->max_kv_tokens;
+  p.D = 128; p.C = 32; p.S = a->codebook_size; p.br = a->radius_bits; p.w = a->index_bits;
+  p.g = (int)(a->q_heads / a->kv_heads); p.causal = 1;
+  p.scale_log2 = (float)(a->scale * 1.4426950408889634);
+  p.splits = pl.splits; p.keys_per_split = pl.keys_per_split;
+  p.nrows = p.g;
+  p.q = a->q;
+  auto view = [](const hqmq_paged_view& v) {
+    AttView o;
+    o.scales = v.scale_pages; o.idxw = v.index_pages; o.radw = v.radius_pages;
+    o.flagw = nullptr; o.payloads = nullptr; o.tokoff = nullptr;
+    o.table = reinterpret_cast<const float4*>(v.joint_f32);
+    o.table16 = reinterpret_cast<const uint2*>(v.joint_f16);
+    return o;
+  };
+  p.k = view(a->k);
+  p.v = view(a->v);
+  p.out = a->out;
+  float* ws = reinterpret_cast<float*>(a->workspace);
+  const int64_t parts = a->batch * a->kv_heads * p.nrows * pl.splits;
+  p.part_o = ws;
+  p.part_ml = ws ? ws + parts * 128 : nullptr;
+  p.kv_lens = a->kv_lens; p.block_table = a->block_table; p.max_pages = a->max_pages;
+  void (*mk)(AttParams) = nullptr;
+  switch (a->index_bits * 16 + a->radius_bits) {
+    case 9 * 16 + 4: mk = attention_mma_kernel<9, 4, true>; break;
+    case 11 * 16 + 4: mk = attention_mma_kernel<11, 4, true>; break;
+    case 13 * 16 + 4: mk = attention_mma_kernel<13, 4, true>; break;
+    case 11 * 16 + 6: mk = attention_mma_kernel<11, 6, true>; break;
+    default: return HQMQ_ERR_UNSUPPORTED;
+  }
+  const size_t msmem = mma_smem_bytes(a->codebook_size, a->index_bits, a->radius_bits);
+  if (msmem > 200 * 1024) return HQMQ_ERR_UNSUPPORTED;
+  cudaFuncSetAttribute(mk, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  mk<<<dim3((unsigned)pl.splits, (unsigned)(a->batch * a->kv_heads)), kMThreads, msmem, st>>>(p);
   int rc = check_launch();
   if (rc != HQMQ_OK) return rc;
   if (pl.splits > 1) {

@@ -1,0 +1,174 @@
+"""Paged HQMQ KV cache for decode-time serving (append
+encode into a paged layout; north star: decode fused inside a *paged*
+decode-attention kernel).
+
+The reference keeps one dense tensor per (layer, role) and has no append
+(codec.py:232-287).  Here a cache for one layer holds K and V as pools of
+128-token pages; a page is one (sequence, kv head) row's tokens
+[128 i, 128 i + 128) in the token-aligned stream format the encoder already
+produces without Med3x (index_bits words of index codes, radius_bits words of
+radius codes and one fp16 scale per token), so appending is:
+
+  1. encode_tensor of the new tokens (the sm_100a encode, bit-identical to the
+     reference on those tokens: without extraction the codec is token-local);
+  2. a row scatter of each new token's code words into its page slot
+     (device index_copy); pages are taken from a free list as rows grow.
+
+attend() runs the decode-attention kernel with a block table
+(hqmq_attention_decode_paged).  Med3x is not supported here: its median
+pools the whole (layer, role) call, which an append cannot reproduce.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+from . import _native as nat
+from .codebook import CodebookBank
+from .codec import CodecConfig, _bank_for, _torch, encode_tensor
+from .errors import InvalidArgument
+
+PAGE_TOKENS = 128
+
+
+class PagedKVCache:
+    """K/V page pools of one layer for `batch` sequences of up to `max_tokens`."""
+
+    def __init__(self, config: CodecConfig, batch: int, kv_heads: int, max_tokens: int,
+                 layer: int = 0, bank: CodebookBank | None = None, head_base: int = 0,
+                 head_dim: int = 128, num_pages: int | None = None, device="cuda",
+                 page_order_seed: int | None = None):
+        torch = _torch()
+        if config.outlier_multiplier is not None:
+            raise InvalidArgument("paged caches hold token-aligned streams: no outlier extraction")
+        if head_dim != 128:
+            raise InvalidArgument("paged caches support head_dim 128")
+        if batch < 1 or kv_heads < 1 or max_tokens < 1:
+            raise InvalidArgument("batch, kv_heads and max_tokens must be positive")
+        nat.require_cuda(device)
+        self.config, self.layer, self.head_base = config, layer, head_base
+        self.bank = _bank_for(config, bank)
+        self.batch, self.kv_heads, self.head_dim = batch, kv_heads, head_dim
+        self.device = torch.device(device)
+        self.max_pages = math.ceil(max_tokens / PAGE_TOKENS)
+        self.max_tokens = self.max_pages * PAGE_TOKENS
+        rows = batch * kv_heads
+        self.num_pages = num_pages if num_pages is not None else rows * self.max_pages
+        w, br = config.index_bits, config.radius_bits
+        dev = self.device
+        self.pages = {}
+        for role in ("K", "V"):
+            self.pages[role] = {
+                "index": torch.zeros((self.num_pages, PAGE_TOKENS * w), dtype=torch.int32, device=dev),
+                "radius": torch.zeros((self.num_pages, PAGE_TOKENS * br), dtype=torch.int32,
+                                      device=dev),
+                "scales": torch.zeros((self.num_pages, PAGE_TOKENS), dtype=torch.float16, device=dev),
+            }
+        self.block_table = torch.full((batch, kv_heads, self.max_pages), -1, dtype=torch.int32,
+                                      device=dev)
+        self._table_host = [[[-1] * self.max_pages for _ in range(kv_heads)] for _ in range(batch)]
+        self.lengths = [0] * batch
+        self.kv_lens = torch.zeros(batch, dtype=torch.int32, device=dev)
+        self._free = list(range(self.num_pages - 1, -1, -1))
+        if page_order_seed is not None:  # a fragmented pool: pages handed out in random order
+            import random
+
+            random.Random(page_order_seed).shuffle(self._free)
+
+    # ------------------------------------------------------------ append
+    def _page(self, b: int, h: int, i: int) -> int:
+        pid = self._table_host[b][h][i]
+        if pid < 0:
+            if not self._free:
+                raise InvalidArgument("page pool exhausted")
+            pid = self._free.pop()
+            self._table_host[b][h][i] = pid
+        return pid
+
+    def append(self, k, v, seqs=None) -> None:
+        """Append new tokens (len(seqs), kv_heads, n_new, head_dim) for the listed
+        sequences (default: all, in order)."""
+        torch = _torch()
+        seqs = list(range(self.batch)) if seqs is None else list(seqs)
+        if len(set(seqs)) != len(seqs) or any(not 0 <= b < self.batch for b in seqs):
+            raise InvalidArgument(f"seqs must be distinct sequence ids in [0, {self.batch})")
+        shape = tuple(k.shape)
+        if shape != tuple(v.shape) or len(shape) != 4 or shape[0] != len(seqs) or \
+                shape[1] != self.kv_heads or shape[3] != self.head_dim:
+            raise InvalidArgument(f"k/v shape {shape} does not match the cache")
+        n_new = shape[2]
+        if n_new == 0:
+            return
+        for b in seqs:
+            if self.lengths[b] + n_new > self.max_tokens:
+                raise InvalidArgument(f"sequence {b} would exceed {self.max_tokens} tokens")
+        # take pages for the new tokens, then the destination slot
+        # (page * 128 + offset) of every new token in encode order (seq, head, token)
+        for b in seqs:
+            first, last = self.lengths[b] // PAGE_TOKENS, (self.lengths[b] + n_new - 1) // PAGE_TOKENS
+            for h in range(self.kv_heads):
+                for i in range(first, last + 1):
+                    self._page(b, h, i)
+        self.block_table.copy_(torch.tensor(self._table_host, dtype=torch.int32))
+        dev = self.device
+        sel = torch.tensor(seqs, dtype=torch.int64, device=dev)
+        t = torch.tensor([self.lengths[b] for b in seqs], dtype=torch.int64, device=dev)[:, None, None] \
+            + torch.arange(n_new, device=dev)[None, None, :]
+        heads = torch.arange(self.kv_heads, device=dev)[None, :, None]
+        page = self.block_table[sel[:, None, None], heads, t // PAGE_TOKENS].to(torch.int64)
+        slots = (page * PAGE_TOKENS + t % PAGE_TOKENS).reshape(-1)
+        n_tok = slots.numel()
+        w, br = self.config.index_bits, self.config.radius_bits
+        for role, x in (("K", k), ("V", v)):
+            qt = encode_tensor(x, self.config, layer=self.layer, role=role, bank=self.bank,
+                               head_base=self.head_base, device=self.device)
+            pool = self.pages[role]
+            pool["index"].view(-1, w).index_copy_(0, slots, qt.index_words[: n_tok * w].view(n_tok, w))
+            pool["radius"].view(-1, br).index_copy_(0, slots,
+                                                    qt.radius_words[: n_tok * br].view(n_tok, br))
+            pool["scales"].view(-1).index_copy_(0, slots, qt.scales.reshape(-1))
+        for b in seqs:
+            self.lengths[b] += n_new
+        self.kv_lens.copy_(torch.tensor(self.lengths, dtype=torch.int32))
+
+    # ------------------------------------------------------------ attend
+    def attend(self, q, scale: float | None = None, out=None, num_splits: int = 0):
+        """One decode step: q (batch, q_heads, 1, head_dim) fp32 -> attention over
+        each sequence's cached keys (fused decode, paged block table)."""
+        torch = _torch()
+        B, HQ, TQ, D = q.shape
+        if B != self.batch or TQ != 1 or D != self.head_dim or HQ % self.kv_heads:
+            raise InvalidArgument(f"q shape {tuple(q.shape)} does not match the cache")
+        if max(self.lengths) == 0:
+            raise InvalidArgument("empty cache")
+        q = q.to(device=self.device, dtype=torch.float32).contiguous()
+        if out is None:
+            out = torch.empty_like(q)
+        c = self.config
+        a = nat.PagedAttentionArgs()
+        a.batch, a.q_heads, a.kv_heads, a.head_dim = B, HQ, self.kv_heads, D
+        a.codebook_size, a.radius_bits, a.index_bits = c.codebook_size, c.radius_bits, c.index_bits
+        a.page_tokens, a.max_pages = PAGE_TOKENS, self.max_pages
+        a.max_kv_tokens = max(self.lengths)
+        a.scale = float(scale if scale is not None else D ** -0.5)
+        a.kv_lens, a.block_table = self.kv_lens.data_ptr(), self.block_table.data_ptr()
+        a.q, a.out = q.data_ptr(), out.data_ptr()
+        for role, view in (("K", a.k), ("V", a.v)):
+            tabs = self.bank.device_tables(self.layer, self.head_base, self.kv_heads, role,
+                                           self.device)
+            pool = self.pages[role]
+            view.index_pages = pool["index"].data_ptr()
+            view.radius_pages = pool["radius"].data_ptr()
+            view.scale_pages = pool["scales"].data_ptr()
+            view.joint_f32 = tabs["joint_f32"].data_ptr()
+            view.joint_f16 = tabs["joint_f16"].data_ptr()
+        a.num_splits = num_splits
+        L = nat.lib()
+        ws_bytes = int(L.hqmq_paged_attention_workspace_bytes(ctypes.byref(a)))
+        ws = torch.empty(max(1, ws_bytes), dtype=torch.uint8, device=self.device)
+        a.workspace, a.workspace_bytes = ws.data_ptr(), ws_bytes
+        nat.check(L.hqmq_attention_decode_paged(ctypes.byref(a), nat.stream_handle(self.device)),
+                  "hqmq_attention_decode_paged")
+        out._ws = ws
+        return out
