@@ -951,92 +951,97 @@ __global__ void __launch_bounds__(kTcThreads, kMinB) encode_tc_kernel(EncParams 
   const bool ext = p.tokoff != nullptr;
   const bool leader = wl == 0 && lane == 0;
 
-  int64_t tile = (int64_t)blockIdx.x * 2 + grp;
-  uint2 raw = make_uint2(0u, 0u);
   auto load = [&](int64_t t4) {
     const int64_t t = t4 * 4 + wl;
     return (t4 < ntiles && t < p.T)
                ? __ldg(reinterpret_cast<const uint2*>(data + (row * p.T + t) * 128) + lane)
                : make_uint2(0u, 0u);
   };
-  raw = load(tile);
-  for (; tile < ntiles; tile += stride) {
-    const uint2 nxt = load(tile + stride);
-    const int64_t t = tile * 4 + wl;  // this warp's token
-    const bool valid = t < p.T;
-    const int64_t tok = row * p.T + t;
-    // ---- direction, liveness, A row (m = 32 wl + lane)
-    const uint32_t fmask = (ext && valid) ? __ldg(p.flagw + tok) : 0u;
-    const bool fl = (fmask >> lane) & 1u;
-    const InT* v = reinterpret_cast<const InT*>(&raw);
+  // this thread's chunk of a tile: token, flags, fp32 direction; writes the
+  // split-fp16 A row (m = 32 wl + lane) into the A buffer `ab`
+  struct TokState {
+    int64_t tok;
+    uint32_t fmask;
+    bool valid, fl, live;
+    float4 u4;
+  };
+  auto prepare = [&](int64_t tl, uint2 rv, unsigned char* ab) {
+    TokState st;
+    const int64_t t = tl * 4 + wl;
+    st.valid = tl < ntiles && t < p.T;
+    st.tok = row * p.T + t;
+    st.fmask = (ext && st.valid) ? __ldg(p.flagw + st.tok) : 0u;
+    st.fl = (st.fmask >> lane) & 1u;
+    const InT* v = reinterpret_cast<const InT*>(&rv);
     InT vv[4] = {v[0], v[1], v[2], v[3]};
-    const bool nz = (raw.x | raw.y) & 0x7fff7fffu;
-    const bool live = valid && !fl && nz;
-    float4 u4 = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (live) {
+    const bool nz = (rv.x | rv.y) & 0x7fff7fffu;
+    st.live = st.valid && !st.fl && nz;
+    st.u4 = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (st.live) {
       double x[4] = {0.0, 0.0, 0.0, 0.0};
       const Dir2 d = fast_dir_lazy_norm(vv, x);
-      u4 = make_float4(d.a.x, d.b.x, d.c.x, d.d.x);
+      st.u4 = make_float4(d.a.x, d.b.x, d.c.x, d.d.x);
     }
-    {
-      const __half h0 = __float2half_rn(u4.x), h1 = __float2half_rn(u4.y);
-      const __half h2 = __float2half_rn(u4.z), h3 = __float2half_rn(u4.w);
-      const uint32_t u1a = pack2h(__half2float(h0), __half2float(h1));
-      const uint32_t u1b = pack2h(__half2float(h2), __half2float(h3));
-      const uint32_t u2a = pack2h(u4.x - __half2float(h0), u4.y - __half2float(h1));
-      const uint32_t u2b = pack2h(u4.z - __half2float(h2), u4.w - __half2float(h3));
-      const int m = wl * 32 + lane;
-      *reinterpret_cast<uint4*>(at + tc_kmaj(m, 0)) = make_uint4(u1a, u1b, u1a, u1b);
-      *reinterpret_cast<uint4*>(at + tc_kmaj(m, 8)) = make_uint4(u2a, u2b, 0u, 0u);
+    const float4 u4 = st.u4;
+    const __half h0 = __float2half_rn(u4.x), h1 = __float2half_rn(u4.y);
+    const __half h2 = __float2half_rn(u4.z), h3 = __float2half_rn(u4.w);
+    const uint32_t u1a = pack2h(__half2float(h0), __half2float(h1));
+    const uint32_t u1b = pack2h(__half2float(h2), __half2float(h3));
+    const uint32_t u2a = pack2h(u4.x - __half2float(h0), u4.y - __half2float(h1));
+    const uint32_t u2b = pack2h(u4.z - __half2float(h2), u4.w - __half2float(h3));
+    const int m = wl * 32 + lane;
+    *reinterpret_cast<uint4*>(ab + tc_kmaj(m, 0)) = make_uint4(u1a, u1b, u1a, u1b);
+    *reinterpret_cast<uint4*>(ab + tc_kmaj(m, 8)) = make_uint4(u2a, u2b, 0u, 0u);
+    return st;
+  };
+  auto issue_mma = [&](uint32_t a_addr, int blk) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint64_t da = tc_desc(a_addr), db = tc_desc(b_saddr + (uint32_t)blk * kBB);
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_grp),
+        "l"(da), "l"(db), "r"(tc_idesc(128, kN)), "r"(0));
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+        smem_u32(&mbar[grp])));
+  };
+  // score one block of 32 (or 16) secondaries from TMEM, tracking the top two
+  auto score_block = [&](int blk, float& best, float& second, int& bs) {
+    mbar_wait(&mbar[grp], phase);
+    phase ^= 1u;
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // (two 32-column loads per tcgen05.wait::ld measured 2% slower: registers)
+#pragma unroll
+    for (int q = 0; q < kN / 32; ++q) {
+      float vals[32];
+      tc_ld32(tmem + (uint32_t)(q * 32), vals);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const float2 wx = make_float2(vals[4 * j], vals[4 * j + 1]);
+        const float2 yz = make_float2(vals[4 * j + 2], vals[4 * j + 3]);
+        const float sc = coset_score(wx, yz);
+        const int s = blk * kBlk + q * 8 + j;
+        const bool gt = sc > best;
+        second = fmaxf(second, fminf(sc, best));
+        best = fmaxf(best, sc);
+        bs = gt ? s : bs;
+      }
     }
-    fence_proxy_async();
+    // TMEM reads done before the next MMA overwrites it.  (Issuing the next
+  // tile's first MMA here, into a second A buffer, so it runs under this
+  // tile's certification, measured 3.6% slower than the plain order.)
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
-    // ---- per block of 32 secondaries: MMA into TMEM, then score from TMEM
-    float best = -1.f, second = -1.f;
-    int bs = 0;
-    for (int blk = 0; blk < nblk; ++blk) {
-      if (leader) {
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint64_t da = tc_desc(a_saddr), db = tc_desc(b_saddr + (uint32_t)blk * kBB);
-        asm volatile(
-            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_grp),
-            "l"(da), "l"(db), "r"(tc_idesc(128, kN)), "r"(0));
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-            smem_u32(&mbar[grp])));
-      }
-      mbar_wait(&mbar[grp], phase);
-      phase ^= 1u;
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#pragma unroll
-      for (int q = 0; q < kN / 32; ++q) {
-        float vals[32];
-        tc_ld32(tmem + (uint32_t)(q * 32), vals);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float2 wx = make_float2(vals[4 * j], vals[4 * j + 1]);
-          const float2 yz = make_float2(vals[4 * j + 2], vals[4 * j + 3]);
-          const float sc = coset_score(wx, yz);
-          const int s = blk * kBlk + q * 8 + j;
-          const bool gt = sc > best;
-          second = fmaxf(second, fminf(sc, best));
-          best = fmaxf(best, sc);
-          bs = gt ? s : bs;
-        }
-      }
-      // TMEM reads done before the next MMA (or the next tile's) overwrites it
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
-    }
-    // ---- certification (exact fp32 rotation of the chosen secondary) + fixup
+  };
+  // certification (exact fp32 rotation of the chosen secondary), fixup, packing
+  auto finish = [&](const TokState& st, int bs, float second) {
     int idx = 0;
     bool unsure = false;
-    if (live) {
+    if (st.live) {
       Dir2 d;
-      d.a = make_float2(u4.x, u4.x);
-      d.b = make_float2(u4.y, u4.y);
-      d.c = make_float2(u4.z, u4.z);
-      d.d = make_float2(u4.w, u4.w);
+      d.a = make_float2(st.u4.x, st.u4.x);
+      d.b = make_float2(st.u4.y, st.u4.y);
+      d.c = make_float2(st.u4.z, st.u4.z);
+      d.d = make_float2(st.u4.w, st.u4.w);
       float2 wx, yz;
       rotate(d, tab_s[4 * bs], tab_s[4 * bs + 1], tab_s[4 * bs + 2], tab_s[4 * bs + 3], wx, yz);
       int pidx;
@@ -1054,7 +1059,7 @@ __global__ void __launch_bounds__(kTcThreads, kMinB) encode_tc_kernel(EncParams 
     while (um) {
       const int L = __ffs(um) - 1;
       um &= um - 1;
-      const uint2 rw = __ldg(reinterpret_cast<const uint2*>(data + tok * 128) + L);
+      const uint2 rw = __ldg(reinterpret_cast<const uint2*>(data + st.tok * 128) + L);
       const InT* vr = reinterpret_cast<const InT*>(&rw);
       InT vx[4] = {vr[0], vr[1], vr[2], vr[3]};
       double x[4];
@@ -1065,14 +1070,13 @@ __global__ void __launch_bounds__(kTcThreads, kMinB) encode_tc_kernel(EncParams 
       const int ex = warp_exact_index(x, rl, ud, tab_s, joint, S, lane);
       if (lane == L) idx = ex;
     }
-    // ---- pack this token's index codes
-    if (valid) {
-      const uint64_t P0 = ext ? (uint64_t)__ldg(p.tokoff + tok) : (uint64_t)tok * 32;
+    if (st.valid) {
+      const uint64_t P0 = ext ? (uint64_t)__ldg(p.tokoff + st.tok) : (uint64_t)st.tok * 32;
       const uint32_t lbi = (uint32_t)((P0 * (uint64_t)w) & 31);
-      const uint32_t rel = __popc(~fmask & lanemask_lt);
-      if (!fl) stage_bits(st_i, (uint64_t)lbi + (uint64_t)rel * w, (uint32_t)idx, w);
+      const uint32_t rel = __popc(~st.fmask & lanemask_lt);
+      if (!st.fl) stage_bits(st_i, (uint64_t)lbi + (uint64_t)rel * w, (uint32_t)idx, w);
       __syncwarp();
-      const uint32_t coded = __popc(~fmask);
+      const uint32_t coded = __popc(~st.fmask);
       const uint64_t end = lbi + (uint64_t)coded * w;
       const uint32_t nw = (uint32_t)((end + 31) >> 5);
       const uint64_t gw0 = (P0 * (uint64_t)w) >> 5;
@@ -1085,6 +1089,22 @@ __global__ void __launch_bounds__(kTcThreads, kMinB) encode_tc_kernel(EncParams 
       }
       __syncwarp();
     }
+  };
+
+  int64_t tile = (int64_t)blockIdx.x * 2 + grp;
+  uint2 raw = load(tile);
+  for (; tile < ntiles; tile += stride) {
+    const uint2 nxt = load(tile + stride);
+    const TokState cur = prepare(tile, raw, at);
+    fence_proxy_async();
+    asm volatile("bar.sync %0, 128;" ::"r"(1 + grp) : "memory");
+    float best = -1.f, second = -1.f;
+    int bs = 0;
+    for (int blk = 0; blk < nblk; ++blk) {
+      if (leader) issue_mma(a_saddr, blk);
+      score_block(blk, best, second, bs);
+    }
+    finish(cur, bs, second);
     raw = nxt;
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1586,27 +1606,31 @@ int launch_encode(const hqmq_encode_args* a, const Layout& L, cudaStream_t st) {
           launch(encode_warp_kernel<InT, 4, 2, 2>, 4, 2);
           break;
         default: {  // split: prep pass, then the tensor-core search pass
+          const bool tc32 = a->codebook_size % kTcBlk == 0;
+          // e.g. S = 48: N = 64 blocks (at S = 16 the per-tile MMA round trip
+          // outweighs the work: measured 0.52 vs 0.47 ms, FFMA2 kept)
+          const bool tc16 = !tc32 && a->codebook_size % 16 == 0 && a->codebook_size >= 48;
+          if (!tc32 && !tc16) {
+            launch(encode_warp_kernel<InT, 4, 4, 1>, 4, 4);
+            launch(encode_warp_kernel<InT, 4, 2, 2>, 4, 2);
+            break;
+          }
+          // the prep stays a pass of its own: fusing it into the tensor-core
+          // kernel (run under the first MMA of each tile) measured 1.7% slower
+          // at S = 64 and 2.7% at S = 256
           launch(encode_warp_kernel<InT, 4, 4, 1>, 4, 4);
-          auto tc = [&](auto kern, int blk, int minb) {
+          auto tc = [&](auto kern) {
             const size_t tsmem = 2 * 4096 + (size_t)a->codebook_size * 4 * 32 +
                                  (size_t)a->codebook_size * 64;
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tsmem);
             const int64_t ntiles = ceil_div(a->tokens, 4);
-            const int64_t want = std::max<int64_t>(1, ceil_div((int64_t)148 * minb, L.rows));
+            const int64_t want = std::max<int64_t>(1, ceil_div((int64_t)148 * 2, L.rows));
             const int64_t bx = std::max<int64_t>(1, std::min<int64_t>(want, ceil_div(ntiles, 2)));
             kern<<<dim3((unsigned)bx, (unsigned)L.rows), kTcThreads, tsmem, st>>>(p);
-            (void)blk;
           };
           // (64-secondary blocks at 1 CTA/SM measured 2x slower: occupancy wins)
-          if (a->codebook_size % kTcBlk == 0) {
-            tc(encode_tc_kernel<InT, kTcBlk, 2>, kTcBlk, 2);
-          } else if (a->codebook_size % 16 == 0 && a->codebook_size >= 48) {
-            // e.g. S = 48: N = 64 blocks (at S = 16 the per-tile MMA round trip
-            // outweighs the work: measured 0.52 vs 0.47 ms, FFMA2 kept)
-            tc(encode_tc_kernel<InT, 16, 2>, 16, 2);
-          } else {
-            launch(encode_warp_kernel<InT, 4, 2, 2>, 4, 2);
-          }
+          if (tc32) tc(encode_tc_kernel<InT, kTcBlk, 2>);
+          else tc(encode_tc_kernel<InT, 16, 2>);
           break;
         }
       }
