@@ -19,6 +19,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -320,10 +321,302 @@ __global__ void __launch_bounds__(kFaThreads, 2) attention_fa_tc_kernel(FaParams
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "n"(256));
 }
 
+// ------------------------------------------------------------------------
+// Warp-specialised version (default).  CTA = 2 query tiles of 128 rows (256
+// rows = (256 / g) tokens x g heads of one kv head), 10 warps:
+//   warps 0-3 / 4-7  softmax of query tile 0 / 1 (thread = row = TMEM lane)
+//   warp 8           producer: one 1-D bulk copy (TMA) per K / V tile from the
+//                    workspace, where the decode left them pre-arranged in the
+//                    UMMA canonical layouts (16 KB per 64-key tile)
+//   warp 9           MMA issuer (one thread)
+// TMEM (512 columns): S0 double buffer [0,128), S1 [128,256), O0 [256,384),
+// O1 [384,512).  MMA order S0(0) S1(0) | S0(t+1) S1(t+1) PV0(t) PV1(t) | ...:
+// the scores of tile t+1 are computed while both softmax groups work on tile
+// t, and each PV as soon as its P is in shared memory.  A 3-stage K/V
+// ring (full / empty mbarriers; the stage is released by tcgen05.commit after
+// the last MMA that reads it).  The running max is only raised when a row's
+// tile max exceeds it by more than 8 (log2 domain): exponents stay <= 2^8 in
+// fp16 P, O is rescaled in TMEM far less often, and O / l is unchanged.
+constexpr int kF2Keys = 64, kF2Stages = 3, kF2Threads = 320;
+constexpr uint32_t kF2TileBytes = kF2Keys * kFaD * 2;  // 16 KB
+constexpr uint32_t kF2QOff = 0, kF2KVOff = 2 * kQBytes;
+constexpr uint32_t kF2POff = kF2KVOff + kF2Stages * 2 * kF2TileBytes;
+constexpr uint32_t kF2Smem = kF2POff + 2 * kF2Keys * kFaRows * 2;
+
+struct Fa2Params {
+  int64_t B, Hq, Hkv, Tq, Tkv, ntk;
+  int g, causal;
+  float scale_log2;
+  const float* q;
+  const unsigned char* kt;  // [B*Hkv][ntk] K tiles, K-major canonical
+  const unsigned char* vt;  // [B*Hkv][ntk] V tiles, MN-major canonical
+  float* out;
+};
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__global__ void __launch_bounds__(kF2Threads, 1) attention_fa2_kernel(Fa2Params p) {
+  extern __shared__ __align__(1024) unsigned char fsm[];
+  __shared__ __align__(8) uint64_t full[kF2Stages], empty[kF2Stages];
+  __shared__ __align__(8) uint64_t bar_s[2], bar_p[2], bar_o[2];
+  __shared__ uint32_t tmem_slot;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t bh = blockIdx.y;
+  const int64_t b = bh / p.Hkv, hkv = bh % p.Hkv;
+  const int g = p.g;
+  const int tpt = 2 * kFaRows / g;
+  const int64_t tok0 = (int64_t)blockIdx.x * tpt;
+  const int64_t off = p.causal ? (p.Tkv - p.Tq) : 0;
+  const int64_t last_tok = std::min(p.Tq, tok0 + tpt) - 1;
+  const int64_t kend = p.causal ? std::min(p.Tkv, last_tok + off + 1) : p.Tkv;
+  const int ntiles = kend > 0 ? (int)((kend + kF2Keys - 1) / kF2Keys) : 0;
+
+  if (warp == 9) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_slot)),
+                 "n"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < kF2Stages; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bar_s[i], 1);
+      mbar_init(&bar_p[i], kFaRows);
+      mbar_init(&bar_o[i], 1);
+    }
+    fence_mbar_init();
+  }
+  // softmax threads: this thread's row and its Q row -> fp16 (pre-scaled) A operand
+  const int wg = tid >> 7, r = tid & 127;
+  const int crow = wg * kFaRows + r;
+  const int64_t qtok = tok0 + crow / g;
+  const int qhead = crow % g;
+  const bool rvalid = tid < 2 * kFaRows && qtok < p.Tq;
+  const int64_t vis = p.causal ? std::min(qtok + off + 1, p.Tkv) : p.Tkv;
+  if (tid < 2 * kFaRows) {
+    unsigned char* qs = fsm + kF2QOff + wg * kQBytes;
+    const float4* qr = reinterpret_cast<const float4*>(
+        p.q + ((b * p.Hq + hkv * g + qhead) * p.Tq + (rvalid ? qtok : 0)) * kFaD);
+#pragma unroll 4
+    for (int kg = 0; kg < kFaD / 8; ++kg) {
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f), c = a;
+      if (rvalid) {
+        a = __ldg(qr + 2 * kg);
+        c = __ldg(qr + 2 * kg + 1);
+      }
+      const float sl = p.scale_log2;
+      const __half2 h0 = __floats2half2_rn(a.x * sl, a.y * sl), h1 = __floats2half2_rn(a.z * sl, a.w * sl);
+      const __half2 h2 = __floats2half2_rn(c.x * sl, c.y * sl), h3 = __floats2half2_rn(c.z * sl, c.w * sl);
+      *reinterpret_cast<uint4*>(qs + (r >> 3) * kSboQK + kg * 128 + (r & 7) * 16) =
+          make_uint4(*reinterpret_cast<const uint32_t*>(&h0), *reinterpret_cast<const uint32_t*>(&h1),
+                     *reinterpret_cast<const uint32_t*>(&h2), *reinterpret_cast<const uint32_t*>(&h3));
+    }
+  }
+  fence_proxy_async();
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tm = tmem_slot;
+  const uint32_t sbase = smem_u32(fsm);
+  auto kv_smem = [&](int stage, int which) {
+    return kF2KVOff + (uint32_t)(stage * 2 + which) * kF2TileBytes;
+  };
+
+  if (warp == 8) {
+    // ---- producer
+    if (lane == 0) {
+      const unsigned char* kb = p.kt + (size_t)bh * p.ntk * kF2TileBytes;
+      const unsigned char* vb = p.vt + (size_t)bh * p.ntk * kF2TileBytes;
+      for (int t = 0; t < ntiles; ++t) {
+        const int st = t % kF2Stages;
+        if (t >= kF2Stages) mbar_wait(&empty[st], (uint32_t)((t / kF2Stages) - 1) & 1u);
+        mbar_arrive_expect_tx(&full[st], 2 * kF2TileBytes);
+        bulk_g2s(fsm + kv_smem(st, 0), kb + (size_t)t * kF2TileBytes, kF2TileBytes, &full[st]);
+        bulk_g2s(fsm + kv_smem(st, 1), vb + (size_t)t * kF2TileBytes, kF2TileBytes, &full[st]);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 9) {
+    // ---- MMA issuer
+    if (lane == 0 && ntiles > 0) {
+      auto s_mma = [&](int i, int t) {  // S_i(t) = Q_i K(t)^T -> TMEM cols 128 i + 64 (t & 1)
+        const int st = t % kF2Stages;
+#pragma unroll
+        for (int kk = 0; kk < kFaD / 16; ++kk)
+          fa_mma(tm + (uint32_t)i * 128 + (uint32_t)(t & 1) * 64, fa_desc(sbase + kF2QOff + i * kQBytes + kk * 256, kSboQK),
+                 fa_desc(sbase + kv_smem(st, 0) + kk * 256, kSboQK), fa_idesc(kFaRows, kF2Keys, 0),
+                 kk > 0);
+        fa_commit(&bar_s[i]);
+      };
+      auto pv_mma = [&](int i, int t) {  // O_i += P_i V(t) -> TMEM cols 256 + 128 i
+        const int st = t % kF2Stages;
+#pragma unroll
+        for (int kk = 0; kk < kF2Keys / 16; ++kk)
+          fa_mma(tm + 256 + (uint32_t)i * 128,
+                 fa_desc(sbase + kF2POff + i * (kF2Keys * kFaRows * 2) + kk * 256, kSboP),
+                 fa_desc(sbase + kv_smem(st, 1) + kk * 256, kSboV), fa_idesc(kFaRows, kFaD, 1),
+                 (t > 0 || kk > 0) ? 1u : 0u);
+        fa_commit(&bar_o[i]);
+      };
+      mbar_wait(&full[0], 0);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      s_mma(0, 0);
+      s_mma(1, 0);
+      for (int t = 0; t < ntiles; ++t) {
+        const uint32_t ph = (uint32_t)t & 1u;
+        // S(t+1) into the other S buffers: group i finished reading them
+        // (tile t-1) before its P(t-1) arrival, already waited for below
+        if (t + 1 < ntiles) {
+          mbar_wait(&full[(t + 1) % kF2Stages], (uint32_t)((t + 1) / kF2Stages) & 1u);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          s_mma(0, t + 1);
+          s_mma(1, t + 1);
+        }
+        mbar_wait(&bar_p[0], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        pv_mma(0, t);
+        mbar_wait(&bar_p[1], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        pv_mma(1, t);
+        fa_commit(&empty[t % kF2Stages]);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---- softmax (warps 0-7): thread = row r of query tile wg
+    const uint32_t tm_row = tm + ((uint32_t)((warp & 3) * 32) << 16);
+    const uint32_t o_col = 256 + (uint32_t)wg * 128;
+    unsigned char* psm = fsm + kF2POff + wg * (kF2Keys * kFaRows * 2);
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int t = 0; t < ntiles; ++t) {
+      const uint32_t ph = (uint32_t)t & 1u;
+      const int64_t k0 = (int64_t)t * kF2Keys;
+      mbar_wait(&bar_s[wg], ph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const uint32_t s_col = (uint32_t)wg * 128 + ph * 64;
+      uint32_t sr[64];
+      FA_LD32(tm_row + s_col, sr);
+      FA_LD32(tm_row + s_col + 32, (sr + 32));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (!rvalid || k0 + kF2Keys > vis) {  // causal / tail / padding-row mask
+#pragma unroll
+        for (int j = 0; j < 64; ++j)
+          if (!rvalid || k0 + j >= vis) sr[j] = __float_as_uint(-INFINITY);
+      }
+      float mx = -INFINITY;
+#pragma unroll
+      for (int j = 0; j < 64; ++j) mx = fmaxf(mx, __uint_as_float(sr[j]));
+      const float m_new = (mx > m_run + 8.f) ? mx : m_run;  // also true when m_run = -inf
+      const float alpha = (m_new == m_run) ? 1.f : exp2f(m_run - m_new);
+      const float m_use = m_new == -INFINITY ? 0.f : m_new;  // all-masked row: exp2(-inf) = 0
+      float psum = 0.f;
+      uint32_t hw[32];
+#pragma unroll
+      for (int e = 0; e < 32; ++e) {
+        const float e0 = exp2f(__uint_as_float(sr[2 * e]) - m_use);
+        const float e1 = exp2f(__uint_as_float(sr[2 * e + 1]) - m_use);
+        psum += e0 + e1;
+        const __half2 h = __floats2half2_rn(e0, e1);
+        hw[e] = *reinterpret_cast<const uint32_t*>(&h);
+      }
+      l_run = l_run * alpha + psum;
+      m_run = m_new;
+      // PV(t-1) done: P buffer and O accumulator are free
+      if (t > 0) {
+        mbar_wait(&bar_o[wg], ph ^ 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (__any_sync(0xffffffffu, alpha != 1.f)) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint32_t orr[32];
+            FA_LD32(tm_row + o_col + c * 32, orr);
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int j = 0; j < 32; ++j) orr[j] = __float_as_uint(__uint_as_float(orr[j]) * alpha);
+            FA_ST32(tm_row + o_col + c * 32, orr);
+          }
+          asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        }
+      }
+#pragma unroll
+      for (int kg = 0; kg < 8; ++kg)
+        *reinterpret_cast<uint4*>(psm + (r >> 3) * kSboP + kg * 128 + (r & 7) * 16) =
+            make_uint4(hw[4 * kg], hw[4 * kg + 1], hw[4 * kg + 2], hw[4 * kg + 3]);
+      fence_proxy_async();
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(&bar_p[wg]);
+    }
+    if (ntiles > 0) {
+      mbar_wait(&bar_o[wg], (uint32_t)(ntiles - 1) & 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+    float* orow = p.out + ((b * p.Hq + hkv * g + qhead) * p.Tq + (rvalid ? qtok : 0)) * kFaD;
+    const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint32_t orr[32];
+      if (ntiles > 0) {
+        FA_LD32(tm_row + o_col + c * 32, orr);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) orr[j] = 0u;
+      }
+      if (rvalid) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4)
+          *reinterpret_cast<float4*>(orow + c * 32 + j) =
+              make_float4(__uint_as_float(orr[j]) * inv, __uint_as_float(orr[j + 1]) * inv,
+                          __uint_as_float(orr[j + 2]) * inv, __uint_as_float(orr[j + 3]) * inv);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 9)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "n"(512));
+}
+
+// Linear decoded fp16 (B*Hkv, T, 128) -> 64-key UMMA tiles (16-byte units):
+//   K-major (K):  unit(key, dg) at (key/8)*128 + dg*8 + key%8
+//   MN-major (V): unit(key, dg) at dg*64 + (key/8)*8 + key%8
+// keys past T are zero-filled (masked P = 0 must not meet a NaN in V).
+__global__ void fa_tile_kernel(const uint4* __restrict__ lin, uint4* __restrict__ tiles, int64_t BH,
+                               int64_t T, int64_t ntk, int mn_major) {
+  const int64_t per_bh = ntk * kF2Keys * 16;
+  const int64_t n = BH * per_bh;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int dg = (int)(i & 15);
+    const int64_t bh = i / per_bh, tok = (i - bh * per_bh) >> 4;
+    const uint4 v = tok < T ? __ldg(lin + (bh * T + tok) * 16 + dg) : make_uint4(0u, 0u, 0u, 0u);
+    const int key = (int)(tok & 63);
+    const int64_t tile = tok >> 6;
+    const int o = mn_major ? dg * 64 + (key >> 3) * 8 + (key & 7) : (key >> 3) * 128 + dg * 8 + (key & 7);
+    tiles[(bh * ntk + tile) * 1024 + o] = v;
+  }
+}
+
 // Decode-once + tcgen05 flash attention for prefill shapes.  Workspace: the
 // two decoded fp16 tensors (kv layout) + an error word.
+static int prefill_variant() {
+  static const int v = [] {
+    const char* e = getenv("HQMQ_FA_VARIANT");  // 1: the 4-warp kernel (A/B)
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+
 size_t prefill_tc_workspace(const hqmq_attention_args* a) {
-  return 2 * (size_t)a->batch * a->kv_heads * a->kv_tokens * kFaD * 2 + 256;
+  const size_t bh = (size_t)a->batch * a->kv_heads;
+  const size_t lin = 2 * bh * a->kv_tokens * kFaD * 2;
+  const size_t tiles = 2 * bh * (size_t)ceil_div(a->kv_tokens, kF2Keys) * kF2TileBytes;
+  return lin + tiles + 256;
 }
 
 bool prefill_tc_applicable(const hqmq_attention_args* a) {
@@ -354,6 +647,32 @@ int launch_prefill_tc(const hqmq_attention_args* a, cudaStream_t st) {
     d.error_word = err;
     const int rc = hqmq_decode(&d, st);
     if (rc != HQMQ_OK) return rc;
+  }
+  if (prefill_variant() == 0) {
+    const int64_t bh = a->batch * a->kv_heads;
+    const int64_t ntk = ceil_div(a->kv_tokens, kF2Keys);
+    unsigned char* kt = ws + 2 * nelem * 2;
+    unsigned char* vt = kt + (size_t)bh * ntk * kF2TileBytes;
+    err = reinterpret_cast<uint32_t*>(vt + (size_t)bh * ntk * kF2TileBytes);
+    const int64_t units = bh * ntk * kF2Keys * 16;
+    const unsigned grid_t = (unsigned)std::min<int64_t>(ceil_div(units, 256), 148 * 16);
+    fa_tile_kernel<<<grid_t, 256, 0, st>>>(reinterpret_cast<const uint4*>(kd), reinterpret_cast<uint4*>(kt),
+                                           bh, a->kv_tokens, ntk, 0);
+    fa_tile_kernel<<<grid_t, 256, 0, st>>>(reinterpret_cast<const uint4*>(vd), reinterpret_cast<uint4*>(vt),
+                                           bh, a->kv_tokens, ntk, 1);
+    int rc = check_launch();
+    if (rc != HQMQ_OK) return rc;
+    Fa2Params q2;
+    q2.B = a->batch; q2.Hq = a->q_heads; q2.Hkv = a->kv_heads; q2.Tq = a->q_tokens;
+    q2.Tkv = a->kv_tokens; q2.ntk = ntk;
+    q2.g = (int)(a->q_heads / a->kv_heads); q2.causal = a->causal;
+    q2.scale_log2 = (float)(a->scale * 1.4426950408889634);
+    q2.q = a->q; q2.kt = kt; q2.vt = vt; q2.out = a->out;
+    cudaFuncSetAttribute(attention_fa2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF2Smem);
+    const int64_t tpt = 2 * kFaRows / q2.g;
+    const dim3 grid((unsigned)ceil_div(a->q_tokens, tpt), (unsigned)bh);
+    attention_fa2_kernel<<<grid, kF2Threads, kF2Smem, st>>>(q2);
+    return check_launch();
   }
   FaParams p;
   p.B = a->batch; p.Hq = a->q_heads; p.Hkv = a->kv_heads; p.Tq = a->q_tokens; p.Tkv = a->kv_tokens;
