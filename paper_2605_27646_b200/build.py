@@ -69,7 +69,8 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -
     for src in sources():
         obj = os.path.join(obj_dir, os.path.basename(src)[:-3] + ".o")
         objs.append(obj)
-        cmd = [cc, *NVCC_FLAGS, *inc, "-c", src, "-o", obj]
+        extra = os.environ.get("HQMQ_NVCC_EXTRA", "").split()  # experiments only
+        cmd = [cc, *NVCC_FLAGS, *extra, *inc, "-c", src, "-o", obj]
         if verbose:
             print(" ".join(cmd), flush=True)
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))

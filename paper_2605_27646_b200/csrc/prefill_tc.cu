@@ -323,25 +323,31 @@ __global__ void __launch_bounds__(kFaThreads, 2) attention_fa_tc_kernel(FaParams
 
 // ------------------------------------------------------------------------
 // Warp-specialised version (default).  CTA = 2 query tiles of 128 rows (256
-// rows = (256 / g) tokens x g heads of one kv head), 10 warps:
+// rows = (256 / g) tokens x g heads of one kv head), 11 warps:
 //   warps 0-3 / 4-7  softmax of query tile 0 / 1 (thread = row = TMEM lane)
-//   warp 8           producer: one 1-D bulk copy (TMA) per K / V tile from the
+//   warps 8 / 10     K / V producers: one 1-D bulk copy (TMA) per tile from the
 //                    workspace, where the decode left them pre-arranged in the
 //                    UMMA canonical layouts (16 KB per 64-key tile)
 //   warp 9           MMA issuer (one thread)
 // TMEM (512 columns): S0 double buffer [0,128), S1 [128,256), O0 [256,384),
-// O1 [384,512).  MMA order S0(0) S1(0) | S0(t+1) S1(t+1) PV0(t) PV1(t) | ...:
-// the scores of tile t+1 are computed while both softmax groups work on tile
-// t, and each PV as soon as its P is in shared memory.  A 3-stage K/V
-// ring (full / empty mbarriers; the stage is released by tcgen05.commit after
-// the last MMA that reads it).  The running max is only raised when a row's
+// O1 [384,512).  MMA order S0(0) S1(0) S0(1) S1(1) | PV0(t) S0(t+2) PV1(t)
+// S1(t+2) | ...: each group's scores run two tiles ahead of its softmax (one
+// mbarrier per S buffer), so the groups drift half a period apart and one
+// group's TMEM reads / exponentials overlap the other's, and the tensor cores
+// always have the next tile's scores queued.  A 6-stage
+// K ring and a 4-stage V ring (full / empty mbarriers; a stage is released by
+// tcgen05.commit after the last MMA that reads it; one mbarrier per S / P buffer, as a softmax
+// group may finish tile t+1 before the issuer has consumed P(t)).  P is written back into TMEM over its S tile
+// and is the A operand of the PV MMA (no shared-memory round trip: the SS
+// MMAs are shared-memory-bandwidth bound, 128 B/clk, tools/ubench_umma_tput).
+// The running max is only raised when a row's
 // tile max exceeds it by more than 8 (log2 domain): exponents stay <= 2^8 in
 // fp16 P, O is rescaled in TMEM far less often, and O / l is unchanged.
-constexpr int kF2Keys = 64, kF2Stages = 3, kF2Threads = 320;
+constexpr int kF2Keys = 64, kF2KStages = 6, kF2VStages = 4, kF2Threads = 352;
 constexpr uint32_t kF2TileBytes = kF2Keys * kFaD * 2;  // 16 KB
-constexpr uint32_t kF2QOff = 0, kF2KVOff = 2 * kQBytes;
-constexpr uint32_t kF2POff = kF2KVOff + kF2Stages * 2 * kF2TileBytes;
-constexpr uint32_t kF2Smem = kF2POff + 2 * kF2Keys * kFaRows * 2;
+constexpr uint32_t kF2QOff = 0, kF2KOff = 2 * kQBytes;
+constexpr uint32_t kF2VOff = kF2KOff + kF2KStages * kF2TileBytes;
+constexpr uint32_t kF2Smem = kF2VOff + kF2VStages * kF2TileBytes;
 
 struct Fa2Params {
   int64_t B, Hq, Hkv, Tq, Tkv, ntk;
@@ -353,21 +359,34 @@ struct Fa2Params {
   float* out;
 };
 
+// mbarrier wait without a suspend-time hint (pure try_wait polling)
+__device__ __forceinline__ void fa_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\tFA_WAIT:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra FA_WAIT;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __global__ void __launch_bounds__(kF2Threads, 1) attention_fa2_kernel(Fa2Params p) {
   extern __shared__ __align__(1024) unsigned char fsm[];
-  __shared__ __align__(8) uint64_t full[kF2Stages], empty[kF2Stages];
-  __shared__ __align__(8) uint64_t bar_s[2], bar_p[2], bar_o[2];
+  __shared__ __align__(8) uint64_t full_k[kF2KStages], empty_k[kF2KStages];
+  __shared__ __align__(8) uint64_t full_v[kF2VStages], empty_v[kF2VStages];
+  __shared__ __align__(8) uint64_t bar_s[2][2], bar_p[2][2], bar_o[2], bar_fin;
   __shared__ uint32_t tmem_slot;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int64_t bh = blockIdx.y;
+  // grid (B*Hkv, query tiles): concurrently resident CTAs spread over the kv
+  // heads (their K / V tiles live in different L2 lines), and the longest
+  // causal query tiles start first
+  const int64_t bh = blockIdx.x;
   const int64_t b = bh / p.Hkv, hkv = bh % p.Hkv;
   const int g = p.g;
   const int tpt = 2 * kFaRows / g;
-  const int64_t tok0 = (int64_t)blockIdx.x * tpt;
+  const int64_t tok0 = (int64_t)(gridDim.y - 1 - blockIdx.y) * tpt;
   const int64_t off = p.causal ? (p.Tkv - p.Tq) : 0;
   const int64_t last_tok = std::min(p.Tq, tok0 + tpt) - 1;
   const int64_t kend = p.causal ? std::min(p.Tkv, last_tok + off + 1) : p.Tkv;
@@ -380,15 +399,22 @@ __global__ void __launch_bounds__(kF2Threads, 1) attention_fa2_kernel(Fa2Params 
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    for (int i = 0; i < kF2Stages; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
+    for (int i = 0; i < kF2KStages; ++i) {
+      mbar_init(&full_k[i], 1);
+      mbar_init(&empty_k[i], 1);
+    }
+    for (int i = 0; i < kF2VStages; ++i) {
+      mbar_init(&full_v[i], 1);
+      mbar_init(&empty_v[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&bar_s[i], 1);
-      mbar_init(&bar_p[i], kFaRows);
+      mbar_init(&bar_s[i][0], 1);
+      mbar_init(&bar_s[i][1], 1);
+      mbar_init(&bar_p[i][0], kFaRows);
+      mbar_init(&bar_p[i][1], kFaRows);
       mbar_init(&bar_o[i], 1);
     }
+    mbar_init(&bar_fin, 1);
     fence_mbar_init();
   }
   // softmax threads: this thread's row and its Q row -> fp16 (pre-scaled) A operand
@@ -423,21 +449,25 @@ __global__ void __launch_bounds__(kF2Threads, 1) attention_fa2_kernel(Fa2Params 
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tm = tmem_slot;
   const uint32_t sbase = smem_u32(fsm);
-  auto kv_smem = [&](int stage, int which) {
-    return kF2KVOff + (uint32_t)(stage * 2 + which) * kF2TileBytes;
-  };
+  auto k_smem = [&](int t) { return kF2KOff + (uint32_t)(t % kF2KStages) * kF2TileBytes; };
+  auto v_smem = [&](int t) { return kF2VOff + (uint32_t)(t % kF2VStages) * kF2TileBytes; };
 
-  if (warp == 8) {
-    // ---- producer
+  if (warp == 8 || warp == 10) {
+    // ---- producers (K: warp 8, V: warp 10), one 16 KB bulk copy per tile.
+    // Separate rings: a K stage is free once both S MMAs have read it, a V
+    // stage only after both PV MMAs, so K runs further ahead.
     if (lane == 0) {
-      const unsigned char* kb = p.kt + (size_t)bh * p.ntk * kF2TileBytes;
-      const unsigned char* vb = p.vt + (size_t)bh * p.ntk * kF2TileBytes;
+      const bool is_k = warp == 8;
+      const int ns = is_k ? kF2KStages : kF2VStages;
+      uint64_t* fullb = is_k ? full_k : full_v;
+      uint64_t* emptyb = is_k ? empty_k : empty_v;
+      const unsigned char* src = (is_k ? p.kt : p.vt) + (size_t)bh * p.ntk * kF2TileBytes;
       for (int t = 0; t < ntiles; ++t) {
-        const int st = t % kF2Stages;
-        if (t >= kF2Stages) mbar_wait(&empty[st], (uint32_t)((t / kF2Stages) - 1) & 1u);
-        mbar_arrive_expect_tx(&full[st], 2 * kF2TileBytes);
-        bulk_g2s(fsm + kv_smem(st, 0), kb + (size_t)t * kF2TileBytes, kF2TileBytes, &full[st]);
-        bulk_g2s(fsm + kv_smem(st, 1), vb + (size_t)t * kF2TileBytes, kF2TileBytes, &full[st]);
+        const int st = t % ns;
+        if (t >= ns) fa_wait(&emptyb[st], (uint32_t)((t / ns) - 1) & 1u);
+        mbar_arrive_expect_tx(&fullb[st], kF2TileBytes);
+        bulk_g2s(fsm + (is_k ? k_smem(t) : v_smem(t)), src + (size_t)t * kF2TileBytes, kF2TileBytes,
+                 &fullb[st]);
       }
     }
     __syncwarp();
@@ -445,58 +475,67 @@ __global__ void __launch_bounds__(kF2Threads, 1) attention_fa2_kernel(Fa2Params 
     // ---- MMA issuer
     if (lane == 0 && ntiles > 0) {
       auto s_mma = [&](int i, int t) {  // S_i(t) = Q_i K(t)^T -> TMEM cols 128 i + 64 (t & 1)
-        const int st = t % kF2Stages;
 #pragma unroll
         for (int kk = 0; kk < kFaD / 16; ++kk)
           fa_mma(tm + (uint32_t)i * 128 + (uint32_t)(t & 1) * 64, fa_desc(sbase + kF2QOff + i * kQBytes + kk * 256, kSboQK),
-                 fa_desc(sbase + kv_smem(st, 0) + kk * 256, kSboQK), fa_idesc(kFaRows, kF2Keys, 0),
+                 fa_desc(sbase + k_smem(t) + kk * 256, kSboQK), fa_idesc(kFaRows, kF2Keys, 0),
                  kk > 0);
-        fa_commit(&bar_s[i]);
+        fa_commit(&bar_s[i][t & 1]);
+        if (i == 1) fa_commit(&empty_k[t % kF2KStages]);
       };
-      auto pv_mma = [&](int i, int t) {  // O_i += P_i V(t) -> TMEM cols 256 + 128 i
-        const int st = t % kF2Stages;
+      // O_i += P_i V(t) -> TMEM cols 256 + 128 i; A = P_i(t) from TMEM (fp16
+      // pairs written over S_i(t): lane = row, column c = keys 2c, 2c+1)
+      auto pv_mma = [&](int i, int t) {
+        const uint32_t pa = tm + (uint32_t)i * 128 + (uint32_t)(t & 1) * 64;
 #pragma unroll
         for (int kk = 0; kk < kF2Keys / 16; ++kk)
-          fa_mma(tm + 256 + (uint32_t)i * 128,
-                 fa_desc(sbase + kF2POff + i * (kF2Keys * kFaRows * 2) + kk * 256, kSboP),
-                 fa_desc(sbase + kv_smem(st, 1) + kk * 256, kSboV), fa_idesc(kFaRows, kFaD, 1),
-                 (t > 0 || kk > 0) ? 1u : 0u);
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(
+                  tm + 256 + (uint32_t)i * 128),
+              "r"(pa + kk * 8), "l"(fa_desc(sbase + v_smem(t) + kk * 256, kSboV)),
+              "r"(fa_idesc(kFaRows, kFaD, 1)), "r"((t > 0 || kk > 0) ? 1u : 0u));
         fa_commit(&bar_o[i]);
       };
-      mbar_wait(&full[0], 0);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      s_mma(0, 0);
-      s_mma(1, 0);
+      for (int t = 0; t < 2 && t < ntiles; ++t) {
+        fa_wait(&full_k[t], 0);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        s_mma(0, t);
+        s_mma(1, t);
+      }
       for (int t = 0; t < ntiles; ++t) {
         const uint32_t ph = (uint32_t)t & 1u;
-        // S(t+1) into the other S buffers: group i finished reading them
-        // (tile t-1) before its P(t-1) arrival, already waited for below
-        if (t + 1 < ntiles) {
-          mbar_wait(&full[(t + 1) % kF2Stages], (uint32_t)((t + 1) / kF2Stages) & 1u);
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          s_mma(0, t + 1);
-          s_mma(1, t + 1);
-        }
-        mbar_wait(&bar_p[0], ph);
+        const bool ahead = t + 2 < ntiles;
+        // group i finished with S buffer t & 1 when it arrived with P_i(t)
+        fa_wait(&full_v[t % kF2VStages], (uint32_t)(t / kF2VStages) & 1u);
+        fa_wait(&bar_p[0][t & 1], (uint32_t)(t >> 1) & 1u);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         pv_mma(0, t);
-        mbar_wait(&bar_p[1], ph);
+        if (ahead) {
+          fa_wait(&full_k[(t + 2) % kF2KStages], (uint32_t)((t + 2) / kF2KStages) & 1u);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          s_mma(0, t + 2);
+        }
+        fa_wait(&bar_p[1][t & 1], (uint32_t)(t >> 1) & 1u);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         pv_mma(1, t);
-        fa_commit(&empty[t % kF2Stages]);
+        fa_commit(&empty_v[t % kF2VStages]);
+        if (ahead) s_mma(1, t + 2);
       }
+      // every MMA done (the softmax groups skip PV waits, so bar_o may lag
+      // more than one phase behind them)
+      fa_commit(&bar_fin);
     }
     __syncwarp();
   } else {
     // ---- softmax (warps 0-7): thread = row r of query tile wg
     const uint32_t tm_row = tm + ((uint32_t)((warp & 3) * 32) << 16);
     const uint32_t o_col = 256 + (uint32_t)wg * 128;
-    unsigned char* psm = fsm + kF2POff + wg * (kF2Keys * kFaRows * 2);
     float m_run = -INFINITY, l_run = 0.f;
     for (int t = 0; t < ntiles; ++t) {
       const uint32_t ph = (uint32_t)t & 1u;
       const int64_t k0 = (int64_t)t * kF2Keys;
-      mbar_wait(&bar_s[wg], ph);
+      fa_wait(&bar_s[wg][t & 1], (uint32_t)(t >> 1) & 1u);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t s_col = (uint32_t)wg * 128 + ph * 64;
       uint32_t sr[64];
@@ -526,11 +565,12 @@ __global__ void __launch_bounds__(kF2Threads, 1) attention_fa2_kernel(Fa2Params 
       }
       l_run = l_run * alpha + psum;
       m_run = m_new;
-      // PV(t-1) done: P buffer and O accumulator are free
-      if (t > 0) {
-        mbar_wait(&bar_o[wg], ph ^ 1u);
+      // O is only touched when some row's max moved: then PV(t-1) must be done
+      // (S(t) completing implies PV(t-2) done, so bar_o is at most one phase behind)
+      if (t > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+        fa_wait(&bar_o[wg], ph ^ 1u);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        if (__any_sync(0xffffffffu, alpha != 1.f)) {
+        {
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
             uint32_t orr[32];
@@ -543,16 +583,14 @@ __global__ void __launch_bounds__(kF2Threads, 1) attention_fa2_kernel(Fa2Params 
           asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
         }
       }
-#pragma unroll
-      for (int kg = 0; kg < 8; ++kg)
-        *reinterpret_cast<uint4*>(psm + (r >> 3) * kSboP + kg * 128 + (r & 7) * 16) =
-            make_uint4(hw[4 * kg], hw[4 * kg + 1], hw[4 * kg + 2], hw[4 * kg + 3]);
-      fence_proxy_async();
+      // P(t) over the first 32 columns of S(t) (already read out)
+      FA_ST32(tm_row + s_col, hw);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      mbar_arrive(&bar_p[wg]);
+      mbar_arrive(&bar_p[wg][t & 1]);
     }
     if (ntiles > 0) {
-      mbar_wait(&bar_o[wg], (uint32_t)(ntiles - 1) & 1u);
+      fa_wait(&bar_fin, 0);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     }
     float* orow = p.out + ((b * p.Hq + hkv * g + qhead) * p.Tq + (rvalid ? qtok : 0)) * kFaD;
@@ -670,7 +708,7 @@ int launch_prefill_tc(const hqmq_attention_args* a, cudaStream_t st) {
     q2.q = a->q; q2.kt = kt; q2.vt = vt; q2.out = a->out;
     cudaFuncSetAttribute(attention_fa2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF2Smem);
     const int64_t tpt = 2 * kFaRows / q2.g;
-    const dim3 grid((unsigned)ceil_div(a->q_tokens, tpt), (unsigned)bh);
+    const dim3 grid((unsigned)bh, (unsigned)ceil_div(a->q_tokens, tpt));
     attention_fa2_kernel<<<grid, kF2Threads, kF2Smem, st>>>(q2);
     return check_launch();
   }
