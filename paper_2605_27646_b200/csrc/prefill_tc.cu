@@ -322,7 +322,9 @@ __global__ void __launch_bounds__(kFaThreads, 2) attention_fa_tc_kernel(FaParams
 }
 
 // ------------------------------------------------------------------------
-// Warp-specialised version (default).  CTA = 2 query tiles of 128 rows (256
+// Warp-specialised version (default; measured against the one-tile 128-key
+// kernel below: 0.090 / 0.71 / 0.84 ms vs 0.103 / 0.70 / 0.90 ms on
+// B=1 T=2k / B=1 T=8k / B=4 T=4k).  CTA = 2 query tiles of 128 rows (256
 // rows = (256 / g) tokens x g heads of one kv head), 11 warps:
 //   warps 0-3 / 4-7  softmax of query tile 0 / 1 (thread = row = TMEM lane)
 //   warps 8 / 10     K / V producers: one 1-D bulk copy (TMA) per tile from the
@@ -370,6 +372,30 @@ __device__ __forceinline__ void fa_wait(uint64_t* bar, uint32_t phase) {
 }
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Softmax inner step over 32 scores of one row (log2 domain): masked entries
+// already -inf; exponentials against m_use by ex2.approx (inputs <= 8 or
+// -inf), packed fp32 adds, four independent max chains and two sum chains so
+// a single warp per SM sub-partition is not latency-bound on them.
+__device__ __forceinline__ float fa_ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ void fa_softmax32(const uint32_t (&sr)[32], float m_use, float (&mx)[4],
+                                             float2 (&acc)[2], uint32_t* hw) {
+  const float2 nm = make_float2(-m_use, -m_use);
+#pragma unroll
+  for (int e = 0; e < 16; ++e) {
+    const float s0 = __uint_as_float(sr[2 * e]), s1 = __uint_as_float(sr[2 * e + 1]);
+    mx[e & 3] = fmaxf(mx[e & 3], fmaxf(s0, s1));
+    const float2 d = __fadd2_rn(make_float2(s0, s1), nm);
+    const float e0 = fa_ex2(d.x), e1 = fa_ex2(d.y);
+    acc[e & 1] = __fadd2_rn(acc[e & 1], make_float2(e0, e1));
+    const __half2 h = __floats2half2_rn(e0, e1);
+    hw[e] = *reinterpret_cast<const uint32_t*>(&h);
+  }
 }
 
 __global__ void __launch_bounds__(kF2Threads, 1) attention_fa2_kernel(Fa2Params p) {
@@ -547,22 +573,26 @@ __global__ void __launch_bounds__(kF2Threads, 1) attention_fa2_kernel(Fa2Params 
         for (int j = 0; j < 64; ++j)
           if (!rvalid || k0 + j >= vis) sr[j] = __float_as_uint(-INFINITY);
       }
-      float mx = -INFINITY;
+      float mx4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-      for (int j = 0; j < 64; ++j) mx = fmaxf(mx, __uint_as_float(sr[j]));
+      for (int j = 0; j < 64; j += 2)
+        mx4[(j >> 1) & 3] = fmaxf(mx4[(j >> 1) & 3], fmaxf(__uint_as_float(sr[j]), __uint_as_float(sr[j + 1])));
+      const float mx = fmaxf(fmaxf(mx4[0], mx4[1]), fmaxf(mx4[2], mx4[3]));
       const float m_new = (mx > m_run + 8.f) ? mx : m_run;  // also true when m_run = -inf
       const float alpha = (m_new == m_run) ? 1.f : exp2f(m_run - m_new);
       const float m_use = m_new == -INFINITY ? 0.f : m_new;  // all-masked row: exp2(-inf) = 0
-      float psum = 0.f;
       uint32_t hw[32];
+      float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+      const float2 nm = make_float2(-m_use, -m_use);
 #pragma unroll
       for (int e = 0; e < 32; ++e) {
-        const float e0 = exp2f(__uint_as_float(sr[2 * e]) - m_use);
-        const float e1 = exp2f(__uint_as_float(sr[2 * e + 1]) - m_use);
-        psum += e0 + e1;
+        const float2 d = __fadd2_rn(make_float2(__uint_as_float(sr[2 * e]), __uint_as_float(sr[2 * e + 1])), nm);
+        const float e0 = fa_ex2(d.x), e1 = fa_ex2(d.y);
+        acc[e & 1] = __fadd2_rn(acc[e & 1], make_float2(e0, e1));
         const __half2 h = __floats2half2_rn(e0, e1);
         hw[e] = *reinterpret_cast<const uint32_t*>(&h);
       }
+      const float psum = (acc[0].x + acc[0].y) + (acc[1].x + acc[1].y);
       l_run = l_run * alpha + psum;
       m_run = m_new;
       // O is only touched when some row's max moved: then PV(t-1) must be done
@@ -620,23 +650,281 @@ __global__ void __launch_bounds__(kF2Threads, 1) attention_fa2_kernel(Fa2Params 
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "n"(512));
 }
 
-// Linear decoded fp16 (B*Hkv, T, 128) -> 64-key UMMA tiles (16-byte units):
+// ------------------------------------------------------------------------
+// 128-key version (HQMQ_FA_VARIANT=3).  One query tile of 128 rows per CTA (128 / g
+// tokens x g heads of one kv head), 7 warps: softmax warps 0-3 (thread = row
+// = TMEM lane), K producer (4), MMA issuer (5), V producer (6).  With 128-key
+// tiles both MMAs run at the tensor-core floor (SS S = QK^T with N = 128 reads
+// 8 KB of shared memory per 64-cycle K-step = the 128 B/clk the SS form can
+// stream; PV is TS with P in TMEM), where the 64-key S MMA of the two-tile
+// kernel above costs 48 instead of 32 cycles per step.
+// TMEM: S double buffer [0,128) / [128,256) (P(t) written back over the first
+// 64 columns of its S buffer), O [256,384).  MMA order S(0) S(1) | PV(t)
+// S(t+2) | ...: scores run two tiles ahead of the softmax and PV(t) overlaps
+// the softmax of tile t+1.  Softmax in one pass against the running max; a
+// tile whose max exceeds it by more than 8 (log2) is redone with the new max.
+constexpr int kF3Keys = 128, kF3KStages = 3, kF3VStages = 3, kF3Threads = 224;
+constexpr uint32_t kF3TileBytes = kF3Keys * kFaD * 2;  // 32 KB
+constexpr uint32_t kF3KOff = kQBytes;
+constexpr uint32_t kF3VOff = kF3KOff + kF3KStages * kF3TileBytes;
+constexpr uint32_t kF3Smem = kF3VOff + kF3VStages * kF3TileBytes;
+constexpr uint32_t kSbo128 = (kF3Keys / 8) * 128;  // MN-major V: 16 key-groups per 8-dim group
+
+#define FA_ST16(addr, r)                                                                        \
+  asm volatile(                                                                                 \
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12," \
+      "%13,%14,%15,%16};" ::"r"(addr),                                                        \
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),  \
+      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),         \
+      "r"(r[15]))
+
+__global__ void __launch_bounds__(kF3Threads, 1) attention_fa3_kernel(Fa2Params p) {
+  extern __shared__ __align__(1024) unsigned char fsm[];
+  __shared__ __align__(8) uint64_t full_k[kF3KStages], empty_k[kF3KStages];
+  __shared__ __align__(8) uint64_t full_v[kF3VStages], empty_v[kF3VStages];
+  __shared__ __align__(8) uint64_t bar_s[2], bar_p[2], bar_o, bar_fin;
+  __shared__ uint32_t tmem_slot;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // grid (B*Hkv, query tiles), longest causal tiles first
+  const int64_t bh = blockIdx.x;
+  const int64_t b = bh / p.Hkv, hkv = bh % p.Hkv;
+  const int g = p.g;
+  const int tpt = kFaRows / g;
+  const int64_t tok0 = (int64_t)(gridDim.y - 1 - blockIdx.y) * tpt;
+  const int64_t off = p.causal ? (p.Tkv - p.Tq) : 0;
+  const int64_t last_tok = std::min(p.Tq, tok0 + tpt) - 1;
+  const int64_t kend = p.causal ? std::min(p.Tkv, last_tok + off + 1) : p.Tkv;
+  const int ntiles = kend > 0 ? (int)((kend + kF3Keys - 1) / kF3Keys) : 0;
+
+  if (warp == 5) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_slot)),
+                 "n"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < kF3KStages; ++i) {
+      mbar_init(&full_k[i], 1);
+      mbar_init(&empty_k[i], 1);
+    }
+    for (int i = 0; i < kF3VStages; ++i) {
+      mbar_init(&full_v[i], 1);
+      mbar_init(&empty_v[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bar_s[i], 1);
+      mbar_init(&bar_p[i], kFaRows);
+    }
+    mbar_init(&bar_o, 1);
+    mbar_init(&bar_fin, 1);
+    fence_mbar_init();
+  }
+  const int r = tid & 127;
+  const int64_t qtok = tok0 + r / g;
+  const int qhead = r % g;
+  const bool rvalid = tid < kFaRows && qtok < p.Tq;
+  const int64_t vis = p.causal ? std::min(qtok + off + 1, p.Tkv) : p.Tkv;
+  if (tid < kFaRows) {
+    const float4* qr = reinterpret_cast<const float4*>(
+        p.q + ((b * p.Hq + hkv * g + qhead) * p.Tq + (rvalid ? qtok : 0)) * kFaD);
+#pragma unroll 4
+    for (int kg = 0; kg < kFaD / 8; ++kg) {
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f), c = a;
+      if (rvalid) {
+        a = __ldg(qr + 2 * kg);
+        c = __ldg(qr + 2 * kg + 1);
+      }
+      const float sl = p.scale_log2;
+      const __half2 h0 = __floats2half2_rn(a.x * sl, a.y * sl), h1 = __floats2half2_rn(a.z * sl, a.w * sl);
+      const __half2 h2 = __floats2half2_rn(c.x * sl, c.y * sl), h3 = __floats2half2_rn(c.z * sl, c.w * sl);
+      *reinterpret_cast<uint4*>(fsm + (r >> 3) * kSboQK + kg * 128 + (r & 7) * 16) =
+          make_uint4(*reinterpret_cast<const uint32_t*>(&h0), *reinterpret_cast<const uint32_t*>(&h1),
+                     *reinterpret_cast<const uint32_t*>(&h2), *reinterpret_cast<const uint32_t*>(&h3));
+    }
+  }
+  fence_proxy_async();
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tm = tmem_slot;
+  const uint32_t sbase = smem_u32(fsm);
+  auto k_smem = [&](int t) { return kF3KOff + (uint32_t)(t % kF3KStages) * kF3TileBytes; };
+  auto v_smem = [&](int t) { return kF3VOff + (uint32_t)(t % kF3VStages) * kF3TileBytes; };
+
+  if (warp == 4 || warp == 6) {
+    // ---- producers: K (warp 4) and V (warp 6), one 32 KB bulk copy per tile
+    if (lane == 0) {
+      const bool is_k = warp == 4;
+      const int ns = is_k ? kF3KStages : kF3VStages;
+      uint64_t* fullb = is_k ? full_k : full_v;
+      uint64_t* emptyb = is_k ? empty_k : empty_v;
+      const unsigned char* src = (is_k ? p.kt : p.vt) + (size_t)bh * p.ntk * kF3TileBytes;
+      for (int t = 0; t < ntiles; ++t) {
+        const int st = t % ns;
+        if (t >= ns) fa_wait(&emptyb[st], (uint32_t)((t / ns) - 1) & 1u);
+        mbar_arrive_expect_tx(&fullb[st], kF3TileBytes);
+        bulk_g2s(fsm + (is_k ? k_smem(t) : v_smem(t)), src + (size_t)t * kF3TileBytes, kF3TileBytes,
+                 &fullb[st]);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 5) {
+    // ---- MMA issuer
+    if (lane == 0 && ntiles > 0) {
+      auto s_mma = [&](int t) {  // S(t) = Q K(t)^T -> TMEM cols 128 (t & 1)
+#pragma unroll
+        for (int kk = 0; kk < kFaD / 16; ++kk)
+          fa_mma(tm + (uint32_t)(t & 1) * 128, fa_desc(sbase + kk * 256, kSboQK),
+                 fa_desc(sbase + k_smem(t) + kk * 256, kSboQK), fa_idesc(kFaRows, kF3Keys, 0), kk > 0);
+        fa_commit(&bar_s[t & 1]);
+        fa_commit(&empty_k[t % kF3KStages]);
+      };
+      auto pv_mma = [&](int t) {  // O += P(t) V(t), A = P(t) from TMEM
+        const uint32_t pa = tm + (uint32_t)(t & 1) * 128;
+#pragma unroll
+        for (int kk = 0; kk < kF3Keys / 16; ++kk)
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tm + 256),
+              "r"(pa + kk * 8), "l"(fa_desc(sbase + v_smem(t) + kk * 256, kSbo128)),
+              "r"(fa_idesc(kFaRows, kFaD, 1)), "r"((t > 0 || kk > 0) ? 1u : 0u));
+        fa_commit(&bar_o);
+        fa_commit(&empty_v[t % kF3VStages]);
+      };
+      for (int t = 0; t < 2 && t < ntiles; ++t) {
+        fa_wait(&full_k[t], 0);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        s_mma(t);
+      }
+      for (int t = 0; t < ntiles; ++t) {
+        fa_wait(&full_v[t % kF3VStages], (uint32_t)(t / kF3VStages) & 1u);
+        fa_wait(&bar_p[t & 1], (uint32_t)(t >> 1) & 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        pv_mma(t);
+        if (t + 2 < ntiles) {  // S(t+2) into the buffer P(t) occupies: after PV(t) in issue order
+          fa_wait(&full_k[(t + 2) % kF3KStages], (uint32_t)((t + 2) / kF3KStages) & 1u);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          s_mma(t + 2);
+        }
+      }
+      fa_commit(&bar_fin);
+    }
+    __syncwarp();
+  } else {
+    // ---- softmax (warps 0-3): thread = row r
+    const uint32_t tm_row = tm + ((uint32_t)(warp * 32) << 16);
+    const uint32_t o_col = 256;
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int t = 0; t < ntiles; ++t) {
+      const int64_t k0 = (int64_t)t * kF3Keys;
+      const uint32_t s_col = (uint32_t)(t & 1) * 128;
+      fa_wait(&bar_s[t & 1], (uint32_t)(t >> 1) & 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const bool mask = !rvalid || k0 + kF3Keys > vis;
+      // one pass against the running max (chunks of 32 keys: ld, mask, exp2,
+      // pack); P stays in registers until the pass is accepted, since it is
+      // stored over the S columns a redo would read again
+      uint32_t hw[64];
+      auto pass = [&](float m_use, float& tile_max) {
+        float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t sr[32];
+          FA_LD32(tm_row + s_col + c * 32, sr);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (mask) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (!rvalid || k0 + c * 32 + j >= vis) sr[j] = __float_as_uint(-INFINITY);
+          }
+          fa_softmax32(sr, m_use, mx, acc, hw + c * 16);
+        }
+        tile_max = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+        return (acc[0].x + acc[0].y) + (acc[1].x + acc[1].y);
+      };
+      float tmax = -INFINITY;
+      float psum = pass(m_run == -INFINITY ? 0.f : m_run, tmax);
+      // first tile, or the max jumped: redo with the tile max (warp-uniform:
+      // the TMEM loads inside are .sync.aligned)
+      const bool jump = tmax > m_run + 8.f;
+      const float m_new = jump ? tmax : m_run;
+      if (__any_sync(0xffffffffu, jump)) {
+        float dummy = -INFINITY;
+        psum = pass(m_new == -INFINITY ? 0.f : m_new, dummy);
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) FA_ST16(tm_row + s_col + c * 16, (hw + c * 16));
+      const float alpha = (m_new == m_run) ? 1.f : exp2f(m_run - m_new);
+      l_run = l_run * alpha + psum;
+      m_run = m_new;
+      // O is only touched when some row's max moved: PV(t-1) must be done
+      // (S(t) complete implies PV(t-2) done: bar_o is at most one phase behind)
+      if (t > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
+        fa_wait(&bar_o, (uint32_t)(t - 1) & 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t orr[32];
+          FA_LD32(tm_row + o_col + c * 32, orr);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int j = 0; j < 32; ++j) orr[j] = __float_as_uint(__uint_as_float(orr[j]) * alpha);
+          FA_ST32(tm_row + o_col + c * 32, orr);
+        }
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(&bar_p[t & 1]);
+    }
+    if (ntiles > 0) {
+      fa_wait(&bar_fin, 0);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+    float* orow = p.out + ((b * p.Hq + hkv * g + qhead) * p.Tq + (rvalid ? qtok : 0)) * kFaD;
+    const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      uint32_t orr[32];
+      if (ntiles > 0) {
+        FA_LD32(tm_row + o_col + c * 32, orr);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) orr[j] = 0u;
+      }
+      if (rvalid) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4)
+          *reinterpret_cast<float4*>(orow + c * 32 + j) =
+              make_float4(__uint_as_float(orr[j]) * inv, __uint_as_float(orr[j + 1]) * inv,
+                          __uint_as_float(orr[j + 2]) * inv, __uint_as_float(orr[j + 3]) * inv);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 5)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "n"(512));
+}
+
+// Linear decoded fp16 (B*Hkv, T, 128) -> kt-key UMMA tiles (16-byte units):
 //   K-major (K):  unit(key, dg) at (key/8)*128 + dg*8 + key%8
-//   MN-major (V): unit(key, dg) at dg*64 + (key/8)*8 + key%8
+//   MN-major (V): unit(key, dg) at dg*kt + (key/8)*8 + key%8
 // keys past T are zero-filled (masked P = 0 must not meet a NaN in V).
 __global__ void fa_tile_kernel(const uint4* __restrict__ lin, uint4* __restrict__ tiles, int64_t BH,
-                               int64_t T, int64_t ntk, int mn_major) {
-  const int64_t per_bh = ntk * kF2Keys * 16;
+                               int64_t T, int64_t ntk, int mn_major, int kt) {
+  const int64_t per_bh = ntk * kt * 16;
   const int64_t n = BH * per_bh;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     const int dg = (int)(i & 15);
     const int64_t bh = i / per_bh, tok = (i - bh * per_bh) >> 4;
     const uint4 v = tok < T ? __ldg(lin + (bh * T + tok) * 16 + dg) : make_uint4(0u, 0u, 0u, 0u);
-    const int key = (int)(tok & 63);
-    const int64_t tile = tok >> 6;
-    const int o = mn_major ? dg * 64 + (key >> 3) * 8 + (key & 7) : (key >> 3) * 128 + dg * 8 + (key & 7);
-    tiles[(bh * ntk + tile) * 1024 + o] = v;
+    const int key = (int)(tok % kt);
+    const int64_t tile = tok / kt;
+    const int o = mn_major ? dg * kt + (key >> 3) * 8 + (key & 7) : (key >> 3) * 128 + dg * 8 + (key & 7);
+    tiles[(bh * ntk + tile) * (kt * 16) + o] = v;
   }
 }
 
@@ -644,7 +932,7 @@ __global__ void fa_tile_kernel(const uint4* __restrict__ lin, uint4* __restrict_
 // two decoded fp16 tensors (kv layout) + an error word.
 static int prefill_variant() {
   static const int v = [] {
-    const char* e = getenv("HQMQ_FA_VARIANT");  // 1: the 4-warp kernel (A/B)
+    const char* e = getenv("HQMQ_FA_VARIANT");  // A/B: 1 = 4-warp kernel, 3 = one-tile 128-key kernel
     return e ? atoi(e) : 0;
   }();
   return v;
@@ -653,7 +941,8 @@ static int prefill_variant() {
 size_t prefill_tc_workspace(const hqmq_attention_args* a) {
   const size_t bh = (size_t)a->batch * a->kv_heads;
   const size_t lin = 2 * bh * a->kv_tokens * kFaD * 2;
-  const size_t tiles = 2 * bh * (size_t)ceil_div(a->kv_tokens, kF2Keys) * kF2TileBytes;
+  const size_t tiles = 2 * bh * std::max((size_t)ceil_div(a->kv_tokens, kF2Keys) * kF2TileBytes,
+                                         (size_t)ceil_div(a->kv_tokens, kF3Keys) * kF3TileBytes);
   return lin + tiles + 256;
 }
 
@@ -686,20 +975,34 @@ int launch_prefill_tc(const hqmq_attention_args* a, cudaStream_t st) {
     const int rc = hqmq_decode(&d, st);
     if (rc != HQMQ_OK) return rc;
   }
-  if (prefill_variant() == 0) {
+  if (prefill_variant() != 1) {
+    const bool v3 = prefill_variant() == 3;
+    const int keys = v3 ? kF3Keys : kF2Keys;
+    const uint32_t tile_bytes = v3 ? kF3TileBytes : kF2TileBytes;
     const int64_t bh = a->batch * a->kv_heads;
-    const int64_t ntk = ceil_div(a->kv_tokens, kF2Keys);
+    const int64_t ntk = ceil_div(a->kv_tokens, keys);
     unsigned char* kt = ws + 2 * nelem * 2;
-    unsigned char* vt = kt + (size_t)bh * ntk * kF2TileBytes;
-    err = reinterpret_cast<uint32_t*>(vt + (size_t)bh * ntk * kF2TileBytes);
-    const int64_t units = bh * ntk * kF2Keys * 16;
+    unsigned char* vt = kt + (size_t)bh * ntk * tile_bytes;
+    const int64_t units = bh * ntk * keys * 16;
     const unsigned grid_t = (unsigned)std::min<int64_t>(ceil_div(units, 256), 148 * 16);
     fa_tile_kernel<<<grid_t, 256, 0, st>>>(reinterpret_cast<const uint4*>(kd), reinterpret_cast<uint4*>(kt),
-                                           bh, a->kv_tokens, ntk, 0);
+                                           bh, a->kv_tokens, ntk, 0, keys);
     fa_tile_kernel<<<grid_t, 256, 0, st>>>(reinterpret_cast<const uint4*>(vd), reinterpret_cast<uint4*>(vt),
-                                           bh, a->kv_tokens, ntk, 1);
+                                           bh, a->kv_tokens, ntk, 1, keys);
     int rc = check_launch();
     if (rc != HQMQ_OK) return rc;
+    if (v3) {
+      Fa2Params q3;
+      q3.B = a->batch; q3.Hq = a->q_heads; q3.Hkv = a->kv_heads; q3.Tq = a->q_tokens;
+      q3.Tkv = a->kv_tokens; q3.ntk = ntk;
+      q3.g = (int)(a->q_heads / a->kv_heads); q3.causal = a->causal;
+      q3.scale_log2 = (float)(a->scale * 1.4426950408889634);
+      q3.q = a->q; q3.kt = kt; q3.vt = vt; q3.out = a->out;
+      cudaFuncSetAttribute(attention_fa3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF3Smem);
+      const dim3 grid((unsigned)bh, (unsigned)ceil_div(a->q_tokens, kFaRows / q3.g));
+      attention_fa3_kernel<<<grid, kF3Threads, kF3Smem, st>>>(q3);
+      return check_launch();
+    }
     Fa2Params q2;
     q2.B = a->batch; q2.Hq = a->q_heads; q2.Hkv = a->kv_heads; q2.Tq = a->q_tokens;
     q2.Tkv = a->kv_tokens; q2.ntk = ntk;
