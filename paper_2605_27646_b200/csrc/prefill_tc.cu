@@ -322,9 +322,9 @@ __global__ void __launch_bounds__(kFaThreads, 2) attention_fa_tc_kernel(FaParams
 }
 
 // ------------------------------------------------------------------------
-// Warp-specialised version (default; measured against the one-tile 128-key
-// kernel below: 0.090 / 0.71 / 0.84 ms vs 0.103 / 0.70 / 0.90 ms on
-// B=1 T=2k / B=1 T=8k / B=4 T=4k).  CTA = 2 query tiles of 128 rows (256
+// Warp-specialised two-tile version (default below 4096 keys; measured against
+// the one-tile 128-key kernel below: 0.090 / 0.71 / 0.84 ms vs 0.099 / 0.66 /
+// 0.85 ms on B=1 T=2k / B=1 T=8k / B=4 T=4k).  CTA = 2 query tiles of 128 rows (256
 // rows = (256 / g) tokens x g heads of one kv head), 11 warps:
 //   warps 0-3 / 4-7  softmax of query tile 0 / 1 (thread = row = TMEM lane)
 //   warps 8 / 10     K / V producers: one 1-D bulk copy (TMA) per tile from the
@@ -651,19 +651,21 @@ __global__ void __launch_bounds__(kF2Threads, 1) attention_fa2_kernel(Fa2Params 
 }
 
 // ------------------------------------------------------------------------
-// 128-key version (HQMQ_FA_VARIANT=3).  One query tile of 128 rows per CTA (128 / g
-// tokens x g heads of one kv head), 7 warps: softmax warps 0-3 (thread = row
-// = TMEM lane), K producer (4), MMA issuer (5), V producer (6).  With 128-key
-// tiles both MMAs run at the tensor-core floor (SS S = QK^T with N = 128 reads
-// 8 KB of shared memory per 64-cycle K-step = the 128 B/clk the SS form can
-// stream; PV is TS with P in TMEM), where the 64-key S MMA of the two-tile
-// kernel above costs 48 instead of 32 cycles per step.
-// TMEM: S double buffer [0,128) / [128,256) (P(t) written back over the first
-// 64 columns of its S buffer), O [256,384).  MMA order S(0) S(1) | PV(t)
-// S(t+2) | ...: scores run two tiles ahead of the softmax and PV(t) overlaps
-// the softmax of tile t+1.  Softmax in one pass against the running max; a
-// tile whose max exceeds it by more than 8 (log2) is redone with the new max.
-constexpr int kF3Keys = 128, kF3KStages = 3, kF3VStages = 3, kF3Threads = 224;
+// 128-key version (default from 4096 keys; HQMQ_FA_VARIANT=3 forces it).  One query tile of 128 rows per CTA
+// (128 / g tokens x g heads of one kv head), 11 warps: softmax warps 0-7
+// (warps w and w+4 share TMEM lanes 32 (w % 4): warp w < 4 takes keys 0-63
+// of each row, warp w+4 keys 64-127), K producer (8), MMA issuer (9), V
+// producer (10).  With 128-key tiles both MMAs run at the tensor-core floor
+// (SS S = QK^T with N = 128 streams 8 KB of shared memory per 64-cycle K-step
+// = the 128 B/clk the SS form can read; PV is TS with P in TMEM), where the
+// 64-key S MMA of the two-tile kernel costs 48 instead of 32 cycles a step.
+// TMEM: three S buffers [0,128) / [128,256) / [256,384) (P(t) written back
+// over the first 64 columns of its S buffer), O [384,512).  MMA order S(0)
+// S(1) S(2) | PV(t) S(t+3) | ...: two score tiles stay queued on the tensor
+// cores while a P(t) round trip (commit -> softmax -> arrive) is in flight.  Softmax in one pass against the running max; the two halves
+// of a row exchange tile maxima through shared memory (named barrier per
+// warp pair) and redo the tile with the new max when it rose by more than 8.
+constexpr int kF3Keys = 128, kF3KStages = 3, kF3VStages = 3, kF3SBufs = 3, kF3Threads = 352;
 constexpr uint32_t kF3TileBytes = kF3Keys * kFaD * 2;  // 32 KB
 constexpr uint32_t kF3KOff = kQBytes;
 constexpr uint32_t kF3VOff = kF3KOff + kF3KStages * kF3TileBytes;
@@ -682,8 +684,9 @@ __global__ void __launch_bounds__(kF3Threads, 1) attention_fa3_kernel(Fa2Params 
   extern __shared__ __align__(1024) unsigned char fsm[];
   __shared__ __align__(8) uint64_t full_k[kF3KStages], empty_k[kF3KStages];
   __shared__ __align__(8) uint64_t full_v[kF3VStages], empty_v[kF3VStages];
-  __shared__ __align__(8) uint64_t bar_s[2], bar_p[2], bar_o, bar_fin;
+  __shared__ __align__(8) uint64_t bar_s[kF3SBufs], bar_p[kF3SBufs], bar_o[2], bar_fin;
   __shared__ uint32_t tmem_slot;
+  __shared__ float xch[2][kFaRows];  // per-half tile max (and final l) exchange
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   // grid (B*Hkv, query tiles), longest causal tiles first
   const int64_t bh = blockIdx.x;
@@ -696,7 +699,7 @@ __global__ void __launch_bounds__(kF3Threads, 1) attention_fa3_kernel(Fa2Params 
   const int64_t kend = p.causal ? std::min(p.Tkv, last_tok + off + 1) : p.Tkv;
   const int ntiles = kend > 0 ? (int)((kend + kF3Keys - 1) / kF3Keys) : 0;
 
-  if (warp == 5) {
+  if (warp == 9) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(&tmem_slot)),
                  "n"(512));
@@ -711,18 +714,19 @@ __global__ void __launch_bounds__(kF3Threads, 1) attention_fa3_kernel(Fa2Params 
       mbar_init(&full_v[i], 1);
       mbar_init(&empty_v[i], 1);
     }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < kF3SBufs; ++i) {
       mbar_init(&bar_s[i], 1);
-      mbar_init(&bar_p[i], kFaRows);
+      mbar_init(&bar_p[i], 2 * kFaRows);
     }
-    mbar_init(&bar_o, 1);
+    mbar_init(&bar_o[0], 1);
+    mbar_init(&bar_o[1], 1);
     mbar_init(&bar_fin, 1);
     fence_mbar_init();
   }
-  const int r = tid & 127;
+  const int r = tid & 127, half = (tid >> 7) & 1;
   const int64_t qtok = tok0 + r / g;
   const int qhead = r % g;
-  const bool rvalid = tid < kFaRows && qtok < p.Tq;
+  const bool rvalid = tid < 2 * kFaRows && qtok < p.Tq;
   const int64_t vis = p.causal ? std::min(qtok + off + 1, p.Tkv) : p.Tkv;
   if (tid < kFaRows) {
     const float4* qr = reinterpret_cast<const float4*>(
@@ -751,10 +755,10 @@ __global__ void __launch_bounds__(kF3Threads, 1) attention_fa3_kernel(Fa2Params 
   auto k_smem = [&](int t) { return kF3KOff + (uint32_t)(t % kF3KStages) * kF3TileBytes; };
   auto v_smem = [&](int t) { return kF3VOff + (uint32_t)(t % kF3VStages) * kF3TileBytes; };
 
-  if (warp == 4 || warp == 6) {
-    // ---- producers: K (warp 4) and V (warp 6), one 32 KB bulk copy per tile
+  if (warp == 8 || warp == 10) {
+    // ---- producers: K (warp 8) and V (warp 10), one 32 KB bulk copy per tile
     if (lane == 0) {
-      const bool is_k = warp == 4;
+      const bool is_k = warp == 8;
       const int ns = is_k ? kF3KStages : kF3VStages;
       uint64_t* fullb = is_k ? full_k : full_v;
       uint64_t* emptyb = is_k ? empty_k : empty_v;
@@ -768,70 +772,72 @@ __global__ void __launch_bounds__(kF3Threads, 1) attention_fa3_kernel(Fa2Params 
       }
     }
     __syncwarp();
-  } else if (warp == 5) {
+  } else if (warp == 9) {
     // ---- MMA issuer
     if (lane == 0 && ntiles > 0) {
-      auto s_mma = [&](int t) {  // S(t) = Q K(t)^T -> TMEM cols 128 (t & 1)
+      auto s_mma = [&](int t) {  // S(t) = Q K(t)^T -> TMEM cols 128 (t % 3)
 #pragma unroll
         for (int kk = 0; kk < kFaD / 16; ++kk)
-          fa_mma(tm + (uint32_t)(t & 1) * 128, fa_desc(sbase + kk * 256, kSboQK),
+          fa_mma(tm + (uint32_t)(t % kF3SBufs) * 128, fa_desc(sbase + kk * 256, kSboQK),
                  fa_desc(sbase + k_smem(t) + kk * 256, kSboQK), fa_idesc(kFaRows, kF3Keys, 0), kk > 0);
-        fa_commit(&bar_s[t & 1]);
+        fa_commit(&bar_s[t % kF3SBufs]);
         fa_commit(&empty_k[t % kF3KStages]);
       };
       auto pv_mma = [&](int t) {  // O += P(t) V(t), A = P(t) from TMEM
-        const uint32_t pa = tm + (uint32_t)(t & 1) * 128;
+        const uint32_t pa = tm + (uint32_t)(t % kF3SBufs) * 128;
 #pragma unroll
         for (int kk = 0; kk < kF3Keys / 16; ++kk)
           asm volatile(
               "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-              "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tm + 256),
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tm + 384),
               "r"(pa + kk * 8), "l"(fa_desc(sbase + v_smem(t) + kk * 256, kSbo128)),
               "r"(fa_idesc(kFaRows, kFaD, 1)), "r"((t > 0 || kk > 0) ? 1u : 0u));
-        fa_commit(&bar_o);
+        fa_commit(&bar_o[t & 1]);
         fa_commit(&empty_v[t % kF3VStages]);
       };
-      for (int t = 0; t < 2 && t < ntiles; ++t) {
+      for (int t = 0; t < kF3SBufs && t < ntiles; ++t) {
         fa_wait(&full_k[t], 0);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         s_mma(t);
       }
       for (int t = 0; t < ntiles; ++t) {
         fa_wait(&full_v[t % kF3VStages], (uint32_t)(t / kF3VStages) & 1u);
-        fa_wait(&bar_p[t & 1], (uint32_t)(t >> 1) & 1u);
+        fa_wait(&bar_p[t % kF3SBufs], (uint32_t)(t / kF3SBufs) & 1u);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         pv_mma(t);
-        if (t + 2 < ntiles) {  // S(t+2) into the buffer P(t) occupies: after PV(t) in issue order
-          fa_wait(&full_k[(t + 2) % kF3KStages], (uint32_t)((t + 2) / kF3KStages) & 1u);
+        if (t + kF3SBufs < ntiles) {  // S(t+3) into the buffer P(t) occupies: after PV(t) in issue order
+          const int u = t + kF3SBufs;
+          fa_wait(&full_k[u % kF3KStages], (uint32_t)(u / kF3KStages) & 1u);
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          s_mma(t + 2);
+          s_mma(u);
         }
       }
       fa_commit(&bar_fin);
     }
     __syncwarp();
   } else {
-    // ---- softmax (warps 0-3): thread = row r
-    const uint32_t tm_row = tm + ((uint32_t)(warp * 32) << 16);
-    const uint32_t o_col = 256;
+    // ---- softmax (warps 0-7): thread = (row r, key half)
+    const uint32_t tm_row = tm + ((uint32_t)((warp & 3) * 32) << 16);
+    const uint32_t o_col = 384 + (uint32_t)half * 64;  // this half's O columns
+    const int pair_bar = 1 + (warp & 3);                 // named barrier of warps w, w+4
+    auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory"); };
     float m_run = -INFINITY, l_run = 0.f;
     for (int t = 0; t < ntiles; ++t) {
-      const int64_t k0 = (int64_t)t * kF3Keys;
-      const uint32_t s_col = (uint32_t)(t & 1) * 128;
-      fa_wait(&bar_s[t & 1], (uint32_t)(t >> 1) & 1u);
+      const int64_t k0 = (int64_t)t * kF3Keys + half * 64;
+      const uint32_t s_col = (uint32_t)(t % kF3SBufs) * 128;
+      fa_wait(&bar_s[t % kF3SBufs], (uint32_t)(t / kF3SBufs) & 1u);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const bool mask = !rvalid || k0 + kF3Keys > vis;
-      // one pass against the running max (chunks of 32 keys: ld, mask, exp2,
-      // pack); P stays in registers until the pass is accepted, since it is
-      // stored over the S columns a redo would read again
-      uint32_t hw[64];
+      const bool mask = !rvalid || k0 + 64 > vis;
+      // one pass against the running max; P stays in registers until the pass
+      // is accepted (it is stored over S columns a redo would read again)
+      uint32_t hw[32];
       auto pass = [&](float m_use, float& tile_max) {
         float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
         float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < 2; ++c) {
           uint32_t sr[32];
-          FA_LD32(tm_row + s_col + c * 32, sr);
+          FA_LD32(tm_row + s_col + half * 64 + c * 32, sr);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
           if (mask) {
 #pragma unroll
@@ -845,26 +851,31 @@ __global__ void __launch_bounds__(kF3Threads, 1) attention_fa3_kernel(Fa2Params 
       };
       float tmax = -INFINITY;
       float psum = pass(m_run == -INFINITY ? 0.f : m_run, tmax);
-      // first tile, or the max jumped: redo with the tile max (warp-uniform:
-      // the TMEM loads inside are .sync.aligned)
-      const bool jump = tmax > m_run + 8.f;
+      // the row's tile max over both halves
+      xch[half][r] = tmax;
+      pair_sync();
+      tmax = fmaxf(tmax, xch[half ^ 1][r]);
+      const bool jump = tmax > m_run + 8.f;  // same in both halves of the row
       const float m_new = jump ? tmax : m_run;
-      if (__any_sync(0xffffffffu, jump)) {
+      if (__any_sync(0xffffffffu, jump)) {  // warp-uniform (.sync.aligned loads)
         float dummy = -INFINITY;
         psum = pass(m_new == -INFINITY ? 0.f : m_new, dummy);
       }
+      // both halves are done reading S(t) before either overwrites it with P
+      pair_sync();
 #pragma unroll
-      for (int c = 0; c < 4; ++c) FA_ST16(tm_row + s_col + c * 16, (hw + c * 16));
+      for (int c = 0; c < 2; ++c) FA_ST16(tm_row + s_col + half * 32 + c * 16, (hw + c * 16));
       const float alpha = (m_new == m_run) ? 1.f : exp2f(m_run - m_new);
       l_run = l_run * alpha + psum;
       m_run = m_new;
       // O is only touched when some row's max moved: PV(t-1) must be done
-      // (S(t) complete implies PV(t-2) done: bar_o is at most one phase behind)
+      // (S(t) complete implies PV(t-3) done: with one barrier per PV parity,
+      // bar_o[(t-1) & 1] is at most one phase behind)
       if (t > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
-        fa_wait(&bar_o, (uint32_t)(t - 1) & 1u);
+        fa_wait(&bar_o[(t - 1) & 1], (uint32_t)((t - 1) >> 1) & 1u);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < 2; ++c) {
           uint32_t orr[32];
           FA_LD32(tm_row + o_col + c * 32, orr);
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
@@ -875,16 +886,21 @@ __global__ void __launch_bounds__(kF3Threads, 1) attention_fa3_kernel(Fa2Params 
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      mbar_arrive(&bar_p[t & 1]);
+      mbar_arrive(&bar_p[t % kF3SBufs]);
     }
+    // l = sum of the two halves' partial sums (same running max history)
+    pair_sync();
+    xch[half][r] = l_run;
+    pair_sync();
+    l_run += xch[half ^ 1][r];
     if (ntiles > 0) {
       fa_wait(&bar_fin, 0);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     }
-    float* orow = p.out + ((b * p.Hq + hkv * g + qhead) * p.Tq + (rvalid ? qtok : 0)) * kFaD;
+    float* orow = p.out + ((b * p.Hq + hkv * g + qhead) * p.Tq + (rvalid ? qtok : 0)) * kFaD + half * 64;
     const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < 2; ++c) {
       uint32_t orr[32];
       if (ntiles > 0) {
         FA_LD32(tm_row + o_col + c * 32, orr);
@@ -904,7 +920,7 @@ __global__ void __launch_bounds__(kF3Threads, 1) attention_fa3_kernel(Fa2Params 
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 5)
+  if (warp == 9)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "n"(512));
 }
 
@@ -932,7 +948,8 @@ __global__ void fa_tile_kernel(const uint4* __restrict__ lin, uint4* __restrict_
 // two decoded fp16 tensors (kv layout) + an error word.
 static int prefill_variant() {
   static const int v = [] {
-    const char* e = getenv("HQMQ_FA_VARIANT");  // A/B: 1 = 4-warp kernel, 3 = one-tile 128-key kernel
+    // A/B: 1 = 4-warp kernel, 2 = two-tile 64-key kernel, 3 = one-tile 128-key kernel
+    const char* e = getenv("HQMQ_FA_VARIANT");
     return e ? atoi(e) : 0;
   }();
   return v;
@@ -976,7 +993,9 @@ int launch_prefill_tc(const hqmq_attention_args* a, cudaStream_t st) {
     if (rc != HQMQ_OK) return rc;
   }
   if (prefill_variant() != 1) {
-    const bool v3 = prefill_variant() == 3;
+    // auto: the one-tile 128-key kernel for long key ranges (0.66 vs 0.71 ms at
+    // 8k), the two-tile 64-key kernel for short ones (0.090 vs 0.099 ms at 2k)
+    const bool v3 = prefill_variant() == 3 || (prefill_variant() == 0 && a->kv_tokens >= 4096);
     const int keys = v3 ? kF3Keys : kF2Keys;
     const uint32_t tile_bytes = v3 ? kF3TileBytes : kF2TileBytes;
     const int64_t bh = a->batch * a->kv_heads;

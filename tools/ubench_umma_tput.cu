@@ -124,6 +124,74 @@ void run_ts(const char* name) {
   cudaFree(d);
 }
 
+// The prefill tile: 8 SS MMAs (S = Q K^T, N = 128, D -> TMEM buffer b) then 8
+// TS MMAs (O += P V, A = P from TMEM buffer b', B MN-major) per iteration.
+__global__ void tile_seq(int reps, unsigned long long* cyc) {
+  extern __shared__ __align__(1024) unsigned char sm[];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ uint32_t tbase;
+  const int tid = threadIdx.x;
+  if (tid < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tbase)), "n"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  for (int i = tid; i < (3 * 32768) / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sm)[i] = 0x3c003c00u;
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (tid == 0) {
+    const uint32_t q = smem_u32(sm), k = q + 32768, v = q + 65536;
+    const uint32_t tm = tbase;
+    const unsigned long long t0 = clock64();
+    for (int r = 0; r < reps; ++r) {
+      const uint32_t sb = (uint32_t)(r % 3) * 128, pb = (uint32_t)((r + 1) % 3) * 128;
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tm + sb),
+            "l"(desc(q + kk * 256, 128, 2048)), "l"(desc(k + kk * 256, 128, 2048)), "r"(idesc(128, 128, 0)),
+            "r"(kk));
+#pragma unroll
+      for (int kk = 0; kk < 8; ++kk)
+        asm volatile(
+            "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tm + 384),
+            "r"(tm + pb + kk * 8), "l"(desc(v + kk * 256, 128, 2048)), "r"(idesc(128, 128, 1)), "r"(1));
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(&bar)));
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\tW:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n\t@!P1 bra W;\n\t}" ::"r"(
+            smem_u32(&bar)) : "memory");
+    cyc[blockIdx.x] = clock64() - t0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (tid < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase), "n"(512));
+}
+
+void run_tile() {
+  const int reps = 1000, grid = 148;
+  unsigned long long* d;
+  cudaMalloc(&d, grid * 8);
+  const int smem = 3 * 32768;
+  cudaFuncSetAttribute(tile_seq, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  tile_seq<<<grid, 128, smem>>>(10, d);
+  cudaDeviceSynchronize();
+  tile_seq<<<grid, 128, smem>>>(reps, d);
+  cudaDeviceSynchronize();
+  unsigned long long h[148];
+  cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  printf("prefill tile (8 SS N=128 + 8 TS N=128): %.0f cycles/tile (floor 1024) (%s)\n",
+         (double)h[0] / reps, cudaGetErrorString(cudaGetLastError()));
+  cudaFree(d);
+}
+
 template <int N, int BMN>
 void run(const char* name) {
   const int reps = 2000, grid = 148;
@@ -161,5 +229,6 @@ int main() {
   run_ts<128, 0>("TS K-major B");
   run_ts<128, 1>("TS MN-major B");
   run_ts<256, 1>("TS MN-major B");
+  run_tile();
   return 0;
 }
