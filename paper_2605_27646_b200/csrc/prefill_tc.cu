@@ -651,7 +651,7 @@ __global__ void __launch_bounds__(kF2Threads, 1) attention_fa2_kernel(Fa2Params 
 }
 
 // ------------------------------------------------------------------------
-// 128-key version (default from 4096 keys; HQMQ_FA_VARIANT=3 forces it).  One query tile of 128 rows per CTA
+// 128-key one-tile version (HQMQ_FA_VARIANT=3).  One query tile of 128 rows per CTA
 // (128 / g tokens x g heads of one kv head), 11 warps: softmax warps 0-7
 // (warps w and w+4 share TMEM lanes 32 (w % 4): warp w < 4 takes keys 0-63
 // of each row, warp w+4 keys 64-127), K producer (8), MMA issuer (9), V
@@ -924,6 +924,227 @@ __global__ void __launch_bounds__(kF3Threads, 1) attention_fa3_kernel(Fa2Params 
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "n"(512));
 }
 
+// ------------------------------------------------------------------------
+// Two-CTAs-per-SM version (default from 4096 keys).  Each CTA is one strictly
+// sequential pipeline over 128-key tiles -- S(t) -> softmax(t) -> PV(t) ->
+// S(t+1) -- and the two co-resident CTAs interleave on the SM's tensor cores,
+// MUFU and TMEM ports, so one CTA's softmax hides the other's MMAs (and each
+// CTA's prologue / epilogue hides behind the other's steady state).
+// CTA = 128 query rows, 10 warps: softmax 0-7 (warps w and w+4 share TMEM
+// lanes 32 (w % 4) and split each row's 128 keys), producer 8 (K then V, one
+// stage each: K(t+1) streams in during softmax(t), V(t+1) during S(t+1)),
+// MMA issuer 9.  TMEM 256 columns: S [0,128) with P(t) over
+// its first 64, O [128,256).  Because S(t) is issued after PV(t-1), S(t)
+// complete implies O is idle: the softmax rescales O without any wait.
+constexpr int kF4Threads = 320;
+constexpr uint32_t kF4KOff = kQBytes, kF4VOff = kQBytes + kF3TileBytes;
+constexpr uint32_t kF4Smem = kQBytes + 2 * kF3TileBytes;  // 96 KB: two CTAs per SM
+
+__global__ void __launch_bounds__(kF4Threads, 2) attention_fa4_kernel(Fa2Params p) {
+  extern __shared__ __align__(1024) unsigned char fsm[];
+  __shared__ __align__(8) uint64_t full_k, empty_k, full_v, empty_v, bar_s, bar_p, bar_fin;
+  __shared__ uint32_t tmem_slot;
+  __shared__ float xch[2][kFaRows];  // per-half tile max / final l exchange
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t bh = blockIdx.x;
+  const int64_t b = bh / p.Hkv, hkv = bh % p.Hkv;
+  const int g = p.g;
+  const int tpt = kFaRows / g;
+  const int64_t tok0 = (int64_t)(gridDim.y - 1 - blockIdx.y) * tpt;
+  const int64_t off = p.causal ? (p.Tkv - p.Tq) : 0;
+  const int64_t last_tok = std::min(p.Tq, tok0 + tpt) - 1;
+  const int64_t kend = p.causal ? std::min(p.Tkv, last_tok + off + 1) : p.Tkv;
+  const int ntiles = kend > 0 ? (int)((kend + kF3Keys - 1) / kF3Keys) : 0;
+
+  if (warp == 9) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(&tmem_slot)),
+                 "n"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    mbar_init(&full_k, 1);
+    mbar_init(&empty_k, 1);
+    mbar_init(&full_v, 1);
+    mbar_init(&empty_v, 1);
+    mbar_init(&bar_s, 1);
+    mbar_init(&bar_p, 2 * kFaRows);
+    mbar_init(&bar_fin, 1);
+    fence_mbar_init();
+  }
+  const int r = tid & 127, half = (tid >> 7) & 1;
+  const int64_t qtok = tok0 + r / g;
+  const int qhead = r % g;
+  const bool rvalid = tid < 2 * kFaRows && qtok < p.Tq;
+  const int64_t vis = p.causal ? std::min(qtok + off + 1, p.Tkv) : p.Tkv;
+  if (tid < kFaRows) {
+    const float4* qr = reinterpret_cast<const float4*>(
+        p.q + ((b * p.Hq + hkv * g + qhead) * p.Tq + (rvalid ? qtok : 0)) * kFaD);
+#pragma unroll 4
+    for (int kg = 0; kg < kFaD / 8; ++kg) {
+      float4 a = make_float4(0.f, 0.f, 0.f, 0.f), c = a;
+      if (rvalid) {
+        a = __ldg(qr + 2 * kg);
+        c = __ldg(qr + 2 * kg + 1);
+      }
+      const float sl = p.scale_log2;
+      const __half2 h0 = __floats2half2_rn(a.x * sl, a.y * sl), h1 = __floats2half2_rn(a.z * sl, a.w * sl);
+      const __half2 h2 = __floats2half2_rn(c.x * sl, c.y * sl), h3 = __floats2half2_rn(c.z * sl, c.w * sl);
+      *reinterpret_cast<uint4*>(fsm + (r >> 3) * kSboQK + kg * 128 + (r & 7) * 16) =
+          make_uint4(*reinterpret_cast<const uint32_t*>(&h0), *reinterpret_cast<const uint32_t*>(&h1),
+                     *reinterpret_cast<const uint32_t*>(&h2), *reinterpret_cast<const uint32_t*>(&h3));
+    }
+  }
+  fence_proxy_async();
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tm = tmem_slot;
+  const uint32_t sbase = smem_u32(fsm);
+
+  if (warp == 8) {
+    // ---- producer: K(t) when S(t-1) has read the K stage, V(t) when PV(t-1)
+    // has read the V stage
+    if (lane == 0) {
+      const unsigned char* kb = p.kt + (size_t)bh * p.ntk * kF3TileBytes;
+      const unsigned char* vb = p.vt + (size_t)bh * p.ntk * kF3TileBytes;
+      for (int t = 0; t < ntiles; ++t) {
+        if (t > 0) fa_wait(&empty_k, (uint32_t)(t - 1) & 1u);
+        mbar_arrive_expect_tx(&full_k, kF3TileBytes);
+        bulk_g2s(fsm + kF4KOff, kb + (size_t)t * kF3TileBytes, kF3TileBytes, &full_k);
+        if (t > 0) fa_wait(&empty_v, (uint32_t)(t - 1) & 1u);
+        mbar_arrive_expect_tx(&full_v, kF3TileBytes);
+        bulk_g2s(fsm + kF4VOff, vb + (size_t)t * kF3TileBytes, kF3TileBytes, &full_v);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 9) {
+    // ---- MMA issuer
+    if (lane == 0 && ntiles > 0) {
+      for (int t = 0; t < ntiles; ++t) {
+        const uint32_t ph = (uint32_t)t & 1u;
+        fa_wait(&full_k, ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+        for (int kk = 0; kk < kFaD / 16; ++kk)
+          fa_mma(tm, fa_desc(sbase + kk * 256, kSboQK), fa_desc(sbase + kF4KOff + kk * 256, kSboQK),
+                 fa_idesc(kFaRows, kF3Keys, 0), kk > 0);
+        fa_commit(&bar_s);
+        fa_commit(&empty_k);
+        fa_wait(&bar_p, ph);
+        fa_wait(&full_v, ph);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+        for (int kk = 0; kk < kF3Keys / 16; ++kk)
+          asm volatile(
+              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tm + 128),
+              "r"(tm + kk * 8), "l"(fa_desc(sbase + kF4VOff + kk * 256, kSbo128)),
+              "r"(fa_idesc(kFaRows, kFaD, 1)), "r"((t > 0 || kk > 0) ? 1u : 0u));
+        fa_commit(&empty_v);
+      }
+      fa_commit(&bar_fin);
+    }
+    __syncwarp();
+  } else {
+    // ---- softmax (warps 0-7): thread = (row r, key half); warps w and w+4
+    // share TMEM lanes 32 (w % 4) and exchange tile maxima / l in shared memory
+    const uint32_t tm_row = tm + ((uint32_t)((warp & 3) * 32) << 16);
+    const uint32_t o_col = 128 + (uint32_t)half * 64;
+    const int pair_bar = 1 + (warp & 3);
+    auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory"); };
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int t = 0; t < ntiles; ++t) {
+      const int64_t k0 = (int64_t)t * kF3Keys + half * 64;
+      fa_wait(&bar_s, (uint32_t)t & 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const bool mask = !rvalid || k0 + 64 > vis;
+      uint32_t hw[32];
+      auto pass = [&](float m_use, float& tile_max) {
+        float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+        float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t sr[32];
+          FA_LD32(tm_row + half * 64 + c * 32, sr);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+          if (mask) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (!rvalid || k0 + c * 32 + j >= vis) sr[j] = __float_as_uint(-INFINITY);
+          }
+          fa_softmax32(sr, m_use, mx, acc, hw + c * 16);
+        }
+        tile_max = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+        return (acc[0].x + acc[0].y) + (acc[1].x + acc[1].y);
+      };
+      float tmax = -INFINITY;
+      float psum = pass(m_run == -INFINITY ? 0.f : m_run, tmax);
+      xch[half][r] = tmax;
+      pair_sync();
+      tmax = fmaxf(tmax, xch[half ^ 1][r]);
+      const bool jump = tmax > m_run + 8.f;  // same in both halves of the row
+      const float m_new = jump ? tmax : m_run;
+      if (__any_sync(0xffffffffu, jump)) {  // warp-uniform (.sync.aligned loads)
+        float dummy = -INFINITY;
+        psum = pass(m_new == -INFINITY ? 0.f : m_new, dummy);
+      }
+      pair_sync();  // both halves done reading S(t) before P overwrites it
+#pragma unroll
+      for (int c = 0; c < 2; ++c) FA_ST16(tm_row + half * 32 + c * 16, (hw + c * 16));
+      const float alpha = (m_new == m_run) ? 1.f : exp2f(m_run - m_new);
+      l_run = l_run * alpha + psum;
+      m_run = m_new;
+      if (t > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {  // O idle: S(t) done => PV(t-1) done
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t orr[32];
+          FA_LD32(tm_row + o_col + c * 32, orr);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int j = 0; j < 32; ++j) orr[j] = __float_as_uint(__uint_as_float(orr[j]) * alpha);
+          FA_ST32(tm_row + o_col + c * 32, orr);
+        }
+      }
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(&bar_p);
+    }
+    pair_sync();
+    xch[half][r] = l_run;
+    pair_sync();
+    l_run += xch[half ^ 1][r];
+    if (ntiles > 0) {
+      fa_wait(&bar_fin, 0);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    }
+    float* orow = p.out + ((b * p.Hq + hkv * g + qhead) * p.Tq + (rvalid ? qtok : 0)) * kFaD + half * 64;
+    const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      uint32_t orr[32];
+      if (ntiles > 0) {
+        FA_LD32(tm_row + o_col + c * 32, orr);
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) orr[j] = 0u;
+      }
+      if (rvalid) {
+#pragma unroll
+        for (int j = 0; j < 32; j += 4)
+          *reinterpret_cast<float4*>(orow + c * 32 + j) =
+              make_float4(__uint_as_float(orr[j]) * inv, __uint_as_float(orr[j + 1]) * inv,
+                          __uint_as_float(orr[j + 2]) * inv, __uint_as_float(orr[j + 3]) * inv);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 9)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "n"(256));
+}
+
 // Linear decoded fp16 (B*Hkv, T, 128) -> kt-key UMMA tiles (16-byte units):
 //   K-major (K):  unit(key, dg) at (key/8)*128 + dg*8 + key%8
 //   MN-major (V): unit(key, dg) at dg*kt + (key/8)*8 + key%8
@@ -948,7 +1169,8 @@ __global__ void fa_tile_kernel(const uint4* __restrict__ lin, uint4* __restrict_
 // two decoded fp16 tensors (kv layout) + an error word.
 static int prefill_variant() {
   static const int v = [] {
-    // A/B: 1 = 4-warp kernel, 2 = two-tile 64-key kernel, 3 = one-tile 128-key kernel
+    // A/B: 1 = 4-warp kernel, 2 = two-tile 64-key kernel, 3 = one-tile 128-key
+    // kernel, 4 = two-CTAs-per-SM 128-key kernel
     const char* e = getenv("HQMQ_FA_VARIANT");
     return e ? atoi(e) : 0;
   }();
@@ -993,9 +1215,11 @@ int launch_prefill_tc(const hqmq_attention_args* a, cudaStream_t st) {
     if (rc != HQMQ_OK) return rc;
   }
   if (prefill_variant() != 1) {
-    // auto: the one-tile 128-key kernel for long key ranges (0.66 vs 0.71 ms at
-    // 8k), the two-tile 64-key kernel for short ones (0.090 vs 0.099 ms at 2k)
-    const bool v3 = prefill_variant() == 3 || (prefill_variant() == 0 && a->kv_tokens >= 4096);
+    // auto: the two-CTAs-per-SM 128-key kernel for long key ranges (0.62 ms at
+    // 8k vs 0.655 one-tile 128-key, 0.71 two-tile 64-key), the two-tile 64-key
+    // kernel for short ones (0.090 vs 0.093 ms at 2k)
+    const bool v4 = prefill_variant() == 4 || (prefill_variant() == 0 && a->kv_tokens >= 4096);
+    const bool v3 = v4 || prefill_variant() == 3;
     const int keys = v3 ? kF3Keys : kF2Keys;
     const uint32_t tile_bytes = v3 ? kF3TileBytes : kF2TileBytes;
     const int64_t bh = a->batch * a->kv_heads;
@@ -1010,6 +1234,18 @@ int launch_prefill_tc(const hqmq_attention_args* a, cudaStream_t st) {
                                            bh, a->kv_tokens, ntk, 1, keys);
     int rc = check_launch();
     if (rc != HQMQ_OK) return rc;
+    if (v4) {
+      Fa2Params q4;
+      q4.B = a->batch; q4.Hq = a->q_heads; q4.Hkv = a->kv_heads; q4.Tq = a->q_tokens;
+      q4.Tkv = a->kv_tokens; q4.ntk = ntk;
+      q4.g = (int)(a->q_heads / a->kv_heads); q4.causal = a->causal;
+      q4.scale_log2 = (float)(a->scale * 1.4426950408889634);
+      q4.q = a->q; q4.kt = kt; q4.vt = vt; q4.out = a->out;
+      cudaFuncSetAttribute(attention_fa4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF4Smem);
+      const dim3 grid((unsigned)bh, (unsigned)ceil_div(a->q_tokens, kFaRows / q4.g));
+      attention_fa4_kernel<<<grid, kF4Threads, kF4Smem, st>>>(q4);
+      return check_launch();
+    }
     if (v3) {
       Fa2Params q3;
       q3.B = a->batch; q3.Hq = a->q_heads; q3.Hkv = a->kv_heads; q3.Tq = a->q_tokens;

@@ -1,5 +1,6 @@
 """The tcgen05 prefill kernels forced one by one (HQMQ_FA_VARIANT: 1 = 4-warp
-kernel, 2 = two-tile 64-key kernel, 3 = one-tile 128-key kernel) against the dense fp64 attention over the decoded
+kernel, 2 = two-tile 64-key kernel, 3 = one-tile 128-key kernel, 4 = two-CTAs-per-SM
+128-key kernel) against the dense fp64 attention over the decoded
 cache, in subprocesses (the variant is read once per process).  The default
 kernel is covered by test_gpu_parity.py::test_attention_prefill_tensor_core."""
 
@@ -35,7 +36,7 @@ print("WORST", worst)
 """
 
 
-@pytest.mark.parametrize("variant", ["1", "2", "3"])
+@pytest.mark.parametrize("variant", ["1", "2", "3", "4"])
 def test_prefill_variant(cuda, variant):
     env = dict(os.environ, HQMQ_FA_VARIANT=variant)
     res = subprocess.run([sys.executable, "-c", SNIPPET.format(root=ROOT)], env=env,
