@@ -81,6 +81,27 @@ def test_c_struct_sizes_with_compiler(tmp_path):
                    _native.EncodeArgs.flag_capacity_words.offset]
 
 
+def test_paged_struct_layouts_with_compiler(tmp_path):
+    """The paged decode-attention structs (hqmq_paged_view / hqmq_paged_attention_args)."""
+    from paper_2605_27646_b200 import _native
+
+    src = tmp_path / "probe_paged.c"
+    src.write_text(
+        '#include <stdio.h>\n#include <stddef.h>\n#include "hqmq_b200.h"\n'
+        "int main(){printf(\"%zu %zu %zu %zu %zu %zu\\n\", sizeof(hqmq_paged_view),"
+        " sizeof(hqmq_paged_attention_args), offsetof(hqmq_paged_attention_args, scale),"
+        " offsetof(hqmq_paged_attention_args, k), offsetof(hqmq_paged_attention_args, num_splits),"
+        " offsetof(hqmq_paged_attention_args, workspace_bytes));return 0;}\n")
+    exe = tmp_path / "probe_paged"
+    import subprocess
+
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    out = [int(v) for v in subprocess.check_output([str(exe)]).split()]
+    A = _native.PagedAttentionArgs
+    assert out == [ctypes.sizeof(_native.PagedView), ctypes.sizeof(A), A.scale.offset, A.k.offset,
+                   A.num_splits.offset, A.workspace_bytes.offset]
+
+
 def test_no_cpu_fallback_without_device():
     torch = pytest.importorskip("torch")
     if torch.cuda.is_available():
