@@ -169,12 +169,31 @@ def run_ours(args, wl, world, rank, local):
     import paper_2605_27646_b200 as hq
     from paper_2605_27646_b200 import _native
 
+    # HQMQ_BENCH_BACKEND=gloo runs the N>1 plumbing with several ranks on one
+    # GPU (a check of the multi-rank code path only; real runs use NCCL)
+    backend = os.environ.get("HQMQ_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
+
+    def all_reduce(t, op=None):
+        """all_reduce on the backend's device (gloo: via host memory)."""
+        op = op if op is not None else dist.ReduceOp.SUM
+        if backend == "nccl":
+            dist.all_reduce(t, op=op)
+            return t
+        h = t.cpu()
+        dist.all_reduce(h, op=op)
+        t.copy_(h)
+        return t
     lib = _native.load()
     units = units_for_rank(wl, world, rank)
     cfg = hq.CodecConfig(codebook_size=wl["S"], radius_bits=wl["br"], seed=0,
@@ -336,10 +355,10 @@ def run_ours(args, wl, world, rank, local):
             elapsed_ms = start.elapsed_time(stop)
     if world > 1:
         t = torch.tensor([elapsed_ms, enc_ms, dec_ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed_ms, enc_ms, dec_ms = t.tolist()
         units_total = torch.tensor([len(units)], device=dev)
-        dist.all_reduce(units_total)
+        all_reduce(units_total)
         total_units = int(units_total.item())
     else:
         total_units = len(units)
@@ -474,10 +493,10 @@ def run_ours(args, wl, world, rank, local):
             e2e = {"error": repr(exc)[:300]}
         if world > 1 and "ms_per_step" in e2e:
             t = torch.tensor([e2e["ms_per_step"]], dtype=torch.float64, device=dev)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            all_reduce(t, op=dist.ReduceOp.MAX)
             nb = torch.tensor([e2e["h2d_bytes_per_step"], e2e["d2h_bytes_per_step"]],
                               dtype=torch.float64, device=dev)
-            dist.all_reduce(nb)
+            all_reduce(nb)
             ms = float(t.item())
             e2e.update(ms_per_step=round(ms, 3), h2d_bytes_per_step=int(nb[0].item()),
                        d2h_bytes_per_step=int(nb[1].item()),
