@@ -326,6 +326,13 @@ __device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
   const __half2 h = __floats2half2_rn(lo, hi);
   return *reinterpret_cast<const uint32_t*>(&h);
 }
+// (q, q) as fp16x2 for an integer radius code q < 1024, without the
+// quarter-rate I2F: 0x6400 | q is the fp16 1024 + q (exact), minus 1024.
+__device__ __forceinline__ uint32_t code_half2(uint32_t q) {
+  const uint32_t biased = (q * 0x10001u) | 0x64006400u;
+  const __half2 r = __hsub2(*reinterpret_cast<const __half2*>(&biased), __float2half2_rn(1024.f));
+  return *reinterpret_cast<const uint32_t*>(&r);
+}
 __device__ __forceinline__ uint32_t hmul2u(uint32_t a, uint32_t b) {
   const __half2 r = __hmul2(*reinterpret_cast<const __half2*>(&a), *reinterpret_cast<const __half2*>(&b));
   return *reinterpret_cast<const uint32_t*>(&r);
@@ -502,9 +509,7 @@ __global__ void __launch_bounds__(kMThreads, 2) attention_mma_kernel(AttParams p
 #pragma unroll
         for (int ks = 0; ks < 8; ++ks) {
           const uint2 cw = ktab[min(ic.get(ks), cwmax)];
-          const __half hq = __uint2half_rn(rc.get(ks));
-          const __half2 q2 = __half2half2(hq);
-          const uint32_t qq = *reinterpret_cast<const uint32_t*>(&q2);
+          const uint32_t qq = code_half2(rc.get(ks));
           mma_rows8(sc[nt], qa[ks][0], qa[ks][1], hmul2u(qq, cw.x), hmul2u(qq, cw.y));
         }
       }
@@ -561,8 +566,7 @@ __global__ void __launch_bounds__(kMThreads, 2) attention_mma_kernel(AttParams p
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const uint2 cw = vtab[min(ic.get(j), cwmax)];
-          const __half2 q2 = __half2half2(__uint2half_rn(rc.get(j)));
-          const uint32_t qq = *reinterpret_cast<const uint32_t*>(&q2);
+          const uint32_t qq = code_half2(rc.get(j));
           vv[e][j] = make_uint2(hmul2u(qq, cw.x), hmul2u(qq, cw.y));
         }
       }
