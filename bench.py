@@ -93,6 +93,14 @@ class ClockSampler:
             self.lines.append(line.strip())
 
     def __exit__(self, *exc):
+        self.late = False
+        if self.proc and not self.lines:
+            # timed region shorter than nvidia-smi's start-up + 200 ms period
+            # (e.g. C1): take the first sample right after it, and say so
+            t_end = time.time() + 3.0
+            while not self.lines and time.time() < t_end:
+                time.sleep(0.02)
+            self.late = bool(self.lines)
         if self.proc:
             self.proc.terminate()
             try:
@@ -117,8 +125,11 @@ class ClockSampler:
                     reasons.add(nm)
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-                "samples": len(sm)}
+        out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+               "samples": len(sm)}
+        if getattr(self, "late", False):
+            out["note"] = "timed region shorter than the sampling period: sampled just after it"
+        return out
 
 
 def measured_peaks():
