@@ -14,4 +14,11 @@ timeout 1500 compute-sanitizer --tool racecheck --error-exitcode 9 \
 timeout 900 compute-sanitizer --tool synccheck --error-exitcode 9 \
   python -m pytest tests/test_gpu_parity.py -x -q -k "golden and s64" \
   > gpurun_out/sanitize_synccheck.log 2>&1; echo "synccheck rc=$?" >> gpurun_out/sanitize_synccheck.log
+# paged decode attention and the tcgen05 prefill kernels (all four, via the variant tests)
+timeout 1500 compute-sanitizer --tool memcheck --leak-check no --error-exitcode 9 \
+  python -m pytest tests/test_gpu_paged.py tests/test_gpu_prefill_variants.py -x -q -k "not 256" \
+  > gpurun_out/sanitize_memcheck_attn.log 2>&1; echo "memcheck rc=$?" >> gpurun_out/sanitize_memcheck_attn.log
+timeout 1500 compute-sanitizer --tool racecheck --error-exitcode 9 \
+  python -m pytest tests/test_gpu_parity.py -x -q -k "prefill_tensor_core" \
+  > gpurun_out/sanitize_racecheck_attn.log 2>&1; echo "racecheck rc=$?" >> gpurun_out/sanitize_racecheck_attn.log
 echo done
