@@ -504,13 +504,15 @@ __global__ void __launch_bounds__(kEncThreads, 2) encode_tile_kernel(EncParams p
 constexpr int kWWarps = 8;
 constexpr int kWThreads = kWWarps * 32;
 
-__device__ __forceinline__ double warp_max_f64(double v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const double w = __shfl_xor_sync(0xffffffffu, v, o);
-    v = w > v ? w : v;
-  }
-  return v;
+// Warp max of NON-NEGATIVE doubles (squared norms, norms): their bit patterns
+// order like unsigned integers, so two redux.sync (high words, then low words
+// of the lanes holding the max high word) replace five shuffle/compare rounds.
+__device__ __forceinline__ double warp_max_nonneg_f64(double v) {
+  const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+  const unsigned hi = (unsigned)(b >> 32), lo = (unsigned)b;
+  const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+  const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+  return __longlong_as_double((long long)(((unsigned long long)mhi << 32) | mlo));
 }
 
 // kMode: 0 = fused (one pass), 1 = prep only (exact norms / flags / scales /
@@ -614,7 +616,7 @@ __global__ void __launch_bounds__(kWThreads, kMinB) encode_warp_kernel(EncParams
         const bool valid = j < ntok;
         const bool fl = ext && valid && sqrt_gt(sq[j], thr);
         fmask[j] = __ballot_sync(0xffffffffu, fl);
-        const double m = warp_max_f64(fl ? 0.0 : sq[j]);
+        const double m = warp_max_nonneg_f64(fl ? 0.0 : sq[j]);
         sig_l = (lane % kWT) == j ? m : sig_l;
       }
       sig_l = __dsqrt_rn(sig_l);
@@ -671,7 +673,7 @@ __global__ void __launch_bounds__(kWThreads, kMinB) encode_warp_kernel(EncParams
         const bool fl = valid && r > thr;
         fmask[j] = __ballot_sync(0xffffffffu, fl);
         const bool live = valid && !fl && r > 0.0;
-        double sg = warp_max_f64(fl ? 0.0 : r);
+        double sg = warp_max_nonneg_f64(fl ? 0.0 : r);
         if (!(sg > 0.0)) sg = 1.0;
         const __half hs = __double2half(sg);
         const double sw = (double)__half2float(hs);
