@@ -44,3 +44,26 @@ def test_prefill_variant(cuda, variant):
     assert res.returncode == 0, res.stderr[-2000:]
     worst = float(res.stdout.strip().split("WORST")[-1])
     assert worst < 2e-3, worst
+
+
+def test_prefill_default_long(cuda):
+    """The automatic choice for >= 4096 keys (two-CTAs-per-SM kernel), causal and
+    chunked (T_q < T_kv), against the dense fp64 attention over the decoded cache."""
+    import torch
+
+    import paper_2605_27646_b200 as m
+
+    g = torch.Generator(device=cuda).manual_seed(11)
+    cfg = m.CodecConfig(64, 4)
+    bank = m.CodebookBank(0, 64)
+    for (B, HQ, HKV, TQ, TK) in [(1, 8, 2, 4500, 4500), (1, 4, 1, 700, 5000)]:
+        k = torch.randn((B, HKV, TK, 128), generator=g, device=cuda).half()
+        v = torch.randn((B, HKV, TK, 128), generator=g, device=cuda).half()
+        q = torch.randn((B, HQ, TQ, 128), generator=g, device=cuda)
+        pk = m.encode_tensor(k, cfg, role="K", bank=bank)
+        pv = m.encode_tensor(v, cfg, role="V", bank=bank)
+        acfg = m.AttentionConfig(B, HQ, HKV, TQ, TK, 128, causal=True)
+        out = m.fused_attend(q, pk, pv, bank, acfg).double()
+        dense = m.reference_attend(q, m.decode_tensor(pk, bank, dtype=torch.float64),
+                                   m.decode_tensor(pv, bank, dtype=torch.float64), acfg)
+        assert (out - dense).abs().max().item() < 2e-3
