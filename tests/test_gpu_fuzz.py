@@ -1,0 +1,22 @@
+"""Randomised parity (tools/fuzz_parity.py): random shapes, codebook sizes, radius
+bits, Med3x multipliers, pooling, dtypes, roles and head_base; kvpack bytes and
+fp64 decode bit-exact against the oracle.  The round's evidence run covers 2000
+cases (profiles/r01g_fuzz_parity.log); this keeps 60 in the GPU suite."""
+
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_fuzz_parity(cuda):
+    res = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "fuzz_parity.py"),
+                          "--cases", "60", "--seed", "2024"], capture_output=True, text=True,
+                         timeout=900)
+    assert res.returncode == 0, (res.stdout[-3000:], res.stderr[-2000:])
+    assert "60/60 cases bit-exact" in res.stdout
