@@ -20,3 +20,15 @@ def test_fuzz_parity(cuda):
                          timeout=900)
     assert res.returncode == 0, (res.stdout[-3000:], res.stderr[-2000:])
     assert "60/60 cases bit-exact" in res.stdout
+
+
+def test_fuzz_attention(cuda):
+    """tools/fuzz_attention.py: decode / prefill / paged attention over random shapes,
+    GQA groups, causal masks, Med3x and codebook sizes within 2e-3 of the dense
+    fp64 attention over the decoded cache (1000 cases in
+    profiles/r01g_fuzz_attention.log; 80 here)."""
+    res = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "fuzz_attention.py"),
+                          "--cases", "80", "--seed", "77"], capture_output=True, text=True,
+                         timeout=900)
+    assert res.returncode == 0, (res.stdout[-3000:], res.stderr[-2000:])
+    assert "80/80 attention cases within tolerance" in res.stdout
