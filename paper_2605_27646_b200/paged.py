@@ -140,8 +140,8 @@ class PagedKVCache:
         B, HQ, TQ, D = q.shape
         if B != self.batch or TQ != 1 or D != self.head_dim or HQ % self.kv_heads:
             raise InvalidArgument(f"q shape {tuple(q.shape)} does not match the cache")
-        if max(self.lengths) == 0:
-            raise InvalidArgument("empty cache")
+        if min(self.lengths) == 0:
+            raise InvalidArgument("every sequence needs at least one cached token")
         q = q.to(device=self.device, dtype=torch.float32).contiguous()
         if out is None:
             out = torch.empty_like(q)
