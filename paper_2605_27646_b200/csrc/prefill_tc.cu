@@ -1,19 +1,19 @@
 // Prefill attention on the 5th-gen tensor cores (the
 // paper's weakest number).  Prefill reads every key many
-// times (once per 128-row query tile), so the compressed K / V are decoded
-// ONCE into an fp16 workspace by the HBM-bound decode kernels and this kernel
-// runs flash attention over them:
-//
-//   CTA = 128 query rows ((128 / g) query tokens x the g query heads of one
-//   kv head) = 4 warps = the 128 TMEM lanes; per 64-key tile
-//     K tile -> smem (UMMA K-major canonical layout), S = Q K^T:
-//       tcgen05.mma kind::f16, M=128, N=64, 8 x K=16 steps, fp32 S in TMEM
-//     each thread owns one row: tcgen05.ld its 64 scores, causal mask,
-//       online softmax in the log2 domain, O (fp32, TMEM) rescaled in place
-//       (tcgen05.ld / st) when the row max grows, P -> smem fp16 (K-major)
-//     V tile -> smem (MN-major: rows of V are already dim-contiguous),
-//       O += P V: M=128, N=128, 4 x K=16 steps into the TMEM accumulator
-//   descriptors SWIZZLE_NONE, one thread issues, tcgen05.commit -> mbarrier.
+// times (once per query tile), so the compressed K / V are decoded ONCE into
+// an fp16 workspace by the HBM-bound decode kernels, rearranged into the UMMA
+// canonical tile layouts (fa_tile_kernel), and flash attention runs over them
+// with hand-written tcgen05 MMAs (SWIZZLE_NONE descriptors, one issuing
+// thread, tcgen05.commit -> mbarrier, fp32 S and O in TMEM, P written back to
+// TMEM as the A operand of the PV MMA).  Four kernels, picked by key count
+// (launch_prefill_tc; HQMQ_FA_VARIANT forces one):
+//   attention_fa4_kernel  default from 4096 keys: 128-key tiles, two CTAs per
+//                         SM, each a sequential S -> softmax -> PV pipeline
+//   attention_fa2_kernel  default below: 64-key tiles, two query tiles per CTA,
+//                         double-buffered S, TMA producer warps
+//   attention_fa3_kernel  128-key tiles, one CTA per SM, three S buffers
+//   attention_fa_tc_kernel  the first, 4-warp version (cp.async, P via smem)
+// Design notes and measurements: DESIGN.md §4 (prefill attention).
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
