@@ -236,7 +236,7 @@ int hqmq_attention_decode(const hqmq_attention_args* args, void* stream);
  * page_tokens*index_bits index words, page_tokens*radius_bits radius words,
  * page_tokens fp16 scales.  block_table[(b*kv_heads + h)*max_pages + i] is the
  * page id holding tokens [128 i, 128 i + 128) of row (b, h); kv_lens[b] is
- * sequence b's cache length (<= max_kv_tokens).  One query token per
+ * sequence b's cache length (1 <= kv_lens[b] <= max_kv_tokens).  One query token per
  * sequence; all cached keys visible.  Same numerics as hqmq_attention_decode. */
 typedef struct {
   const uint32_t* index_pages;  /* [num_pages][page_tokens*index_bits] */
