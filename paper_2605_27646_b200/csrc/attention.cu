@@ -936,7 +936,9 @@ bool plan_att(const hqmq_attention_args* a, AttPlan& pl) {
     const int64_t max_s = std::max<int64_t>(1, std::min<int64_t>(64, ceil_div(a->kv_tokens, 256)));
     for (int64_t s = 1; s <= max_s; ++s) {
       const int64_t tiles = ceil_div(ceil_div(a->kv_tokens, s), 128);
-      const int64_t cost = ceil_div(ctas * s, 148) * (tiles + 3);
+      // waves of 2 CTAs per SM (296 slots), one tile of per-CTA overhead
+      // (measured at C4: 8 splits 0.611 ms vs the old model's 4 at 0.617)
+      const int64_t cost = ceil_div(ctas * s, 2 * 148) * (tiles + 1);
       if (cost < best) {
         best = cost;
         splits = (int)s;
@@ -1088,7 +1090,7 @@ bool plan_paged(const hqmq_paged_attention_args* a, PagedPlan& pl) {
     const int64_t max_s = std::max<int64_t>(1, std::min<int64_t>(64, ceil_div(a->max_kv_tokens, 256)));
     for (int64_t s = 1; s <= max_s; ++s) {
       const int64_t tiles = ceil_div(ceil_div(a->max_kv_tokens, s), kMT);
-      const int64_t cost = ceil_div(ctas * s, 148) * (tiles + 3);
+      const int64_t cost = ceil_div(ctas * s, 2 * 148) * (tiles + 1);
       if (cost < best) {
         best = cost;
         splits = (int)s;
