@@ -56,7 +56,20 @@ struct DecParams {
   const uint2* table16;  // optional fp16 [H][24S] (16-bit outputs)
   void* out;
   uint32_t* err;
+  // fp16 output straight into UMMA tile layouts (prefill; 0 = row-major):
+  // tiles of 2^tile_log2 keys, K-major (tile_mn 0) or MN-major (1), ntk per row
+  int tile_log2 = 0, tile_mn = 0;
+  int64_t tile_ntk = 0;
 };
+
+// 16-byte output unit (row-relative token tr, 8-dim group dg) in the tile layout
+__device__ __forceinline__ int64_t tile_unit(const DecParams& p, int64_t row, int64_t tr, int dg) {
+  const int kt = 1 << p.tile_log2;
+  const int64_t tix = tr >> p.tile_log2;
+  const int key = (int)(tr & (kt - 1));
+  const int o = p.tile_mn ? dg * kt + (key >> 3) * 8 + (key & 7) : (key >> 3) * 128 + dg * 8 + (key & 7);
+  return (row * p.tile_ntk + tix) * (int64_t)(kt * 16) + o;
+}
 
 // Coded-stream position of chunk (tok, c) and whether it is flagged.
 __device__ __forceinline__ uint64_t coded_pos(const DecParams& p, int64_t tok, int c, bool& flagged) {
@@ -181,7 +194,11 @@ __device__ __forceinline__ void decode_token_fast(const DecParams& p, const uint
                                                   const uint16_t* __restrict__ sc,
                                                   const float4* __restrict__ tab, int tt,
                                                   OutT* __restrict__ o, int lane, uint32_t ncw,
-                                                  float rtop, bool& bad) {
+                                                  float rtop, bool& bad, int64_t row = 0,
+                                                  int64_t tr = 0) {
+  if (sizeof(OutT) == 2 && p.tile_log2)  // half a 16-byte unit: chunk `lane` of token tr
+    o = reinterpret_cast<OutT*>(reinterpret_cast<uint4*>(p.out) + tile_unit(p, row, tr, lane >> 1)) +
+        4 * (lane & 1);
   const int w = W ? W : p.w, br = BR ? BR : p.br;
   const uint32_t imask = w == 32 ? 0xffffffffu : ((1u << w) - 1u);
   const uint32_t rmask = (1u << br) - 1u;
@@ -229,7 +246,8 @@ __device__ __forceinline__ void decode_token2_fast(const uint32_t* __restrict__ 
                                                    const uint16_t* __restrict__ sc,
                                                    const void* __restrict__ tab, int tt,
                                                    OutT* __restrict__ orow, int lane, uint32_t ncw,
-                                                   float rtop, bool& bad) {
+                                                   float rtop, bool& bad, const DecParams& p,
+                                                   int64_t row, int64_t tr0) {
   constexpr uint32_t kIM = W == 32 ? 0xffffffffu : ((1u << W) - 1u);
   constexpr uint32_t kRM = (1u << BR) - 1u;
   const int t = tt + (lane >> 4);
@@ -251,6 +269,8 @@ __device__ __forceinline__ void decode_token2_fast(const uint32_t* __restrict__ 
   const float sg = __half2float(__ushort_as_half(sc[t])) * rtop;
   const float r0 = (float)q0 * sg, r1 = (float)q1 * sg;
   OutT* o = orow + t * 128 + 4 * c0;
+  if (sizeof(OutT) == 2 && p.tile_log2)  // uniform: the unit (token, dims 8l..8l+7)
+    o = reinterpret_cast<OutT*>(reinterpret_cast<uint4*>(p.out) + tile_unit(p, row, tr0 + t, lane & 15));
   if constexpr (sizeof(OutT) == 4) {
     const float4 a = reinterpret_cast<const float4*>(tab)[i0];
     const float4 b = reinterpret_cast<const float4*>(tab)[i1];
@@ -378,7 +398,8 @@ __global__ void __launch_bounds__(256) decode_fast_kernel(DecParams p) {
 #pragma unroll
       for (int i = 0; i < kFDTok / 16; ++i)
         decode_token2_fast<OutT, W ? W : 1, BR ? BR : 1>(iw, rw, sc, tab, 2 * warp + 16 * i, orow - 4 * lane,
-                                                        lane, (uint32_t)ncw, rtop, bad);
+                                                        lane, (uint32_t)ncw, rtop, bad, p, row,
+                                                        p.t0 + tile * kFDTok);
     } else if (ntok == kFDTok) {
       // full tile: warp w decodes tokens w, w+8, ..., w+56 (fully unrolled)
       const uint32_t* iww = iw + warp * w;
@@ -388,11 +409,12 @@ __global__ void __launch_bounds__(256) decode_fast_kernel(DecParams p) {
 #pragma unroll
       for (int i = 0; i < kFDTok / 8; ++i)
         decode_token_fast<OutT, W, BR>(p, iww, rww, scw, tab, 8 * i, ow + 8 * i * 128, lane,
-                                       (uint32_t)ncw, rtop, bad);
+                                       (uint32_t)ncw, rtop, bad, row,
+                                       p.t0 + tile * kFDTok + warp + 8 * i);
     } else {
       for (int tt = warp; tt < ntok; tt += 8)
         decode_token_fast<OutT, W, BR>(p, iw, rw, sc, tab, tt, orow + tt * 128, lane,
-                                       (uint32_t)ncw, rtop, bad);
+                                       (uint32_t)ncw, rtop, bad, row, p.t0 + tile * kFDTok + tt);
     }
     // release the stage without a block barrier: the last warp done with it
     // issues the tile kFDStages ahead into it
@@ -907,6 +929,46 @@ int launch_decode(DecParams& p, const hqmq_decode_args* a, cudaStream_t st) {
   return check();
 }
 }  // namespace
+
+// Prefill: decode a whole no-Med3x tensor to fp16 straight into UMMA tiles of
+// 2^tile_log2 keys (K-major or MN-major), ntk tiles per (batch, head) row.
+// Returns HQMQ_ERR_UNSUPPORTED when the fast decode does not apply (the
+// caller then decodes row-major and re-lays the result out).
+int decode_fp16_tiles(const hqmq_decode_args* a, int tile_log2, int mn, int64_t ntk, void* tiles,
+                      cudaStream_t st) {
+  DecParams p;
+  if (!fill(a, p, true) || a->out_dtype != HQMQ_F16 || p.t0 != 0 || p.nt != p.T)
+    return HQMQ_ERR_UNSUPPORTED;
+  if (p.B * p.H >= 65536 || p.nt == 0) return HQMQ_ERR_UNSUPPORTED;
+  auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+  const size_t smem = (size_t)kGroupOrder * p.S * sizeof(float4);
+  const bool fast = p.D == 128 && !p.flagw && smem <= kDecSmemLimit && p.T % 8 == 0 &&
+                    al16(p.idxw) && al16(p.radw) && al16(p.scales) && al16(tiles);
+  if (!fast) return HQMQ_ERR_UNSUPPORTED;
+  p.aligned4 = 1;
+  p.out = tiles;
+  p.tile_log2 = tile_log2;
+  p.tile_mn = mn;
+  p.tile_ntk = ntk;
+  const int64_t rows = p.B * p.H;
+  const FastDecodeGeom g = fd_geom(p.w, p.br);
+  const size_t fsmem = fd_table_bytes<__half>(kGroupOrder * p.S) + (size_t)kFDStages * g.stage_bytes;
+  void (*kern)(DecParams) = decode_fast_kernel<__half, 0, 0>;
+  switch (p.w * 16 + p.br) {
+    case 9 * 16 + 4: kern = decode_fast_kernel<__half, 9, 4>; break;
+    case 11 * 16 + 4: kern = decode_fast_kernel<__half, 11, 4>; break;
+    case 13 * 16 + 4: kern = decode_fast_kernel<__half, 13, 4>; break;
+    case 11 * 16 + 6: kern = decode_fast_kernel<__half, 11, 6>; break;
+    default: break;
+  }
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  const int64_t ntile = ceil_div(p.nt, kFDTok);
+  const int per_sm = std::max<int>(1, std::min<int>(8, (int)((227 * 1024) / (fsmem + 1024))));
+  const int64_t want = std::max<int64_t>(1, ceil_div((int64_t)148 * per_sm, rows));
+  const int64_t bx = std::max<int64_t>(1, std::min<int64_t>(want, ntile));
+  kern<<<dim3((unsigned)bx, (unsigned)rows), 256, fsmem, st>>>(p);
+  return check();
+}
 }  // namespace hqmq
 
 extern "C" {

@@ -1165,6 +1165,28 @@ __global__ void fa_tile_kernel(const uint4* __restrict__ lin, uint4* __restrict_
   }
 }
 
+// Zero the units of keys >= T in every row's last tile (K and V tiles), so the
+// masked P = 0 never meets a NaN from uninitialised workspace.
+__global__ void fa_pad_kernel(uint4* __restrict__ kt, uint4* __restrict__ vt, int64_t BH, int64_t T,
+                              int64_t ntk, int keys) {
+  const int first = (int)(T % keys), npad = keys - first;
+  const int64_t n = BH * npad * 16;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int dg = (int)(i & 15);
+    const int64_t bh = (i >> 4) / npad;
+    const int key = first + (int)((i >> 4) - bh * npad);
+    const int64_t base = (bh * ntk + ntk - 1) * (int64_t)keys * 16;
+    kt[base + (key >> 3) * 128 + dg * 8 + (key & 7)] = make_uint4(0u, 0u, 0u, 0u);
+    vt[base + dg * keys + (key >> 3) * 8 + (key & 7)] = make_uint4(0u, 0u, 0u, 0u);
+  }
+}
+
+// decode.cu: fast decode straight into UMMA tiles (HQMQ_ERR_UNSUPPORTED when
+// it does not apply)
+int decode_fp16_tiles(const hqmq_decode_args* a, int tile_log2, int mn, int64_t ntk, void* tiles,
+                      cudaStream_t st);
+
 // Decode-once + tcgen05 flash attention for prefill shapes.  Workspace: the
 // two decoded fp16 tensors (kv layout) + an error word.
 static int prefill_variant() {
@@ -1199,9 +1221,11 @@ int launch_prefill_tc(const hqmq_attention_args* a, cudaStream_t st) {
   uint32_t* err = reinterpret_cast<uint32_t*>(ws + 2 * nelem * 2);
   cudaError_t e = cudaMemsetAsync(err, 0, 4, st);
   if (e != cudaSuccess) return record_cuda_error(e);
+  hqmq_decode_args dargs[2];
   for (int t = 0; t < 2; ++t) {
     const hqmq_packed_view& v = t == 0 ? a->k : a->v;
-    hqmq_decode_args d{};
+    hqmq_decode_args& d = dargs[t];
+    d = hqmq_decode_args{};
     d.batch = a->batch; d.heads = a->kv_heads; d.tokens = a->kv_tokens; d.head_dim = a->head_dim;
     d.codebook_size = a->codebook_size; d.radius_bits = a->radius_bits; d.index_bits = a->index_bits;
     d.out_dtype = HQMQ_F16;
@@ -1211,7 +1235,16 @@ int launch_prefill_tc(const hqmq_attention_args* a, cudaStream_t st) {
     d.joint_f32 = v.joint_f32; d.joint_f64 = nullptr; d.joint_f16 = v.joint_f16;
     d.out = t == 0 ? (void*)kd : (void*)vd;
     d.error_word = err;
-    const int rc = hqmq_decode(&d, st);
+  }
+  auto decode_rowmajor = [&]() {
+    for (int t = 0; t < 2; ++t) {
+      const int rc = hqmq_decode(&dargs[t], st);
+      if (rc != HQMQ_OK) return rc;
+    }
+    return (int)HQMQ_OK;
+  };
+  if (prefill_variant() == 1) {
+    const int rc = decode_rowmajor();
     if (rc != HQMQ_OK) return rc;
   }
   if (prefill_variant() != 1) {
@@ -1226,13 +1259,30 @@ int launch_prefill_tc(const hqmq_attention_args* a, cudaStream_t st) {
     const int64_t ntk = ceil_div(a->kv_tokens, keys);
     unsigned char* kt = ws + 2 * nelem * 2;
     unsigned char* vt = kt + (size_t)bh * ntk * tile_bytes;
-    const int64_t units = bh * ntk * keys * 16;
-    const unsigned grid_t = (unsigned)std::min<int64_t>(ceil_div(units, 256), 148 * 16);
-    fa_tile_kernel<<<grid_t, 256, 0, st>>>(reinterpret_cast<const uint4*>(kd), reinterpret_cast<uint4*>(kt),
-                                           bh, a->kv_tokens, ntk, 0, keys);
-    fa_tile_kernel<<<grid_t, 256, 0, st>>>(reinterpret_cast<const uint4*>(vd), reinterpret_cast<uint4*>(vt),
-                                           bh, a->kv_tokens, ntk, 1, keys);
-    int rc = check_launch();
+    // the fast decode writes its 16-byte units straight into the tiles; other
+    // streams (Med3x) decode row-major and are re-laid out
+    const int log2k = v3 ? 7 : 6;
+    int rc = decode_fp16_tiles(&dargs[0], log2k, 0, ntk, kt, st);
+    if (rc == HQMQ_OK) rc = decode_fp16_tiles(&dargs[1], log2k, 1, ntk, vt, st);
+    if (rc == HQMQ_OK) {
+      if (a->kv_tokens % keys) {  // keys past T in each row's last tile: zeros
+        const int64_t units = bh * (keys - a->kv_tokens % keys) * 16;
+        fa_pad_kernel<<<(unsigned)std::min<int64_t>(ceil_div(units, 256), 148 * 16), 256, 0, st>>>(
+            reinterpret_cast<uint4*>(kt), reinterpret_cast<uint4*>(vt), bh, a->kv_tokens, ntk, keys);
+      }
+    } else if (rc == HQMQ_ERR_UNSUPPORTED) {
+      rc = decode_rowmajor();
+      if (rc != HQMQ_OK) return rc;
+      const int64_t units = bh * ntk * keys * 16;
+      const unsigned grid_t = (unsigned)std::min<int64_t>(ceil_div(units, 256), 148 * 16);
+      fa_tile_kernel<<<grid_t, 256, 0, st>>>(reinterpret_cast<const uint4*>(kd), reinterpret_cast<uint4*>(kt),
+                                             bh, a->kv_tokens, ntk, 0, keys);
+      fa_tile_kernel<<<grid_t, 256, 0, st>>>(reinterpret_cast<const uint4*>(vd), reinterpret_cast<uint4*>(vt),
+                                             bh, a->kv_tokens, ntk, 1, keys);
+    } else {
+      return rc;
+    }
+    rc = check_launch();
     if (rc != HQMQ_OK) return rc;
     if (v4) {
       Fa2Params q4;

@@ -1,6 +1,7 @@
 """Randomised attention parity: fused_attend (decode steps, chunked / full prefill,
 causal or not, GQA groups 1-8, Med3x or not, S in {16, 64, 256}) against the dense
-fp64 attention over the decoded cache (attention.py:80-101), tolerance 2e-3; for
+fp64 attention over the decoded cache (attention.py:80-101), tolerance 2e-3 (relative
+to |out| where that exceeds 1: fp16 P and V); for
 decode steps without Med3x also the paged cache (same tolerance).
 
     python tools/fuzz_attention.py --cases 100 --seed 1
@@ -39,9 +40,13 @@ def one(rs, dev):
     out = m.fused_attend(q, pk, pv, bank, acfg)
     dense = m.reference_attend(q, m.decode_tensor(pk, bank, dtype=torch.float64),
                                m.decode_tensor(pv, bank, dtype=torch.float64), acfg)
-    err = (out.double() - dense).abs().max().item()
-    desc = f"S={S} C={C} B={B} Hkv={HKV} g={g} Tq={TQ} Tkv={TK} causal={causal}: err {err:.2e}"
-    if not err < 2e-3:
+    # fp16 P and V: a row that sees few keys returns ~v rounded to fp16, so the
+    # bound is 2e-3 relative to |out| where that exceeds 1 (Med3x payload rows)
+    diff = (out.double() - dense).abs()
+    err = diff.max().item()
+    rel = (diff / dense.abs().clamp_min(1.0)).max().item()
+    desc = f"S={S} C={C} B={B} Hkv={HKV} g={g} Tq={TQ} Tkv={TK} causal={causal}: err {err:.2e} (scaled {rel:.2e})"
+    if not rel < 2e-3:
         return False, desc
     if decode and C is None and g <= 8:
         cache = m.PagedKVCache(cfg, B, HKV, TK, bank=bank, device=dev,
@@ -52,7 +57,7 @@ def one(rs, dev):
         if cut < TK:
             cache.append(k[:, :, cut:], v[:, :, cut:])
         paged = cache.attend(q)
-        perr = (paged.double() - dense).abs().max().item()
+        perr = ((paged.double() - dense).abs() / dense.abs().clamp_min(1.0)).max().item()
         d = (paged - out).abs().max().item()
         # the contiguous call may take another kernel (fp32 CUDA-core when
         # T_kv % 8 != 0) or another split of the keys, so only the tolerance
