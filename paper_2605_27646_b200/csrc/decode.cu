@@ -188,7 +188,7 @@ __host__ __device__ inline FastDecodeGeom fd_geom(int w, int br) {
 // from p): the lane's bit offsets inside a token are then constants, and the
 // token stride (W words of index codes, BR words of radius codes) folds into
 // immediate load offsets when the caller unrolls over tokens.
-template <typename OutT, int W, int BR>
+template <typename OutT, int W, int BR, bool kTile = false>
 __device__ __forceinline__ void decode_token_fast(const DecParams& p, const uint32_t* __restrict__ iw,
                                                   const uint32_t* __restrict__ rw,
                                                   const uint16_t* __restrict__ sc,
@@ -196,7 +196,7 @@ __device__ __forceinline__ void decode_token_fast(const DecParams& p, const uint
                                                   OutT* __restrict__ o, int lane, uint32_t ncw,
                                                   float rtop, bool& bad, int64_t row = 0,
                                                   int64_t tr = 0) {
-  if (sizeof(OutT) == 2 && p.tile_log2)  // half a 16-byte unit: chunk `lane` of token tr
+  if constexpr (sizeof(OutT) == 2 && kTile)  // half a 16-byte unit: chunk `lane` of token tr
     o = reinterpret_cast<OutT*>(reinterpret_cast<uint4*>(p.out) + tile_unit(p, row, tr, lane >> 1)) +
         4 * (lane & 1);
   const int w = W ? W : p.w, br = BR ? BR : p.br;
@@ -240,7 +240,7 @@ __device__ __forceinline__ void decode_token_fast(const DecParams& p, const uint
 // Two tokens per warp instruction (compile-time W / BR only): half-warp h
 // takes token tt + h, lane l = lane & 15 decodes chunks 2l and 2l+1, so one
 // pair of code loads feeds two chunks and the row store is 16 bytes per lane.
-template <typename OutT, int W, int BR>
+template <typename OutT, int W, int BR, bool kTile = false>
 __device__ __forceinline__ void decode_token2_fast(const uint32_t* __restrict__ iw,
                                                    const uint32_t* __restrict__ rw,
                                                    const uint16_t* __restrict__ sc,
@@ -269,7 +269,7 @@ __device__ __forceinline__ void decode_token2_fast(const uint32_t* __restrict__ 
   const float sg = __half2float(__ushort_as_half(sc[t])) * rtop;
   const float r0 = (float)q0 * sg, r1 = (float)q1 * sg;
   OutT* o = orow + t * 128 + 4 * c0;
-  if (sizeof(OutT) == 2 && p.tile_log2)  // uniform: the unit (token, dims 8l..8l+7)
+  if constexpr (sizeof(OutT) == 2 && kTile)  // the unit (token, dims 8l..8l+7)
     o = reinterpret_cast<OutT*>(reinterpret_cast<uint4*>(p.out) + tile_unit(p, row, tr0 + t, lane & 15));
   if constexpr (sizeof(OutT) == 4) {
     const float4 a = reinterpret_cast<const float4*>(tab)[i0];
@@ -312,7 +312,7 @@ __host__ __device__ inline size_t fd_table_bytes(int ncw) {
   return (b + 127) / 128 * 128;
 }
 
-template <typename OutT, int W, int BR>
+template <typename OutT, int W, int BR, bool kTile = false>
 __global__ void __launch_bounds__(256) decode_fast_kernel(DecParams p) {
   extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ __align__(8) uint64_t full[kFDStages];
@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(256) decode_fast_kernel(DecParams p) {
       // (2w, 2w+1), (2w+16, 2w+17), ... (fully unrolled)
 #pragma unroll
       for (int i = 0; i < kFDTok / 16; ++i)
-        decode_token2_fast<OutT, W ? W : 1, BR ? BR : 1>(iw, rw, sc, tab, 2 * warp + 16 * i, orow - 4 * lane,
+        decode_token2_fast<OutT, W ? W : 1, BR ? BR : 1, kTile>(iw, rw, sc, tab, 2 * warp + 16 * i, orow - 4 * lane,
                                                         lane, (uint32_t)ncw, rtop, bad, p, row,
                                                         p.t0 + tile * kFDTok);
     } else if (ntok == kFDTok) {
@@ -408,13 +408,13 @@ __global__ void __launch_bounds__(256) decode_fast_kernel(DecParams p) {
       OutT* ow = orow + warp * 128;
 #pragma unroll
       for (int i = 0; i < kFDTok / 8; ++i)
-        decode_token_fast<OutT, W, BR>(p, iww, rww, scw, tab, 8 * i, ow + 8 * i * 128, lane,
+        decode_token_fast<OutT, W, BR, kTile>(p, iww, rww, scw, tab, 8 * i, ow + 8 * i * 128, lane,
                                        (uint32_t)ncw, rtop, bad, row,
                                        p.t0 + tile * kFDTok + warp + 8 * i);
     } else {
       for (int tt = warp; tt < ntok; tt += 8)
-        decode_token_fast<OutT, W, BR>(p, iw, rw, sc, tab, tt, orow + tt * 128, lane,
-                                       (uint32_t)ncw, rtop, bad, row, p.t0 + tile * kFDTok + tt);
+        decode_token_fast<OutT, W, BR, kTile>(p, iw, rw, sc, tab, tt, orow + tt * 128, lane,
+                                              (uint32_t)ncw, rtop, bad, row, p.t0 + tile * kFDTok + tt);
     }
     // release the stage without a block barrier: the last warp done with it
     // issues the tile kFDStages ahead into it
@@ -953,12 +953,12 @@ int decode_fp16_tiles(const hqmq_decode_args* a, int tile_log2, int mn, int64_t 
   const int64_t rows = p.B * p.H;
   const FastDecodeGeom g = fd_geom(p.w, p.br);
   const size_t fsmem = fd_table_bytes<__half>(kGroupOrder * p.S) + (size_t)kFDStages * g.stage_bytes;
-  void (*kern)(DecParams) = decode_fast_kernel<__half, 0, 0>;
+  void (*kern)(DecParams) = decode_fast_kernel<__half, 0, 0, true>;
   switch (p.w * 16 + p.br) {
-    case 9 * 16 + 4: kern = decode_fast_kernel<__half, 9, 4>; break;
-    case 11 * 16 + 4: kern = decode_fast_kernel<__half, 11, 4>; break;
-    case 13 * 16 + 4: kern = decode_fast_kernel<__half, 13, 4>; break;
-    case 11 * 16 + 6: kern = decode_fast_kernel<__half, 11, 6>; break;
+    case 9 * 16 + 4: kern = decode_fast_kernel<__half, 9, 4, true>; break;
+    case 11 * 16 + 4: kern = decode_fast_kernel<__half, 11, 4, true>; break;
+    case 13 * 16 + 4: kern = decode_fast_kernel<__half, 13, 4, true>; break;
+    case 11 * 16 + 6: kern = decode_fast_kernel<__half, 11, 6, true>; break;
     default: break;
   }
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
