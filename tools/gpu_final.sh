@@ -16,6 +16,6 @@ timeout 900 ncu --set full --clock-control none --import-source on \
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:'radix_hist|decode_flag' -c 4 \
    -o gpurun_out/prof_med3x -f python tools/prof_unit.py --reps 1 --outlier --attn-batch 0 > gpurun_out/prof_med3x.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:'attention_fa' -c 1 \
-   -o gpurun_out/prof_fa2 -f python tools/prefill_prof.py > gpurun_out/prof_fa2.log 2>&1
+   -o gpurun_out/prof_prefill -f python tools/prefill_prof.py > gpurun_out/prof_prefill.log 2>&1
 timeout 300 python tools/prefill_bench.py > gpurun_out/prefill.log 2>&1
 echo done
