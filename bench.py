@@ -789,7 +789,7 @@ def main():
     ap.add_argument("--attn-tokens", type=int, nargs="+", default=[32768, 131072])
     ap.add_argument("--graph", default="auto", choices=["auto", "on", "off"],
                     help="replay each step as a captured CUDA graph (auto: units < 4M chunks)")
-    ap.add_argument("--streams", type=int, default=2,
+    ap.add_argument("--streams", type=int, default=6,
                     help="CUDA streams the units rotate over inside the timed region")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-step-seconds", type=float, default=4.0)
