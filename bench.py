@@ -6,13 +6,20 @@
 
 A step = encode + decode of every (layer, role) unit this rank owns, inputs
 resident in HBM (synthetic fp16 KV of the named model shape, seeded per
-unit).  Default workload c2 = BASELINE configs[1]: Llama-3-8B full cache
-(32 layers x K,V x 8 KV heads x 32768 tokens x 128), S=64, b_r=4, encode+decode
-on one B200.  Multi-GPU (torchrun, one rank per GPU): units are independent,
-so every rank runs its own full cache (weak scaling) with no data-path
-collective; NCCL only reduces the timing (max over ranks) and gathers stats.
-c5 (Llama-3-70B 128k, S=256) instead shards its 160 units across ranks
-(strong scaling).
+unit).  Default workload at N = 1: c2 = BASELINE configs[1], Llama-3-8B full
+cache (32 layers x K,V x 8 KV heads x 32768 tokens x 128), S=64, b_r=4,
+encode+decode on one B200.  Default at N > 1: c5 = the north-star config,
+Llama-3-70B 128k cache (80 layers x K,V), S=256, its 160 (layer, role) units
+sharded across ranks in contiguous layer blocks (strong scaling; the N = 1
+point of that curve is `--workload c5`).  Units are independent (the Med3x
+median pools one (layer, role) call, codec.py:208-219), so there is no
+data-path collective: NCCL only reduces the timing (max over ranks) and
+all-gathers per-rank statistics after the timed region.
+
+Multi-GPU: one process per GPU.  Under torchrun the ranks come from the
+environment (WORLD_SIZE must equal --gpus); `python bench.py --gpus N`
+without WORLD_SIZE re-launches itself under torch.distributed.run with N
+ranks on 127.0.0.1.
 
 Rank 0 prints ONE JSON line.  Extra keys: encode/decode split, roofline of
 the encode kernel (FP32 pipe; W_enc = 20*S lane-ops per chunk)
@@ -53,6 +60,11 @@ WORKLOADS = {
                     "b_r=4, sharded by layer",
                layers=80, batch=1, heads=8, tokens=131072, head_dim=128, S=256, br=4, C=None,
                profile="gauss", shard="strong"),
+    # test-sized c5 (the multi-rank GPU test): same codec config, 8 layers x 8192 tokens
+    "c5s": dict(desc="c5 codec config at test size, 8 layers x 8 KV heads x 8192 x 128, S=256, "
+                     "b_r=4, sharded by layer",
+                layers=8, batch=1, heads=8, tokens=8192, head_dim=128, S=256, br=4, C=None,
+                profile="gauss", shard="strong"),
 }
 
 
@@ -62,6 +74,23 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return world, rank, local
+
+
+def self_launch(argv, n):
+    """Re-run this script under torch.distributed.run with n ranks (one per
+    GPU) when --gpus N > 1 is given outside torchrun; returns its exit code."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port),
+           os.path.abspath(__file__), *argv]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    return subprocess.call(cmd, env=env)
 
 
 class ClockSampler:
@@ -191,9 +220,12 @@ def run_ours(args, wl, world, rank, local):
         import torch.distributed as dist
 
         if backend == "nccl":
+            os.environ.setdefault("NCCL_DEBUG", "INFO")  # the init lines name nranks
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
+        assert dist.get_world_size() == world
 
     def all_reduce(t, op=None):
         """all_reduce on the backend's device (gloo: via host memory)."""
@@ -364,6 +396,7 @@ def run_ours(args, wl, world, rank, local):
             stop.record(cur)
             torch.cuda.synchronize()
             elapsed_ms = start.elapsed_time(stop)
+    rank_stats = None
     if world > 1:
         t = torch.tensor([elapsed_ms, enc_ms, dec_ms], device=dev)
         all_reduce(t, op=dist.ReduceOp.MAX)
@@ -371,6 +404,15 @@ def run_ours(args, wl, world, rank, local):
         units_total = torch.tensor([len(units)], device=dev)
         all_reduce(units_total)
         total_units = int(units_total.item())
+        # off the hot path: every rank's units, fixups and kvpack-section
+        # digest of its first unit, all-gathered (shard.gather_stats)
+        from paper_2605_27646_b200.shard import gather_stats
+        import hashlib
+
+        first = hashlib.sha256(b"".join(qts[0].section_bytes())).hexdigest()[:16]
+        rank_stats = gather_stats({"rank": rank, "device": torch.cuda.get_device_name(dev),
+                                   "layers": [units[0][0], units[-1][0]], "units": len(units),
+                                   "n_fixup": n_fix, "first_unit_digest": first})
     else:
         total_units = len(units)
     bytes_step = fp16_bytes_unit * total_units  # fp16-eq bytes all ranks process per step
@@ -486,6 +528,12 @@ def run_ours(args, wl, world, rank, local):
         "gpu_launches": launches["n"],
         "clocks": clocks,
     }
+    if rank_stats is not None:
+        result["ranks"] = rank_stats
+        result["config"]["parallelism"] = (
+            f"{wl['shard']} x{world}: " + ("contiguous layer blocks of one cache per rank"
+                                           if wl["shard"] == "strong" else "a full cache per rank")
+            + f" ({backend}; no data-path collective)")
     # free the codec working set before the side measurements
     del qts, inputs, outs
     torch.cuda.empty_cache()
@@ -781,7 +829,8 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default=None, choices=sorted(WORKLOADS),
+                    help="default: c2 at one GPU, c5 (strong scaling) at N > 1")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-attn", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -794,7 +843,13 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--ref-step-seconds", type=float, default=4.0)
     args = ap.parse_args()
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(self_launch(sys.argv[1:], args.gpus))
     world, rank, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={world} but --gpus {args.gpus}")
+    if args.workload is None:
+        args.workload = "c2" if world == 1 else "c5"
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":
         run_reference(args, wl, world, rank)

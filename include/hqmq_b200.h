@@ -130,7 +130,17 @@ typedef struct {
   size_t index_capacity_words;
   size_t radius_capacity_words;
   size_t flag_capacity_words;
+  int32_t search_path; /* hqmq_search_path: which nearest-codeword search runs on
+                          the fp16/bf16 head_dim-128 path (results are
+                          bit-identical either way; AUTO picks the faster) */
+  int32_t _pad1;
 } hqmq_encode_args;
+
+typedef enum {
+  HQMQ_SEARCH_AUTO = 0,        /* tcgen05 rotations when S % 16 == 0 and S >= 48 */
+  HQMQ_SEARCH_CUDA_CORE = 1,   /* the FFMA2 closed-form search on the CUDA cores */
+  HQMQ_SEARCH_TENSOR_CORE = 2  /* tcgen05 rotations whenever S % 16 == 0 */
+} hqmq_search_path;
 
 size_t hqmq_encode_workspace_bytes(const hqmq_encode_args* args);
 int hqmq_encode(const hqmq_encode_args* args, void* stream);
@@ -209,6 +219,7 @@ typedef struct {
   const uint32_t* token_offsets;
   const float* joint_f32;  /* [kv_heads][24*S][4] */
   const uint16_t* joint_f16; /* optional fp16 copy (NULL: converted in-kernel) */
+  const double* joint_f64;   /* [kv_heads][24*S][4]; required by precise = 2 */
 } hqmq_packed_view;
 
 typedef struct {
@@ -219,9 +230,13 @@ typedef struct {
   hqmq_packed_view k, v;
   float* out;
   int32_t num_splits; /* 0 = choose automatically */
-  int32_t precise;    /* 1: fp32 CUDA-core path (|err| <= 2e-5 vs fp64);
-                         0: fp16 tensor-core path (|err| <= 1e-3, the reference's
-                         fp32 tolerance, test_attention.py:97-102) */
+  int32_t precise;    /* 0: fp16 tensor-core path (|err| <= 1e-3, the reference's
+                         fp32 tolerance, test_attention.py:97-102);
+                         1: fp32 CUDA-core path (|err| <= 2e-5 vs fp64);
+                         2: fp64 path, the reference's default dtype
+                         (attention.py:137-145, |err| <= 1e-10 vs the dense fp64
+                         attention, test_attention.py:83-87): q and out are
+                         fp64 (double*), joint_f64 must be set */
   void* workspace;
   size_t workspace_bytes;
 } hqmq_attention_args;

@@ -18,6 +18,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "_lib", "libhqmq_b200.so")
 
 F16, BF16, F32, F64 = 0, 1, 2, 3
+SEARCH_AUTO, SEARCH_CUDA_CORE, SEARCH_TENSOR_CORE = 0, 1, 2
 DEVERR_SIGMA = 0x1
 DEVERR_INDEX = 0x2
 
@@ -42,6 +43,7 @@ class EncodeArgs(ctypes.Structure):
         ("index_capacity_words", ctypes.c_size_t),
         ("radius_capacity_words", ctypes.c_size_t),
         ("flag_capacity_words", ctypes.c_size_t),
+        ("search_path", c_i32), ("_pad1", c_i32),
     ]
 
 
@@ -65,6 +67,7 @@ class PackedView(ctypes.Structure):
         ("flag_words", c_vp), ("payloads", c_vp), ("token_offsets", c_vp),
         ("joint_f32", c_vp),
         ("joint_f16", c_vp),
+        ("joint_f64", c_vp),
     ]
 
 
@@ -184,3 +187,17 @@ def stream_handle(device=None) -> int:
     import torch
 
     return torch.cuda.current_stream(device).cuda_stream
+
+
+def launch(device, what: str, fn, *args) -> None:
+    """Call a C-ABI entry point on `device`'s current stream with `device`
+    made the thread's current CUDA device for the call (the library launches
+    on the current device, so a tensor on cuda:1 must not be driven from a
+    thread whose current device is cuda:0)."""
+    import torch
+
+    dev = torch.device(device)
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    with torch.cuda.device(dev):
+        check(fn(*args, torch.cuda.current_stream(dev).cuda_stream), what)

@@ -141,11 +141,22 @@ class QuantizedTensor:
         self._n_payload = n_payload
         self._n_fixup = None
         self._dense = None
+        self._ready = None  # CUDA event recorded on the encode's stream
 
     # ------------------------------------------------------------ sync
+    def wait(self) -> None:
+        """Order the current stream of this tensor's device after the encode
+        (a no-op when the encode ran on the same stream).  Every device
+        consumer (decode, attention, packing, append) calls it first."""
+        if self._ready is not None:
+            _torch().cuda.current_stream(self.device).wait_event(self._ready)
+
     def synchronize(self) -> "QuantizedTensor":
         """Wait for the encode, read its counters and raise its errors."""
         if self._n_coded is None:
+            if self._ready is not None:
+                self._ready.synchronize()
+            self.wait()
             meta = self._meta.cpu().tolist()
             self._n_coded, self._n_payload, self._n_fixup = int(meta[0]), int(meta[1]), int(meta[2])
             err = int(meta[3]) & 0xFFFFFFFF
@@ -188,10 +199,10 @@ class QuantizedTensor:
             q = torch.zeros(grid, dtype=torch.uint8, device=self.device)
             fl = torch.zeros(grid, dtype=torch.uint8, device=self.device)
             if s.n_chunks:
+                self.wait()
                 args = self._decode_args(0, s.tokens, nat.F32, None, None, None, None)
-                nat.check(nat.lib().hqmq_unpack(ctypes.byref(args), idx.data_ptr(), q.data_ptr(),
-                                                fl.data_ptr(), nat.stream_handle(self.device)),
-                          "hqmq_unpack")
+                nat.launch(self.device, "hqmq_unpack", nat.lib().hqmq_unpack, ctypes.byref(args),
+                           idx.data_ptr(), q.data_ptr(), fl.data_ptr())
             self._dense = (idx, q, fl.bool())
         return self._dense
 
@@ -231,6 +242,7 @@ class QuantizedTensor:
     def packed_view(self, bank: CodebookBank) -> nat.PackedView:
         tabs = bank.device_tables(self.layer, self.head_base, self.shape.heads, self.role,
                                   self.device)
+        self.wait()
         v = nat.PackedView()
         v.scales = self.scales.data_ptr()
         v.index_words = self.index_words.data_ptr()
@@ -240,6 +252,7 @@ class QuantizedTensor:
         v.token_offsets = self.token_offsets.data_ptr() if self.token_offsets is not None else None
         v.joint_f32 = tabs["joint_f32"].data_ptr()
         v.joint_f16 = tabs["joint_f16"].data_ptr()
+        v.joint_f64 = tabs["joint_f64"].data_ptr()
         return v
 
     # ---------------------------------------------------------- sections
@@ -291,11 +304,11 @@ class QuantizedTensor:
                           device=device) if ext else None
         ws = torch.empty(int(nat.lib().hqmq_pack_workspace_bytes(n)), dtype=torch.uint8,
                          device=device)
-        nat.check(nat.lib().hqmq_pack(
-            n, s.chunks_per_vector, c.index_bits, c.radius_bits, idx.data_ptr(), q.data_ptr(),
-            fl.data_ptr() if ext else None, iw.data_ptr(), rw.data_ptr(),
-            fw.data_ptr() if ext else None, tok.data_ptr() if ext else None,
-            ws.data_ptr(), ws.numel(), nat.stream_handle(device)), "hqmq_pack")
+        nat.launch(device, "hqmq_pack", nat.lib().hqmq_pack,
+                   n, s.chunks_per_vector, c.index_bits, c.radius_bits, idx.data_ptr(), q.data_ptr(),
+                   fl.data_ptr() if ext else None, iw.data_ptr(), rw.data_ptr(),
+                   fw.data_ptr() if ext else None, tok.data_ptr() if ext else None,
+                   ws.data_ptr(), ws.numel())
         sc = torch.as_tensor(np.asarray(scales, dtype=np.float16) if not torch.is_tensor(scales)
                              else scales).to(device=device, dtype=torch.float16).reshape(
                                  s.batch, s.heads, s.tokens).contiguous()
@@ -322,6 +335,35 @@ class QuantizedTensor:
 
 
 # --------------------------------------------------------------- helpers
+def same_device(a, b) -> bool:
+    """torch.device equality with an index-less 'cuda' meaning the current device."""
+    torch = _torch()
+    a, b = torch.device(a), torch.device(b)
+    if a.type != b.type:
+        return False
+    if a.type != "cuda":
+        return True
+    cur = torch.cuda.current_device()
+    return (a.index if a.index is not None else cur) == (b.index if b.index is not None else cur)
+
+
+def check_out(out, shape, dtype, device, what: str = "out") -> None:
+    """A caller-supplied output buffer must be exactly what the kernel writes:
+    a contiguous CUDA tensor of this shape and dtype on the packed tensor's
+    device (the kernels write a dense block at out.data_ptr())."""
+    torch = _torch()
+    if not torch.is_tensor(out):
+        raise InvalidArgument(f"{what} must be a torch tensor")
+    if out.dtype != dtype:
+        raise InvalidArgument(f"{what} has dtype {out.dtype}, expected {dtype}")
+    if tuple(out.shape) != tuple(shape):
+        raise InvalidArgument(f"{what} has shape {tuple(out.shape)}, expected {tuple(shape)}")
+    if not out.is_cuda or not same_device(out.device, device):
+        raise InvalidArgument(f"{what} must live on {device}, got {out.device}")
+    if not out.is_contiguous():
+        raise InvalidArgument(f"{what} must be contiguous")
+
+
 def _bank_for(config: CodecConfig, bank: CodebookBank | None) -> CodebookBank:
     """codec.py:222-229."""
     if bank is None:
@@ -349,19 +391,28 @@ def _as_device_4d(data, device):
     return data, TensorShape(*data.shape), torch.device(device)
 
 
+SEARCH_PATHS = {"auto": nat.SEARCH_AUTO, "cuda_core": nat.SEARCH_CUDA_CORE,
+                "tensor_core": nat.SEARCH_TENSOR_CORE}
+
+
 def encode_tensor(data, config: CodecConfig, layer: int = 0, role: str = "K",
                   bank: CodebookBank | None = None, head_base: int = 0, *,
-                  device=None, sync: bool = True) -> QuantizedTensor:
+                  device=None, sync: bool = True, search_path: str = "auto") -> QuantizedTensor:
     """Quantize a (batch, heads, tokens, head_dim) tensor (codec.py:232-287).
 
     Runs Med3x, the fused encode kernel and the section packing on the GPU.
     sync=True (reference semantics) waits for the kernels and raises
     InvalidArgument on a non-positive scale; sync=False returns immediately and
-    defers that check to QuantizedTensor.synchronize().
+    defers that check to QuantizedTensor.synchronize().  search_path selects
+    the nearest-codeword search of the fp16/bf16 head_dim-128 kernels
+    ("auto", "cuda_core" = FFMA2, "tensor_core" = tcgen05 rotations when
+    S % 16 == 0); every path is certified and bit-identical to the reference.
     """
     torch = _torch()
     if role not in ROLE_TAGS:
         raise InvalidArgument(f"role must be one of {sorted(ROLE_TAGS)}")
+    if search_path not in SEARCH_PATHS:
+        raise InvalidArgument(f"search_path must be one of {sorted(SEARCH_PATHS)}")
     if head_base < 0:
         raise InvalidArgument("head_base must be nonnegative")
     data, shape, device = _as_device_4d(data, device)
@@ -402,15 +453,18 @@ def encode_tensor(data, config: CodecConfig, layer: int = 0, role: str = "K",
     a.counters = meta.data_ptr()
     a.error_word = meta.data_ptr() + 24
     a.index_capacity_words, a.radius_capacity_words = iw.numel(), rw.numel()
+    a.search_path = SEARCH_PATHS[search_path]
     a.flag_capacity_words = fw.numel() if ext else 0
     L = nat.lib()
     ws_bytes = int(L.hqmq_encode_workspace_bytes(ctypes.byref(a)))
     ws = torch.empty(max(1, ws_bytes), dtype=torch.uint8, device=device)
     a.workspace, a.workspace_bytes = ws.data_ptr(), ws_bytes
-    nat.check(L.hqmq_encode(ctypes.byref(a), nat.stream_handle(device)), "hqmq_encode")
+    nat.launch(device, "hqmq_encode", L.hqmq_encode, ctypes.byref(a))
     qt = QuantizedTensor(shape, config, layer, role, head_base, scales, iw, rw, fw, pay, tok,
                          meta, device)
     qt._keepalive = (data, ws)
+    qt._ready = torch.cuda.Event()
+    qt._ready.record(torch.cuda.current_stream(device))
     if sync:
         qt.synchronize()
     return qt
@@ -434,21 +488,26 @@ def decode_token_range(packed: QuantizedTensor, bank: CodebookBank, start: int, 
     (codec.py:290-328).  dtype float64 is bit-identical to the reference;
     float32 (default) is within 1e-6 relative; float16/bfloat16 for serving."""
     torch = _torch()
-    dtype = torch.float32 if dtype is None else dtype
+    if dtype is None:
+        dtype = out.dtype if out is not None else torch.float32
     s = packed.shape
     if not 0 <= start <= stop <= s.tokens:
         raise InvalidArgument(f"token range [{start}, {stop}) out of bounds")
     code = _out_code(dtype)
     dev = packed.device
+    want = (s.batch, s.heads, stop - start, s.head_dim)
     if out is None:
-        out = torch.empty((s.batch, s.heads, stop - start, s.head_dim), dtype=dtype, device=dev)
+        out = torch.empty(want, dtype=dtype, device=dev)
+    else:
+        check_out(out, want, dtype, dev, "decode out")
     if stop == start:
         return out
     tabs = bank.device_tables(packed.layer, packed.head_base, s.heads, packed.role, dev)
+    packed.wait()
     err = torch.zeros(1, dtype=torch.int32, device=dev)
     args = packed._decode_args(start, stop, code, out, err,
                                tabs["joint_f32"], tabs["joint_f64"], tabs["joint_f16"])
-    nat.check(nat.lib().hqmq_decode(ctypes.byref(args), nat.stream_handle(dev)), "hqmq_decode")
+    nat.launch(dev, "hqmq_decode", nat.lib().hqmq_decode, ctypes.byref(args))
     if check and int(err.item()) & nat.DEVERR_INDEX:
         raise CorruptData("codeword index out of range")
     return out
@@ -509,6 +568,7 @@ def append_tokens(packed: QuantizedTensor, data, bank: CodebookBank | None = Non
         return out
 
     new.synchronize()
+    packed.wait()
     iw = cat_words(packed.index_words, new.index_words, c.index_bits)
     rw = cat_words(packed.radius_words, new.radius_words, c.radius_bits)
     scales = torch.cat([packed.scales, new.scales], dim=2).contiguous()

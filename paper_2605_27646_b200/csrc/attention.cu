@@ -38,6 +38,7 @@ struct AttView {
   const uint32_t* tokoff;
   const float4* table;  // [Hkv][24S]
   const uint2* table16;  // optional fp16 copy [Hkv][24S]
+  const double* table64;  // [Hkv][24S][4] fp64 (the fp64 path)
 };
 
 struct AttParams {
@@ -246,6 +247,200 @@ __global__ void combine_kernel(AttParams p) {
     }
     o[d] = acc / L;
   }
+}
+
+// ------------------------------------------------------------------------
+// fp64 path: fused_attend(dtype=float64), the reference's default contract
+// (attention.py:137-199, held to 1e-10 of the dense fp64 attention by
+// test_attention.py:83-87).  K/V are decoded exactly as decode_token_range
+// does (codec.py:315-325: ((q * sigma_w) / top) * codeword in fp64, payload
+// rows widened from fp16), logits, softmax (exp) and P.V run in fp64 on the
+// CUDA cores.  Same CTA geometry as attention_split_kernel: 4 query rows (one
+// warp each) of one kv head x a key range, 32-key tiles decoded into shared
+// memory once for the 4 rows; partial (m, l, o) per split merged by
+// combine_f64_kernel.  Any head_dim <= 128 (multiple of 4), Med3x included.
+constexpr int kF64Stride = 129;  // doubles per smem K row: lane = key reads conflict-free
+
+__device__ __forceinline__ void decode_chunk_f64(const AttView& v, const double* tab, int64_t tok,
+                                                 int C, int c, int w, int br, int ncw, double top,
+                                                 double (&x)[4]) {
+  const uint64_t g = (uint64_t)tok * C + c;
+  uint64_t pos = g;
+  bool fl = false;
+  if (v.flagw) {
+    fl = (__ldg(v.flagw + (g >> 5)) >> (g & 31)) & 1u;
+    uint64_t b = (uint64_t)tok * C;
+    uint32_t nflag = 0;
+    while (b < g) {
+      const uint32_t word = __ldg(v.flagw + (b >> 5));
+      const uint32_t sh = (uint32_t)(b & 31);
+      const uint64_t take = min((uint64_t)(32 - sh), g - b);
+      const uint32_t m = take == 32 ? 0xffffffffu : ((1u << take) - 1u);
+      nflag += __popc((word >> sh) & m);
+      b += take;
+    }
+    pos = (uint64_t)__ldg(v.tokoff + tok) + (uint64_t)(c - (int)nflag);
+  }
+  if (fl) {
+    const ushort4 hv = __ldg(reinterpret_cast<const ushort4*>(v.payloads) + (g - pos));
+    x[0] = (double)__half2float(__ushort_as_half(hv.x));
+    x[1] = (double)__half2float(__ushort_as_half(hv.y));
+    x[2] = (double)__half2float(__ushort_as_half(hv.z));
+    x[3] = (double)__half2float(__ushort_as_half(hv.w));
+    return;
+  }
+  uint32_t idx = read_bits(v.idxw, pos * (uint64_t)w, w);
+  const uint32_t q = read_bits(v.radw, pos * (uint64_t)br, br);
+  idx = idx < (uint32_t)ncw ? idx : 0u;
+  const double sw = (double)__half2float(__ushort_as_half(__ldg(v.scales + tok)));
+  const double rad = __ddiv_rn(__dmul_rn((double)q, sw), top);
+#pragma unroll
+  for (int i = 0; i < 4; ++i) x[i] = __dmul_rn(rad, __ldg(tab + 4 * (int64_t)idx + i));
+}
+
+struct AttParams64 {
+  const double* q;
+  double* out;
+  double* part_o;   // [B*Hkv][rows][splits][D]
+  double* part_ml;  // [B*Hkv][rows][splits][2]
+  double scale;
+};
+
+__global__ void __launch_bounds__(kAttThreads) attention_f64_kernel(AttParams p, AttParams64 p64) {
+  extern __shared__ __align__(16) double dsm[];
+  double* q_s = dsm;                          // [kRows][128]
+  double* k_s = q_s + kRows * 4 * kMaxC;      // [kKT][kF64Stride]
+  double* v_s = k_s + kKT * kF64Stride;       // [kKT][128]
+  double* p_s = v_s + kKT * 4 * kMaxC;        // [kRows][kKT]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t bh = blockIdx.y;
+  const int64_t b = bh / p.Hkv, hkv = bh % p.Hkv;
+  const int split = blockIdx.x;
+  const int row0 = blockIdx.z * kRows;
+  const int C = p.C, D = (int)p.D, ncw = kGroupOrder * p.S;
+  const double top = (double)((1 << p.br) - 1);
+  const double* ktab = p.k.table64 + (int64_t)hkv * ncw * 4;
+  const double* vtab = p.v.table64 + (int64_t)hkv * ncw * 4;
+  for (int i = tid; i < kRows * 4 * kMaxC; i += kAttThreads) {
+    const int r = i / (4 * kMaxC), d = i - r * 4 * kMaxC;
+    const int rr = row0 + r;
+    double val = 0.0;
+    if (rr < p.nrows && d < D) {
+      const int gi = rr / (int)p.Tq, qi = rr - gi * (int)p.Tq;
+      const int64_t hq = hkv * p.g + gi;
+      val = p64.q[((b * p.Hq + hq) * p.Tq + qi) * p.D + d];
+    }
+    q_s[i] = val;
+  }
+  const int64_t kbeg = (int64_t)split * p.keys_per_split;
+  const int64_t kend = min(p.Tkv, kbeg + p.keys_per_split);
+  double m_run = -INFINITY, l_run = 0.0;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  const int my_row = row0 + warp;
+  int64_t vis = p.Tkv;
+  if (my_row < p.nrows && p.causal) vis = (my_row % (int)p.Tq) + (p.Tkv - p.Tq) + 1;
+  __syncthreads();
+  for (int64_t t0 = kbeg; t0 < kend; t0 += kKT) {
+    const int nt = (int)min((int64_t)kKT, kend - t0);
+    for (int i = tid; i < nt * C; i += kAttThreads) {
+      const int tt = i / C, c = i - tt * C;
+      const int64_t tok = (b * p.Hkv + hkv) * p.Tkv + t0 + tt;
+      double x[4];
+      decode_chunk_f64(p.k, ktab, tok, C, c, p.w, p.br, ncw, top, x);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) k_s[tt * kF64Stride + 4 * c + e] = x[e];
+      decode_chunk_f64(p.v, vtab, tok, C, c, p.w, p.br, ncw, top, x);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) v_s[tt * 4 * kMaxC + 4 * c + e] = x[e];
+    }
+    __syncthreads();
+    // logits (attention.py:176): (q . k) * scale, lane = key
+    double s = -INFINITY;
+    if (my_row < p.nrows && lane < nt && t0 + lane < vis) {
+      const double* kr = k_s + lane * kF64Stride;
+      const double* qr = q_s + warp * 4 * kMaxC;
+      double a0 = 0.0, a1 = 0.0;
+      for (int d = 0; d < 4 * C; d += 2) {
+        a0 = fma(qr[d], kr[d], a0);
+        a1 = fma(qr[d + 1], kr[d + 1], a1);
+      }
+      s = (a0 + a1) * p64.scale;
+    }
+    double tmax = s;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tmax = fmax(tmax, __shfl_xor_sync(0xffffffffu, tmax, o));
+    const double m_new = fmax(m_run, tmax);
+    double pr = 0.0, alpha = 1.0;
+    if (m_new != -INFINITY) {
+      pr = s == -INFINITY ? 0.0 : exp(s - m_new);
+      alpha = m_run == -INFINITY ? 0.0 : exp(m_run - m_new);
+    }
+    double psum = pr;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) psum += __shfl_xor_sync(0xffffffffu, psum, o);
+    l_run = l_run * alpha + psum;
+    m_run = m_new;
+    p_s[warp * kKT + lane] = pr;
+    __syncwarp();
+    if (lane < C) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[e] *= alpha;
+      for (int tt = 0; tt < nt; ++tt) {
+        const double pv = p_s[warp * kKT + tt];
+        const double* vr = v_s + tt * 4 * kMaxC + 4 * lane;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[e] = fma(pv, vr[e], acc[e]);
+      }
+    }
+    __syncthreads();
+  }
+  if (my_row >= p.nrows || lane >= C) return;
+  const int gi = my_row / (int)p.Tq, qi = my_row - gi * (int)p.Tq;
+  const int64_t hq = hkv * p.g + gi;
+  if (p.splits == 1) {
+    double* o = p64.out + ((b * p.Hq + hq) * p.Tq + qi) * p.D + 4 * lane;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) o[e] = acc[e] / l_run;
+    return;
+  }
+  const int64_t pr_idx = (bh * p.nrows + my_row) * p.splits + split;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) p64.part_o[pr_idx * p.D + 4 * lane + e] = acc[e];
+  if (lane == 0) {
+    p64.part_ml[2 * pr_idx] = m_run;
+    p64.part_ml[2 * pr_idx + 1] = l_run;
+  }
+}
+
+__global__ void combine_f64_kernel(AttParams p, AttParams64 p64) {
+  const int64_t bh = blockIdx.x;
+  const int r = blockIdx.y;
+  const int64_t b = bh / p.Hkv, hkv = bh % p.Hkv;
+  const int64_t base = (bh * p.nrows + r) * p.splits;
+  double M = -INFINITY;
+  for (int s = 0; s < p.splits; ++s) M = fmax(M, p64.part_ml[2 * (base + s)]);
+  double L = 0.0;
+  for (int s = 0; s < p.splits; ++s) {
+    const double m = p64.part_ml[2 * (base + s)];
+    if (m != -INFINITY) L += p64.part_ml[2 * (base + s) + 1] * exp(m - M);
+  }
+  const int gi = r / (int)p.Tq, qi = r - gi * (int)p.Tq;
+  const int64_t hq = hkv * p.g + gi;
+  double* o = p64.out + ((b * p.Hq + hq) * p.Tq + qi) * p.D;
+  for (int d = threadIdx.x; d < p.D; d += blockDim.x) {
+    double acc = 0.0;
+    for (int s = 0; s < p.splits; ++s) {
+      const double m = p64.part_ml[2 * (base + s)];
+      if (m != -INFINITY) acc += p64.part_o[(base + s) * p.D + d] * exp(m - M);
+    }
+    o[d] = acc / L;
+  }
+}
+
+__host__ inline size_t f64_smem_bytes() {
+  return sizeof(double) *
+         ((size_t)kRows * 4 * kMaxC + (size_t)kKT * kF64Stride + (size_t)kKT * 4 * kMaxC +
+          (size_t)kRows * kKT);
 }
 
 // ------------------------------------------------------------------------
@@ -643,265 +838,6 @@ __global__ void __launch_bounds__(kMThreads, 2) attention_mma_kernel(AttParams p
 }
 
 
-// ------------------------------------------------------------------------
-// Tensor-core PREFILL path (q_tokens x GQA group > 8 rows, head_dim 128;
-// SURVEY.md §8(f) rank 3, the paper's weakest number).
-// A CTA owns 64 query rows = (64 / g) consecutive query tokens x the g query
-// heads of one kv head, so the K/V it decodes serve all 64 rows.  Per 64-key
-// tile the 4 warps decode K and V once into shared fp16 tiles (any stream
-// layout, Med3x payloads included, via decode_chunk), then each warp runs
-// flash-attention-2 on its 16 rows: S = Q K^T and O += P V on
-// mma.m16n8k16 (K rows by ldmatrix, V rows by ldmatrix.trans), causal mask,
-// online softmax in the log2 domain, P reused from the S accumulators.
-constexpr int kPR = 128;          // rows per CTA (8 warps x 16)
-constexpr int kPK = 64;           // keys per tile
-constexpr int kPStride = 136;     // halves per smem row (128 + 8: conflict-free ldmatrix)
-constexpr int kPThreads = 256;
-
-__host__ __device__ inline size_t prefill_smem_bytes(int S) {
-  return 2 * (size_t)kGroupOrder * S * sizeof(float4) + 2 * (size_t)kPK * kPStride * 2;
-}
-
-// One warp decodes one key of the tile straight from the token-aligned
-// streams (no Med3x): lane = chunk, codes from global (L2-resident: every CTA
-// of the kv head reads them), fp16 codeword gather from the smem table.
-template <int W, int BR>
-__device__ __forceinline__ uint2 prefill_fast_chunk(const AttView& v, const uint2* tab16, int64_t tok,
-                                                    int lane, uint32_t ncw, float rtop) {
-  constexpr uint32_t kIM = (1u << W) - 1u, kRM = (1u << BR) - 1u;
-  const uint32_t bi = (uint32_t)lane * W, bq = (uint32_t)lane * BR;
-  const uint32_t* ip = v.idxw + tok * W + (bi >> 5);
-  const uint32_t* qp = v.radw + tok * BR + (bq >> 5);
-  uint32_t idx = __funnelshift_r(__ldg(ip), __ldg(ip + 1), bi & 31) & kIM;
-  uint32_t q;
-  if constexpr (32 % BR == 0) q = (__ldg(qp) >> (bq & 31)) & kRM;
-  else q = __funnelshift_r(__ldg(qp), __ldg(qp + 1), bq & 31) & kRM;
-  idx = idx < ncw ? idx : 0u;
-  const float rad = (float)q * (__half2float(__ushort_as_half(__ldg(v.scales + tok))) * rtop);
-  const uint2 cw = tab16[idx];
-  const __half2 r2 = __float2half2_rn(rad);
-  const __half2 a = __hmul2(r2, *reinterpret_cast<const __half2*>(&cw.x));
-  const __half2 b = __hmul2(r2, *reinterpret_cast<const __half2*>(&cw.y));
-  return make_uint2(*reinterpret_cast<const uint32_t*>(&a), *reinterpret_cast<const uint32_t*>(&b));
-}
-
-__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* ptr) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-               : "r"(smem_u32(ptr)));
-}
-__device__ __forceinline__ void ldsm_x4_t(uint32_t (&r)[4], const void* ptr) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-               : "r"(smem_u32(ptr)));
-}
-
-template <int W, int BR>
-__global__ void __launch_bounds__(kPThreads, 1) attention_prefill_kernel(AttParams p) {
-  extern __shared__ __align__(128) unsigned char sm[];
-  const int ncw = kGroupOrder * p.S;
-  constexpr bool kFast = W > 0;  // token-aligned streams, compile-time geometry
-  float4* ktab = reinterpret_cast<float4*>(sm);
-  float4* vtab = ktab + ncw;
-  __half* ks = reinterpret_cast<__half*>(vtab + ncw);
-  __half* vs = ks + kPK * kPStride;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g4 = lane >> 2, t4 = lane & 3;
-  const int64_t bh = blockIdx.y;
-  const int64_t b = bh / p.Hkv, hkv = bh % p.Hkv;
-  const int g = p.g;
-  const int tpt = kPR / g;                         // query tokens per CTA
-  const int64_t tok0 = (int64_t)blockIdx.x * tpt;  // first query token
-  const int64_t off = p.causal ? (p.Tkv - p.Tq) : 0;
-  if (kFast) {  // fp16 tables (8-byte gathers)
-    uint2* k16 = reinterpret_cast<uint2*>(ktab);
-    uint2* v16 = reinterpret_cast<uint2*>(vtab);
-    for (int i = tid; i < ncw; i += kPThreads) {
-      const float4 a = __ldg(p.k.table + hkv * ncw + i), c = __ldg(p.v.table + hkv * ncw + i);
-      k16[i] = make_uint2(pack_half2(a.x, a.y), pack_half2(a.z, a.w));
-      v16[i] = make_uint2(pack_half2(c.x, c.y), pack_half2(c.z, c.w));
-    }
-  } else {
-    for (int i = tid; i < ncw; i += kPThreads) {
-      ktab[i] = __ldg(p.k.table + hkv * ncw + i);
-      vtab[i] = __ldg(p.v.table + hkv * ncw + i);
-    }
-  }
-  // this lane's two rows (m = g4, g4 + 8 of the warp's 16): token / head
-  int64_t qtok[2];
-  int qh[2];
-  bool rvalid[2];
-  int64_t vis[2];
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    const int r = warp * 16 + g4 + 8 * h;
-    qtok[h] = tok0 + r / g;
-    qh[h] = r % g;
-    rvalid[h] = qtok[h] < p.Tq;
-    vis[h] = p.causal ? qtok[h] + off + 1 : p.Tkv;
-  }
-  // Q A-fragments (16 rows x 128 dims, 8 k-slabs), pre-scaled by scale*log2(e)
-  uint32_t qa[8][4];
-#pragma unroll
-  for (int ks8 = 0; ks8 < 8; ++ks8) {
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      float v0 = 0.f, v1 = 0.f, v8 = 0.f, v9 = 0.f;
-      if (rvalid[h]) {
-        const float* qr = p.q + ((b * p.Hq + hkv * g + qh[h]) * p.Tq + qtok[h]) * 128 + ks8 * 16 + 2 * t4;
-        v0 = qr[0] * p.scale_log2; v1 = qr[1] * p.scale_log2;
-        v8 = qr[8] * p.scale_log2; v9 = qr[9] * p.scale_log2;
-      }
-      qa[ks8][h] = pack_half2(v0, v1);       // a0 (row g4) / a1 (row g4+8)
-      qa[ks8][2 + h] = pack_half2(v8, v9);   // a2 / a3
-    }
-  }
-  float o[16][4];
-#pragma unroll
-  for (int i = 0; i < 16; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
-  float m_run[2] = {-INFINITY, -INFINITY}, l_run[2] = {0.f, 0.f};
-  // keys needed by the CTA: up to the last (valid) token's causal limit
-  const int64_t last_tok = min(p.Tq, tok0 + tpt) - 1;
-  const int64_t kend = p.causal ? min(p.Tkv, last_tok + off + 1) : p.Tkv;
-  const float rtop = 1.0f / (float)((1 << p.br) - 1);
-  const int64_t kvrow = bh * p.Tkv;
-  __syncthreads();
-  for (int64_t k0 = 0; k0 < kend; k0 += kPK) {
-    const int nk = (int)min((int64_t)kPK, kend - k0);
-    // ---- cooperative decode of the K and V tiles (fp16, scale applied)
-    if constexpr (kFast) {
-      const uint2* k16 = reinterpret_cast<const uint2*>(ktab);
-      const uint2* v16 = reinterpret_cast<const uint2*>(vtab);
-#pragma unroll 2
-      for (int kk = warp; kk < kPK; kk += kPThreads / 32) {
-        uint2 hk = make_uint2(0u, 0u), hv = make_uint2(0u, 0u);
-        if (kk < nk) {
-          const int64_t tok = kvrow + k0 + kk;
-          hk = prefill_fast_chunk<W ? W : 1, BR ? BR : 1>(p.k, k16, tok, lane, (uint32_t)ncw, rtop);
-          hv = prefill_fast_chunk<W ? W : 1, BR ? BR : 1>(p.v, v16, tok, lane, (uint32_t)ncw, rtop);
-        }
-        *reinterpret_cast<uint2*>(ks + kk * kPStride + 4 * lane) = hk;
-        *reinterpret_cast<uint2*>(vs + kk * kPStride + 4 * lane) = hv;
-      }
-    } else
-    for (int i = tid; i < kPK * 32; i += kPThreads) {
-      const int kk = i >> 5, c = i & 31;
-      uint2 hk = make_uint2(0u, 0u), hv = make_uint2(0u, 0u);
-      if (kk < nk) {
-        const int64_t tok = kvrow + k0 + kk;
-        const float4 a = decode_chunk(p.k, ktab, tok, 32, c, p.w, p.br, ncw, rtop);
-        const float4 d = decode_chunk(p.v, vtab, tok, 32, c, p.w, p.br, ncw, rtop);
-        hk = make_uint2(pack_half2(a.x, a.y), pack_half2(a.z, a.w));
-        hv = make_uint2(pack_half2(d.x, d.y), pack_half2(d.z, d.w));
-      }
-      *reinterpret_cast<uint2*>(ks + kk * kPStride + 4 * c) = hk;
-      *reinterpret_cast<uint2*>(vs + kk * kPStride + 4 * c) = hv;
-    }
-    __syncthreads();
-    // ---- S = Q K^T for this warp's 16 rows x 64 keys
-    float sc[8][4];
-#pragma unroll
-    for (int nt = 0; nt < 8; ++nt) {
-      sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        uint32_t bf[4];
-        ldsm_x4(bf, ks + (nt * 8 + (lane & 7)) * kPStride + kk * 32 + (lane >> 3) * 8);
-        asm volatile(
-            "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
-            "{%8,%9}, {%0,%1,%2,%3};"
-            : "+f"(sc[nt][0]), "+f"(sc[nt][1]), "+f"(sc[nt][2]), "+f"(sc[nt][3])
-            : "r"(qa[2 * kk][0]), "r"(qa[2 * kk][1]), "r"(qa[2 * kk][2]), "r"(qa[2 * kk][3]),
-              "r"(bf[0]), "r"(bf[1]));
-        asm volatile(
-            "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
-            "{%8,%9}, {%0,%1,%2,%3};"
-            : "+f"(sc[nt][0]), "+f"(sc[nt][1]), "+f"(sc[nt][2]), "+f"(sc[nt][3])
-            : "r"(qa[2 * kk + 1][0]), "r"(qa[2 * kk + 1][1]), "r"(qa[2 * kk + 1][2]),
-              "r"(qa[2 * kk + 1][3]), "r"(bf[2]), "r"(bf[3]));
-      }
-    }
-    // ---- mask + online softmax (rows g4: c0,c1; g4+8: c2,c3)
-    float alpha[2];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      float mx = -INFINITY;
-#pragma unroll
-      for (int nt = 0; nt < 8; ++nt) {
-#pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int64_t key = k0 + nt * 8 + 2 * t4 + e;
-          const bool ok = rvalid[h] && key < k0 + nk && key < vis[h];
-          float& v = sc[nt][2 * h + e];
-          v = ok ? v : -INFINITY;
-          mx = fmaxf(mx, v);
-        }
-      }
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-      mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-      const float m_new = fmaxf(m_run[h], mx);
-      float ps = 0.f;
-      if (m_new == -INFINITY) {
-        alpha[h] = 1.f;
-#pragma unroll
-        for (int nt = 0; nt < 8; ++nt) sc[nt][2 * h] = sc[nt][2 * h + 1] = 0.f;
-      } else {
-        alpha[h] = exp2f(m_run[h] - m_new);
-#pragma unroll
-        for (int nt = 0; nt < 8; ++nt) {
-          sc[nt][2 * h] = exp2f(sc[nt][2 * h] - m_new);
-          sc[nt][2 * h + 1] = exp2f(sc[nt][2 * h + 1] - m_new);
-          ps += sc[nt][2 * h] + sc[nt][2 * h + 1];
-        }
-      }
-      ps += __shfl_xor_sync(0xffffffffu, ps, 1);
-      ps += __shfl_xor_sync(0xffffffffu, ps, 2);
-      l_run[h] = l_run[h] * alpha[h] + ps;
-      m_run[h] = m_new;
-    }
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      o[i][0] *= alpha[0]; o[i][1] *= alpha[0]; o[i][2] *= alpha[1]; o[i][3] *= alpha[1];
-    }
-    // ---- O += P V: P's A-fragments from the S accumulators (k-slab = 16 keys)
-#pragma unroll
-    for (int kk = 0; kk < 4; ++kk) {
-      const uint32_t a0 = pack_half2(sc[2 * kk][0], sc[2 * kk][1]);
-      const uint32_t a1 = pack_half2(sc[2 * kk][2], sc[2 * kk][3]);
-      const uint32_t a2 = pack_half2(sc[2 * kk + 1][0], sc[2 * kk + 1][1]);
-      const uint32_t a3 = pack_half2(sc[2 * kk + 1][2], sc[2 * kk + 1][3]);
-#pragma unroll
-      for (int dn = 0; dn < 16; dn += 2) {
-        uint32_t bf[4];
-        // rows = keys 16kk.., cols = dims 8dn..8dn+15 (two n-tiles), transposed
-        ldsm_x4_t(bf, vs + (kk * 16 + (lane & 15)) * kPStride + dn * 8 + (lane >> 4) * 8);
-        asm volatile(
-            "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
-            "{%8,%9}, {%0,%1,%2,%3};"
-            : "+f"(o[dn][0]), "+f"(o[dn][1]), "+f"(o[dn][2]), "+f"(o[dn][3])
-            : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(bf[0]), "r"(bf[1]));
-        asm volatile(
-            "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
-            "{%8,%9}, {%0,%1,%2,%3};"
-            : "+f"(o[dn + 1][0]), "+f"(o[dn + 1][1]), "+f"(o[dn + 1][2]), "+f"(o[dn + 1][3])
-            : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(bf[2]), "r"(bf[3]));
-      }
-    }
-    __syncthreads();  // tiles consumed before the next decode overwrites them
-  }
-  // ---- normalise and write (c0/c1: row g4, dims 8n+2t4, +1; c2/c3: row g4+8)
-#pragma unroll
-  for (int h = 0; h < 2; ++h) {
-    if (!rvalid[h]) continue;
-    const float inv = l_run[h] > 0.f ? 1.0f / l_run[h] : 0.f;
-    float* orow = p.out + ((b * p.Hq + hkv * g + qh[h]) * p.Tq + qtok[h]) * 128;
-#pragma unroll
-    for (int n = 0; n < 16; ++n)
-      *reinterpret_cast<float2*>(orow + n * 8 + 2 * t4) =
-          make_float2(o[n][2 * h] * inv, o[n][2 * h + 1] * inv);
-  }
-}
-
 size_t prefill_tc_workspace(const hqmq_attention_args* a);
 bool prefill_tc_applicable(const hqmq_attention_args* a);
 int launch_prefill_tc(const hqmq_attention_args* a, cudaStream_t st);
@@ -948,7 +884,8 @@ bool plan_att(const hqmq_attention_args* a, AttPlan& pl) {
   pl.keys_per_split = ceil_div(ceil_div(a->kv_tokens, splits), 64) * 64;
   pl.splits = (int)ceil_div(a->kv_tokens, pl.keys_per_split);
   const int64_t parts = a->batch * a->kv_heads * nrows * pl.splits;
-  pl.ws = pl.splits > 1 ? (size_t)parts * (a->head_dim + 2) * sizeof(float) + 256 : 0;
+  const size_t elt = a->precise == 2 ? sizeof(double) : sizeof(float);
+  pl.ws = pl.splits > 1 ? (size_t)parts * (a->head_dim + 2) * elt + 256 : 0;
   if (prefill_tc_applicable(a)) pl.ws = std::max(pl.ws, prefill_tc_workspace(a));
   return true;
 }
@@ -990,11 +927,31 @@ int hqmq_attention_decode(const hqmq_attention_args* a, void* stream) {
     o.payloads = v.payloads; o.tokoff = v.token_offsets;
     o.table = reinterpret_cast<const float4*>(v.joint_f32);
     o.table16 = reinterpret_cast<const uint2*>(v.joint_f16);
+    o.table64 = v.joint_f64;
     return o;
   };
   p.k = view(a->k);
   p.v = view(a->v);
   p.out = a->out;
+  if (a->precise == 2) {  // fp64 contract (attention.py:137-145 default dtype)
+    if (!a->k.joint_f64 || !a->v.joint_f64) return HQMQ_ERR_INVALID_ARGUMENT;
+    AttParams64 p64;
+    p64.q = reinterpret_cast<const double*>(a->q);
+    p64.out = reinterpret_cast<double*>(a->out);
+    double* ws64 = reinterpret_cast<double*>(a->workspace);
+    const int64_t parts64 = a->batch * a->kv_heads * p.nrows * pl.splits;
+    p64.part_o = ws64;
+    p64.part_ml = ws64 ? ws64 + parts64 * a->head_dim : nullptr;
+    p64.scale = a->scale;
+    const size_t sm64 = f64_smem_bytes();
+    cudaFuncSetAttribute(attention_f64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm64);
+    const dim3 g64((unsigned)pl.splits, (unsigned)(a->batch * a->kv_heads), (unsigned)pl.row_groups);
+    attention_f64_kernel<<<g64, kAttThreads, sm64, st>>>(p, p64);
+    int rc = check_launch();
+    if (rc != HQMQ_OK || pl.splits == 1) return rc;
+    combine_f64_kernel<<<dim3((unsigned)(a->batch * a->kv_heads), (unsigned)p.nrows), 128, 0, st>>>(p, p64);
+    return check_launch();
+  }
   float* ws = reinterpret_cast<float*>(a->workspace);
   const int64_t parts = a->batch * a->kv_heads * p.nrows * pl.splits;
   p.part_o = ws;
@@ -1022,41 +979,13 @@ int hqmq_attention_decode(const hqmq_attention_args* a, void* stream) {
     case 12 * 16 + 3: mk = attention_mma_kernel<12, 3>; break;
     default: break;
   }
-  static const int prefill_variant = [] {
-    const char* v = getenv("HQMQ_PREFILL_VARIANT");  // 1: fused mma.sync prefill
-    return v ? atoi(v) : 0;
-  }();
-  if (prefill_variant == 0 && prefill_tc_applicable(a)) return launch_prefill_tc(a, st);
-  const size_t psmem = prefill_smem_bytes(a->codebook_size);
-  const bool prefill = a->head_dim == 128 && p.nrows > 8 && kPR % p.g == 0 && !a->precise &&
-                       psmem <= 200 * 1024;
-  if (prefill) {
-    void (*pk)(AttParams) = attention_prefill_kernel<0, 0>;
-    if (!a->k.flag_words && !a->v.flag_words) {
-      switch (a->index_bits * 16 + a->radius_bits) {
-        case 9 * 16 + 4: pk = attention_prefill_kernel<9, 4>; break;
-        case 11 * 16 + 4: pk = attention_prefill_kernel<11, 4>; break;
-        case 13 * 16 + 4: pk = attention_prefill_kernel<13, 4>; break;
-        case 11 * 16 + 6: pk = attention_prefill_kernel<11, 6>; break;
-        default: break;
-      }
-    }
-    cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    const int64_t tpt = kPR / p.g;
-    const dim3 pgrid((unsigned)ceil_div(a->q_tokens, tpt), (unsigned)(a->batch * a->kv_heads));
-    pk<<<pgrid, kPThreads, psmem, st>>>(p);
-    return check_launch();
-  }
+  if (prefill_tc_applicable(a)) return launch_prefill_tc(a, st);
   if (mma_path && mk) {
     cudaFuncSetAttribute(mk, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     mk<<<dim3((unsigned)pl.splits, (unsigned)(a->batch * a->kv_heads)), kMThreads, msmem, st>>>(p);
   } else if (tab_bytes <= 160 * 1024) {
-    static thread_local bool set = false;
-    if (!set) {
-      cudaFuncSetAttribute(attention_split_kernel<true>,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-      set = true;
-    }
+    cudaFuncSetAttribute(attention_split_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         160 * 1024);
     attention_split_kernel<true><<<grid, kAttThreads, tab_bytes, st>>>(p);
   } else {
     attention_split_kernel<false><<<grid, kAttThreads, 0, st>>>(p);
@@ -1134,6 +1063,7 @@ int hqmq_attention_decode_paged(const hqmq_paged_attention_args* a, void* stream
     o.flagw = nullptr; o.payloads = nullptr; o.tokoff = nullptr;
     o.table = reinterpret_cast<const float4*>(v.joint_f32);
     o.table16 = reinterpret_cast<const uint2*>(v.joint_f16);
+    o.table64 = nullptr;
     return o;
   };
   p.k = view(a->k);

@@ -1008,6 +1008,7 @@ int hqmq_unpack(const hqmq_decode_args* a, int32_t* indices, uint8_t* quanta, ui
 }
 
 size_t hqmq_pack_workspace_bytes(int64_t n_chunks) {
+  if (n_chunks >= (1LL << 31)) return 0;
   size_t cub_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
                                 (int)std::max<int64_t>(n_chunks, 1));
@@ -1020,7 +1021,9 @@ int hqmq_pack(int64_t n, int32_t C, int32_t w, int32_t br, const int32_t* indice
               void* stream) {
   using namespace hqmq;
   if (n < 0 || C < 1 || w < 1 || w > 32 || br < 1 || br > 8) return HQMQ_ERR_INVALID_ARGUMENT;
-  if (n >= (1LL << 32)) return HQMQ_ERR_UNSUPPORTED;
+  // cub's scan takes an int item count: keep n below 2^31 (a single
+  // (layer, role) call that large would be 17 GB of fp16 input)
+  if (n >= (1LL << 31)) return HQMQ_ERR_UNSUPPORTED;
   if (workspace_bytes < hqmq_pack_workspace_bytes(n)) return HQMQ_ERR_WORKSPACE;
   if (n == 0) return HQMQ_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -1030,7 +1033,10 @@ int hqmq_pack(int64_t n, int32_t C, int32_t w, int32_t br, const int32_t* indice
   char* tmp = ws + ((size_t)n * 8 + 255) / 256 * 256;
   size_t tmp_bytes = workspace_bytes - (size_t)(tmp - ws);
   coded_mark_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, flags, mark);
-  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, mark, pos, (int)n, st);
+  {
+    const cudaError_t e = cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, mark, pos, (int)n, st);
+    if (e != cudaSuccess) return record_cuda_error(e);
+  }
   pack_kernel<<<grid_for(n, 256), 256, 0, st>>>(n, C, w, br, indices, quanta, flags, pos, idxw,
                                                   radw, flags ? flagw : nullptr,
                                                   flags ? tokoff : nullptr);
@@ -1038,6 +1044,7 @@ int hqmq_pack(int64_t n, int32_t C, int32_t w, int32_t br, const int32_t* indice
 }
 
 size_t hqmq_token_offsets_workspace_bytes(int64_t n_tokens) {
+  if (n_tokens >= (1LL << 31)) return 0;
   size_t cub_bytes = 0;
   cub::DeviceScan::ExclusiveSum(nullptr, cub_bytes, (const uint32_t*)nullptr, (uint32_t*)nullptr,
                                 (int)std::max<int64_t>(n_tokens, 1));
@@ -1048,6 +1055,7 @@ int hqmq_token_offsets(int64_t n_tokens, int32_t C, const uint32_t* flagw, uint3
                        void* workspace, size_t workspace_bytes, void* stream) {
   using namespace hqmq;
   if (n_tokens < 0 || C < 1) return HQMQ_ERR_INVALID_ARGUMENT;
+  if (n_tokens >= (1LL << 31)) return HQMQ_ERR_UNSUPPORTED;  // cub int item count
   if (workspace_bytes < hqmq_token_offsets_workspace_bytes(n_tokens)) return HQMQ_ERR_WORKSPACE;
   if (n_tokens == 0) return HQMQ_OK;
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -1056,7 +1064,8 @@ int hqmq_token_offsets(int64_t n_tokens, int32_t C, const uint32_t* flagw, uint3
   char* tmp = ws + ((size_t)n_tokens * 4 + 255) / 256 * 256;
   size_t tmp_bytes = workspace_bytes - (size_t)(tmp - ws);
   token_coded_kernel<<<grid_for(n_tokens, 256), 256, 0, st>>>(n_tokens, C, flagw, cnt);
-  cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, tokoff, (int)n_tokens, st);
+  const cudaError_t e = cub::DeviceScan::ExclusiveSum(tmp, tmp_bytes, cnt, tokoff, (int)n_tokens, st);
+  if (e != cudaSuccess) return record_cuda_error(e);
   return check();
 }
 

@@ -1444,6 +1444,7 @@ bool plan(const hqmq_encode_args* a, Layout& L) {
   L.warp_path = use_warp_path(a);
   // prefix granularity: per token on the warp path, per tile otherwise
   const int64_t n_pre = L.warp_path ? L.rows * a->tokens : L.n_tiles;
+  if (n_pre >= (1LL << 31)) return false;  // cub's scan takes an int item count
   size_t off = 0;
   const bool ext = a->outlier_multiplier > 0.0;
   if (ext) {
@@ -1535,8 +1536,9 @@ int launch_encode(const hqmq_encode_args* a, const Layout& L, cudaStream_t st) {
       token_coded_norms_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n_tok, 256), 148 * 16), 256,
                                  0, st>>>(rp.norms, groups, a->heads, a->tokens, n_tok,
                                           a->per_head_pooling, counts);
-      cub::DeviceScan::ExclusiveSum(ws + L.off_cub, cub_bytes, counts, a->token_offsets,
-                                    (int)n_tok, st);
+      e = cub::DeviceScan::ExclusiveSum(ws + L.off_cub, cub_bytes, counts, a->token_offsets,
+                                        (int)n_tok, st);
+      if (e != cudaSuccess) return cuda_fail(e);
       finalize_counts_kernel<<<1, 32, 0, st>>>(counts, a->token_offsets, n_tok, L.n_chunks,
                                                a->counters);
     } else {
@@ -1544,8 +1546,9 @@ int launch_encode(const hqmq_encode_args* a, const Layout& L, cudaStream_t st) {
       tile_count_kernel<<<dim3((unsigned)L.tiles_per_row, (unsigned)L.rows), 256, 0, st>>>(
           rp.norms, groups, a->heads, a->tokens, L.C, L.TT, L.tiles_per_row,
           a->per_head_pooling, counts);
-      cub::DeviceScan::ExclusiveSum(ws + L.off_cub, cub_bytes, counts, prefix, (int)L.n_tiles,
-                                    st);
+      e = cub::DeviceScan::ExclusiveSum(ws + L.off_cub, cub_bytes, counts, prefix, (int)L.n_tiles,
+                                        st);
+      if (e != cudaSuccess) return cuda_fail(e);
       finalize_counts_kernel<<<1, 32, 0, st>>>(counts, prefix, L.n_tiles, L.n_chunks,
                                                a->counters);
     }
@@ -1570,11 +1573,6 @@ int launch_encode(const hqmq_encode_args* a, const Layout& L, cudaStream_t st) {
   const size_t smem = (size_t)std::min(a->codebook_size, kSBlock) * 4 * sizeof(float4);
   if constexpr (sizeof(InT) == 2) {
     if (L.warp_path) {
-      // tile size / occupancy variant (HQMQ_ENC_VARIANT for tuning: 0..3)
-      static const int variant = [] {
-        const char* v = getenv("HQMQ_ENC_VARIANT");
-        return v ? atoi(v) : 0;
-      }();
       auto launch = [&](auto kern, int wt, int minb) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              kSBlock * 4 * (int)sizeof(float4));
@@ -1583,27 +1581,18 @@ int launch_encode(const hqmq_encode_args* a, const Layout& L, cudaStream_t st) {
         const int64_t bx = std::max<int64_t>(1, std::min<int64_t>(want, ceil_div(ntiles, kWWarps)));
         kern<<<dim3((unsigned)bx, (unsigned)L.rows), kWThreads, smem, st>>>(p);
       };
-      switch (variant) {
-        case 1:  // fused single pass
-          launch(encode_warp_kernel<InT, 4, 2, 0>, 4, 2);
-          break;
-        case 2:  // split, search at 3 CTAs/SM
-          launch(encode_warp_kernel<InT, 4, 4, 1>, 4, 4);
-          launch(encode_warp_kernel<InT, 4, 3, 2>, 4, 3);
-          break;
-        case 3:  // split, search kWT 8
-          launch(encode_warp_kernel<InT, 4, 4, 1>, 4, 4);
-          launch(encode_warp_kernel<InT, 8, 2, 2>, 8, 2);
-          break;
-        case 5:  // split: prep pass, then the FFMA2 search pass
+      switch (a->search_path) {
+        case HQMQ_SEARCH_CUDA_CORE:  // prep pass, then the FFMA2 search pass
           launch(encode_warp_kernel<InT, 4, 4, 1>, 4, 4);
           launch(encode_warp_kernel<InT, 4, 2, 2>, 4, 2);
           break;
         default: {  // split: prep pass, then the tensor-core search pass
           const bool tc32 = a->codebook_size % kTcBlk == 0;
           // e.g. S = 48: N = 64 blocks (at S = 16 the per-tile MMA round trip
-          // outweighs the work: measured 0.52 vs 0.47 ms, FFMA2 kept)
-          const bool tc16 = !tc32 && a->codebook_size % 16 == 0 && a->codebook_size >= 48;
+          // outweighs the work: measured 0.52 vs 0.47 ms, FFMA2 kept unless
+          // the caller forces the tensor-core search)
+          const bool tc16 = !tc32 && a->codebook_size % 16 == 0 &&
+                            (a->codebook_size >= 48 || a->search_path == HQMQ_SEARCH_TENSOR_CORE);
           if (!tc32 && !tc16) {
             launch(encode_warp_kernel<InT, 4, 4, 1>, 4, 4);
             launch(encode_warp_kernel<InT, 4, 2, 2>, 4, 2);
@@ -1632,13 +1621,8 @@ int launch_encode(const hqmq_encode_args* a, const Layout& L, cudaStream_t st) {
       return e == cudaSuccess ? HQMQ_OK : cuda_fail(e);
     }
   }
-  static thread_local bool attr_set[4] = {false, false, false, false};
-  const int ti = sizeof(InT) == 2 ? (std::is_same<InT, __half>::value ? 0 : 1) : (sizeof(InT) == 4 ? 2 : 3);
-  if (!attr_set[ti]) {
-    cudaFuncSetAttribute(encode_tile_kernel<InT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         kSBlock * 4 * (int)sizeof(float4));
-    attr_set[ti] = true;
-  }
+  cudaFuncSetAttribute(encode_tile_kernel<InT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       kSBlock * 4 * (int)sizeof(float4));
   encode_tile_kernel<InT><<<dim3((unsigned)L.tiles_per_row, (unsigned)L.rows), kEncThreads, smem, st>>>(p);
   e = cudaGetLastError();
   return e == cudaSuccess ? HQMQ_OK : cuda_fail(e);

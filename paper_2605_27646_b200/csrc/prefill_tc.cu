@@ -5,14 +5,12 @@
 // canonical tile layouts (fa_tile_kernel), and flash attention runs over them
 // with hand-written tcgen05 MMAs (SWIZZLE_NONE descriptors, one issuing
 // thread, tcgen05.commit -> mbarrier, fp32 S and O in TMEM, P written back to
-// TMEM as the A operand of the PV MMA).  Four kernels, picked by key count
-// (launch_prefill_tc; HQMQ_FA_VARIANT forces one):
+// TMEM as the A operand of the PV MMA).  Two kernels, picked by key count
+// (launch_prefill_tc):
 //   attention_fa4_kernel  default from 4096 keys: 128-key tiles, two CTAs per
 //                         SM, each a sequential S -> softmax -> PV pipeline
 //   attention_fa2_kernel  default below: 64-key tiles, two query tiles per CTA,
 //                         double-buffered S, TMA producer warps
-//   attention_fa3_kernel  128-key tiles, one CTA per SM, three S buffers
-//   attention_fa_tc_kernel  the first, 4-warp version (cp.async, P via smem)
 // Design notes and measurements: DESIGN.md §4 (prefill attention).
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -74,252 +72,6 @@ __device__ __forceinline__ void fa_commit(uint64_t* bar) {
         "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]),      \
         "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),      \
         "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31]))
-
-struct FaParams {
-  int64_t B, Hq, Hkv, Tq, Tkv;
-  int g, causal;
-  float scale_log2;
-  const float* q;     // (B, Hq, Tq, 128) fp32
-  const __half* k;    // (B, Hkv, Tkv, 128) fp16 (decoded)
-  const __half* v;
-  float* out;         // (B, Hq, Tq, 128) fp32
-};
-
-__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(smem_u32(dst)), "l"(src),
-               "r"(valid ? 16 : 0)
-               : "memory");
-}
-
-__global__ void __launch_bounds__(kFaThreads, 2) attention_fa_tc_kernel(FaParams p) {
-  extern __shared__ __align__(1024) unsigned char fsm[];
-  unsigned char* qs = fsm;                       // 32 KB
-  unsigned char* kvbuf = qs + kQBytes;           // 2 x (K 16 KB + V 16 KB): cp.async double buffer
-  unsigned char* psm = kvbuf + 4 * kKBytes;      // 16 KB (P)
-  __shared__ __align__(8) uint64_t bar_s, bar_o;
-  __shared__ uint32_t tmem_slot;
-  const int tid = threadIdx.x, warp = tid >> 5;
-  const int64_t bh = blockIdx.y;
-  const int64_t b = bh / p.Hkv, hkv = bh % p.Hkv;
-  const int g = p.g;
-  const int tpt = kFaRows / g;
-  const int64_t tok0 = (int64_t)blockIdx.x * tpt;
-  const int64_t off = p.causal ? (p.Tkv - p.Tq) : 0;
-  // this thread's row
-  const int64_t qtok = tok0 + tid / g;
-  const int qhead = tid % g;
-  const bool rvalid = qtok < p.Tq;
-  const int64_t vis = p.causal ? qtok + off + 1 : p.Tkv;
-
-  if (warp == 0) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(&tmem_slot)),
-                 "n"(256));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  if (tid == 0) {
-    mbar_init(&bar_s, 1);
-    mbar_init(&bar_o, 1);
-    fence_mbar_init();
-  }
-  // Q row -> fp16 (pre-scaled), K-major A operand
-  {
-    const float4* qr = reinterpret_cast<const float4*>(
-        p.q + ((b * p.Hq + hkv * g + qhead) * p.Tq + (rvalid ? qtok : 0)) * kFaD);
-#pragma unroll 4
-    for (int kg = 0; kg < kFaD / 8; ++kg) {
-      float4 a = make_float4(0.f, 0.f, 0.f, 0.f), c = a;
-      if (rvalid) {
-        a = __ldg(qr + 2 * kg);
-        c = __ldg(qr + 2 * kg + 1);
-      }
-      const float sl = p.scale_log2;
-      const __half2 h0 = __floats2half2_rn(a.x * sl, a.y * sl), h1 = __floats2half2_rn(a.z * sl, a.w * sl);
-      const __half2 h2 = __floats2half2_rn(c.x * sl, c.y * sl), h3 = __floats2half2_rn(c.z * sl, c.w * sl);
-      *reinterpret_cast<uint4*>(qs + (tid >> 3) * kSboQK + kg * 128 + (tid & 7) * 16) =
-          make_uint4(*reinterpret_cast<const uint32_t*>(&h0), *reinterpret_cast<const uint32_t*>(&h1),
-                     *reinterpret_cast<const uint32_t*>(&h2), *reinterpret_cast<const uint32_t*>(&h3));
-    }
-  }
-  fence_proxy_async();
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tm = tmem_slot;  // S(t & 1): cols [0, 64) / [64, 128), O: cols [128, 256)
-  const uint32_t tm_row = tm + ((uint32_t)(warp * 32) << 16);
-  const uint32_t q_sa = smem_u32(qs), p_sa = smem_u32(psm);
-
-  const int64_t last_tok = std::min(p.Tq, tok0 + tpt) - 1;
-  const int64_t kend = p.causal ? std::min(p.Tkv, last_tok + off + 1) : p.Tkv;
-  const __half* kbase = p.k + bh * p.Tkv * kFaD;
-  const __half* vbase = p.v + bh * p.Tkv * kFaD;
-  float m_run = -INFINITY, l_run = 0.f;
-  uint32_t ph_s = 0, ph_o = 0;
-  const int ntiles = (int)((kend + kFaKeys - 1) / kFaKeys);
-  // K tiles run two ahead (K-major B: row = key), V tiles one ahead (MN-major
-  // B: n = dim, k = key), each double-buffered and zero-filled past kend; every
-  // call commits one cp.async group so the group count stays uniform
-  auto load_k = [&](int t) {
-    if (t < ntiles) {
-      unsigned char* ks = kvbuf + (t & 1) * kKBytes;
-      const int64_t k0 = (int64_t)t * kFaKeys;
-      for (int i = tid; i < kFaKeys * (kFaD / 8); i += kFaThreads) {
-        const int key = i >> 4, dg = i & 15;
-        const bool ok = k0 + key < kend;
-        cp_async16(ks + (key >> 3) * kSboQK + dg * 128 + (key & 7) * 16,
-                   reinterpret_cast<const uint4*>(kbase + (ok ? k0 + key : 0) * kFaD) + dg, ok);
-      }
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-  auto load_v = [&](int t) {
-    if (t < ntiles) {
-      unsigned char* vs = kvbuf + (2 + (t & 1)) * kKBytes;
-      const int64_t k0 = (int64_t)t * kFaKeys;
-      for (int i = tid; i < kFaKeys * (kFaD / 8); i += kFaThreads) {
-        const int key = i >> 4, dg = i & 15;
-        const bool ok = k0 + key < kend;
-        cp_async16(vs + dg * kSboV + (key >> 3) * 128 + (key & 7) * 16,
-                   reinterpret_cast<const uint4*>(vbase + (ok ? k0 + key : 0) * kFaD) + dg, ok);
-      }
-    }
-    asm volatile("cp.async.commit_group;" ::: "memory");
-  };
-  const uint32_t kv_sa = smem_u32(kvbuf);
-  auto issue_s = [&](int t) {  // S(t) = Q K(t)^T into TMEM columns (t & 1) * 64
-#pragma unroll
-    for (int kk = 0; kk < kFaD / 16; ++kk)
-      fa_mma(tm + (uint32_t)(t & 1) * 64, fa_desc(q_sa + kk * 256, kSboQK),
-             fa_desc(kv_sa + (t & 1) * kKBytes + kk * 256, kSboQK), fa_idesc(kFaRows, kFaKeys, 0),
-             kk > 0);
-    fa_commit(&bar_s);
-  };
-  if (ntiles > 0) {
-    load_k(0);
-    load_k(1);
-    load_v(0);
-    asm volatile("cp.async.wait_group 2;" ::: "memory");
-    fence_proxy_async();
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    if (tid == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      issue_s(0);
-    }
-  }
-  for (int t = 0; t < ntiles; ++t) {
-    const int64_t k0 = (int64_t)t * kFaKeys;
-    const int nk = (int)std::min((int64_t)kFaKeys, kend - k0);
-    // 1. scores of tile t
-    mbar_wait(&bar_s, ph_s);
-    ph_s ^= 1u;
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    uint32_t sr[64];
-    FA_LD32(tm_row + (uint32_t)(t & 1) * 64, sr);
-    FA_LD32(tm_row + (uint32_t)(t & 1) * 64 + 32, (sr + 32));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    // 2. K(t) is consumed: its buffer takes K(t+2)
-    load_k(t + 2);
-    // 3. online softmax (log2 domain), P in registers
-    float mx = -INFINITY;
-#pragma unroll
-    for (int j = 0; j < 64; ++j) {
-      const int64_t key = k0 + j;
-      float sv = __uint_as_float(sr[j]);
-      sv = (rvalid && j < nk && key < vis) ? sv : -INFINITY;
-      sr[j] = __float_as_uint(sv);
-      mx = fmaxf(mx, sv);
-    }
-    const float m_new = fmaxf(m_run, mx);
-    const float alpha = (m_new == -INFINITY) ? 1.f : exp2f(m_run - m_new);
-    float psum = 0.f;
-    uint32_t hw[32];
-#pragma unroll
-    for (int e = 0; e < 32; ++e) {
-      const float s0 = __uint_as_float(sr[2 * e]), s1 = __uint_as_float(sr[2 * e + 1]);
-      const float e0 = m_new == -INFINITY ? 0.f : exp2f(s0 - m_new);
-      const float e1 = m_new == -INFINITY ? 0.f : exp2f(s1 - m_new);
-      psum += e0 + e1;
-      const __half2 h = __floats2half2_rn(e0, e1);
-      hw[e] = *reinterpret_cast<const uint32_t*>(&h);
-    }
-    l_run = l_run * alpha + psum;
-    m_run = m_new;
-    // 4. PV(t-1) done: P smem, V buffer (t-1) & 1 and the O accumulator are free
-    if (t > 0) {
-      mbar_wait(&bar_o, ph_o);
-      ph_o ^= 1u;
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    }
-    // 5. V(t+1) into the freed V buffer
-    load_v(t + 1);
-    // 6. rescale O in TMEM when some row's max moved (warp-uniform), write P(t)
-    if (t > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint32_t orr[32];
-        FA_LD32(tm_row + 128 + c * 32, orr);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-        for (int j = 0; j < 32; ++j) orr[j] = __float_as_uint(__uint_as_float(orr[j]) * alpha);
-        FA_ST32(tm_row + 128 + c * 32, orr);
-      }
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-    }
-#pragma unroll
-    for (int kg = 0; kg < 8; ++kg)
-      *reinterpret_cast<uint4*>(psm + (tid >> 3) * kSboP + kg * 128 + (tid & 7) * 16) =
-          make_uint4(hw[4 * kg], hw[4 * kg + 1], hw[4 * kg + 2], hw[4 * kg + 3]);
-    // 7. K(t+1) and V(t) have landed (the two newest groups may still fly)
-    asm volatile("cp.async.wait_group 2;" ::: "memory");
-    fence_proxy_async();
-    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-    __syncthreads();
-    // 8. O += P(t) V(t); then S(t+1)
-    if (tid == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#pragma unroll
-      for (int kk = 0; kk < kFaKeys / 16; ++kk)
-        fa_mma(tm + 128, fa_desc(p_sa + kk * 256, kSboP),
-               fa_desc(kv_sa + (2 + (t & 1)) * kKBytes + kk * 256, kSboV),
-               fa_idesc(kFaRows, kFaD, 1), (t > 0 || kk > 0) ? 1u : 0u);
-      fa_commit(&bar_o);
-      if (t + 1 < ntiles) issue_s(t + 1);
-    }
-  }
-  const int ntile = ntiles;
-  if (ntile > 0) {
-    mbar_wait(&bar_o, ph_o);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  }
-  // ---- O / l -> out (every thread takes part in the aligned TMEM loads)
-  {
-    float* orow = p.out + ((b * p.Hq + hkv * g + qhead) * p.Tq + (rvalid ? qtok : 0)) * kFaD;
-    const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      uint32_t orr[32];
-      if (ntile > 0) {
-        FA_LD32(tm_row + 128 + c * 32, orr);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      } else {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) orr[j] = 0u;
-      }
-      if (rvalid) {
-#pragma unroll
-        for (int j = 0; j < 32; j += 4)
-          *reinterpret_cast<float4*>(orow + c * 32 + j) =
-              make_float4(__uint_as_float(orr[j]) * inv, __uint_as_float(orr[j + 1]) * inv,
-                          __uint_as_float(orr[j + 2]) * inv, __uint_as_float(orr[j + 3]) * inv);
-      }
-    }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "n"(256));
-}
 
 // ------------------------------------------------------------------------
 // Warp-specialised two-tile version (default below 4096 keys; measured against
@@ -651,25 +403,9 @@ __global__ void __launch_bounds__(kF2Threads, 1) attention_fa2_kernel(Fa2Params 
 }
 
 // ------------------------------------------------------------------------
-// 128-key one-tile version (HQMQ_FA_VARIANT=3).  One query tile of 128 rows per CTA
-// (128 / g tokens x g heads of one kv head), 11 warps: softmax warps 0-7
-// (warps w and w+4 share TMEM lanes 32 (w % 4): warp w < 4 takes keys 0-63
-// of each row, warp w+4 keys 64-127), K producer (8), MMA issuer (9), V
-// producer (10).  With 128-key tiles both MMAs run at the tensor-core floor
-// (SS S = QK^T with N = 128 streams 8 KB of shared memory per 64-cycle K-step
-// = the 128 B/clk the SS form can read; PV is TS with P in TMEM), where the
-// 64-key S MMA of the two-tile kernel costs 48 instead of 32 cycles a step.
-// TMEM: three S buffers [0,128) / [128,256) / [256,384) (P(t) written back
-// over the first 64 columns of its S buffer), O [384,512).  MMA order S(0)
-// S(1) S(2) | PV(t) S(t+3) | ...: two score tiles stay queued on the tensor
-// cores while a P(t) round trip (commit -> softmax -> arrive) is in flight.  Softmax in one pass against the running max; the two halves
-// of a row exchange tile maxima through shared memory (named barrier per
-// warp pair) and redo the tile with the new max when it rose by more than 8.
-constexpr int kF3Keys = 128, kF3KStages = 3, kF3VStages = 3, kF3SBufs = 3, kF3Threads = 352;
+// 128-key tile geometry shared by the two-CTAs-per-SM kernel below.
+constexpr int kF3Keys = 128;
 constexpr uint32_t kF3TileBytes = kF3Keys * kFaD * 2;  // 32 KB
-constexpr uint32_t kF3KOff = kQBytes;
-constexpr uint32_t kF3VOff = kF3KOff + kF3KStages * kF3TileBytes;
-constexpr uint32_t kF3Smem = kF3VOff + kF3VStages * kF3TileBytes;
 constexpr uint32_t kSbo128 = (kF3Keys / 8) * 128;  // MN-major V: 16 key-groups per 8-dim group
 
 #define FA_ST16(addr, r)                                                                        \
@@ -679,250 +415,6 @@ constexpr uint32_t kSbo128 = (kF3Keys / 8) * 128;  // MN-major V: 16 key-groups 
       "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),  \
       "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),         \
       "r"(r[15]))
-
-__global__ void __launch_bounds__(kF3Threads, 1) attention_fa3_kernel(Fa2Params p) {
-  extern __shared__ __align__(1024) unsigned char fsm[];
-  __shared__ __align__(8) uint64_t full_k[kF3KStages], empty_k[kF3KStages];
-  __shared__ __align__(8) uint64_t full_v[kF3VStages], empty_v[kF3VStages];
-  __shared__ __align__(8) uint64_t bar_s[kF3SBufs], bar_p[kF3SBufs], bar_o[2], bar_fin;
-  __shared__ uint32_t tmem_slot;
-  __shared__ float xch[2][kFaRows];  // per-half tile max (and final l) exchange
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  // grid (B*Hkv, query tiles), longest causal tiles first
-  const int64_t bh = blockIdx.x;
-  const int64_t b = bh / p.Hkv, hkv = bh % p.Hkv;
-  const int g = p.g;
-  const int tpt = kFaRows / g;
-  const int64_t tok0 = (int64_t)(gridDim.y - 1 - blockIdx.y) * tpt;
-  const int64_t off = p.causal ? (p.Tkv - p.Tq) : 0;
-  const int64_t last_tok = std::min(p.Tq, tok0 + tpt) - 1;
-  const int64_t kend = p.causal ? std::min(p.Tkv, last_tok + off + 1) : p.Tkv;
-  const int ntiles = kend > 0 ? (int)((kend + kF3Keys - 1) / kF3Keys) : 0;
-
-  if (warp == 9) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(&tmem_slot)),
-                 "n"(512));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  if (tid == 0) {
-    for (int i = 0; i < kF3KStages; ++i) {
-      mbar_init(&full_k[i], 1);
-      mbar_init(&empty_k[i], 1);
-    }
-    for (int i = 0; i < kF3VStages; ++i) {
-      mbar_init(&full_v[i], 1);
-      mbar_init(&empty_v[i], 1);
-    }
-    for (int i = 0; i < kF3SBufs; ++i) {
-      mbar_init(&bar_s[i], 1);
-      mbar_init(&bar_p[i], 2 * kFaRows);
-    }
-    mbar_init(&bar_o[0], 1);
-    mbar_init(&bar_o[1], 1);
-    mbar_init(&bar_fin, 1);
-    fence_mbar_init();
-  }
-  const int r = tid & 127, half = (tid >> 7) & 1;
-  const int64_t qtok = tok0 + r / g;
-  const int qhead = r % g;
-  const bool rvalid = tid < 2 * kFaRows && qtok < p.Tq;
-  const int64_t vis = p.causal ? std::min(qtok + off + 1, p.Tkv) : p.Tkv;
-  if (tid < kFaRows) {
-    const float4* qr = reinterpret_cast<const float4*>(
-        p.q + ((b * p.Hq + hkv * g + qhead) * p.Tq + (rvalid ? qtok : 0)) * kFaD);
-#pragma unroll 4
-    for (int kg = 0; kg < kFaD / 8; ++kg) {
-      float4 a = make_float4(0.f, 0.f, 0.f, 0.f), c = a;
-      if (rvalid) {
-        a = __ldg(qr + 2 * kg);
-        c = __ldg(qr + 2 * kg + 1);
-      }
-      const float sl = p.scale_log2;
-      const __half2 h0 = __floats2half2_rn(a.x * sl, a.y * sl), h1 = __floats2half2_rn(a.z * sl, a.w * sl);
-      const __half2 h2 = __floats2half2_rn(c.x * sl, c.y * sl), h3 = __floats2half2_rn(c.z * sl, c.w * sl);
-      *reinterpret_cast<uint4*>(fsm + (r >> 3) * kSboQK + kg * 128 + (r & 7) * 16) =
-          make_uint4(*reinterpret_cast<const uint32_t*>(&h0), *reinterpret_cast<const uint32_t*>(&h1),
-                     *reinterpret_cast<const uint32_t*>(&h2), *reinterpret_cast<const uint32_t*>(&h3));
-    }
-  }
-  fence_proxy_async();
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tm = tmem_slot;
-  const uint32_t sbase = smem_u32(fsm);
-  auto k_smem = [&](int t) { return kF3KOff + (uint32_t)(t % kF3KStages) * kF3TileBytes; };
-  auto v_smem = [&](int t) { return kF3VOff + (uint32_t)(t % kF3VStages) * kF3TileBytes; };
-
-  if (warp == 8 || warp == 10) {
-    // ---- producers: K (warp 8) and V (warp 10), one 32 KB bulk copy per tile
-    if (lane == 0) {
-      const bool is_k = warp == 8;
-      const int ns = is_k ? kF3KStages : kF3VStages;
-      uint64_t* fullb = is_k ? full_k : full_v;
-      uint64_t* emptyb = is_k ? empty_k : empty_v;
-      const unsigned char* src = (is_k ? p.kt : p.vt) + (size_t)bh * p.ntk * kF3TileBytes;
-      for (int t = 0; t < ntiles; ++t) {
-        const int st = t % ns;
-        if (t >= ns) fa_wait(&emptyb[st], (uint32_t)((t / ns) - 1) & 1u);
-        mbar_arrive_expect_tx(&fullb[st], kF3TileBytes);
-        bulk_g2s(fsm + (is_k ? k_smem(t) : v_smem(t)), src + (size_t)t * kF3TileBytes, kF3TileBytes,
-                 &fullb[st]);
-      }
-    }
-    __syncwarp();
-  } else if (warp == 9) {
-    // ---- MMA issuer
-    if (lane == 0 && ntiles > 0) {
-      auto s_mma = [&](int t) {  // S(t) = Q K(t)^T -> TMEM cols 128 (t % 3)
-#pragma unroll
-        for (int kk = 0; kk < kFaD / 16; ++kk)
-          fa_mma(tm + (uint32_t)(t % kF3SBufs) * 128, fa_desc(sbase + kk * 256, kSboQK),
-                 fa_desc(sbase + k_smem(t) + kk * 256, kSboQK), fa_idesc(kFaRows, kF3Keys, 0), kk > 0);
-        fa_commit(&bar_s[t % kF3SBufs]);
-        fa_commit(&empty_k[t % kF3KStages]);
-      };
-      auto pv_mma = [&](int t) {  // O += P(t) V(t), A = P(t) from TMEM
-        const uint32_t pa = tm + (uint32_t)(t % kF3SBufs) * 128;
-#pragma unroll
-        for (int kk = 0; kk < kF3Keys / 16; ++kk)
-          asm volatile(
-              "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-              "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tm + 384),
-              "r"(pa + kk * 8), "l"(fa_desc(sbase + v_smem(t) + kk * 256, kSbo128)),
-              "r"(fa_idesc(kFaRows, kFaD, 1)), "r"((t > 0 || kk > 0) ? 1u : 0u));
-        fa_commit(&bar_o[t & 1]);
-        fa_commit(&empty_v[t % kF3VStages]);
-      };
-      for (int t = 0; t < kF3SBufs && t < ntiles; ++t) {
-        fa_wait(&full_k[t], 0);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        s_mma(t);
-      }
-      for (int t = 0; t < ntiles; ++t) {
-        fa_wait(&full_v[t % kF3VStages], (uint32_t)(t / kF3VStages) & 1u);
-        fa_wait(&bar_p[t % kF3SBufs], (uint32_t)(t / kF3SBufs) & 1u);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        pv_mma(t);
-        if (t + kF3SBufs < ntiles) {  // S(t+3) into the buffer P(t) occupies: after PV(t) in issue order
-          const int u = t + kF3SBufs;
-          fa_wait(&full_k[u % kF3KStages], (uint32_t)(u / kF3KStages) & 1u);
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          s_mma(u);
-        }
-      }
-      fa_commit(&bar_fin);
-    }
-    __syncwarp();
-  } else {
-    // ---- softmax (warps 0-7): thread = (row r, key half)
-    const uint32_t tm_row = tm + ((uint32_t)((warp & 3) * 32) << 16);
-    const uint32_t o_col = 384 + (uint32_t)half * 64;  // this half's O columns
-    const int pair_bar = 1 + (warp & 3);                 // named barrier of warps w, w+4
-    auto pair_sync = [&]() { asm volatile("bar.sync %0, 64;" ::"r"(pair_bar) : "memory"); };
-    float m_run = -INFINITY, l_run = 0.f;
-    for (int t = 0; t < ntiles; ++t) {
-      const int64_t k0 = (int64_t)t * kF3Keys + half * 64;
-      const uint32_t s_col = (uint32_t)(t % kF3SBufs) * 128;
-      fa_wait(&bar_s[t % kF3SBufs], (uint32_t)(t / kF3SBufs) & 1u);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const bool mask = !rvalid || k0 + 64 > vis;
-      // one pass against the running max; P stays in registers until the pass
-      // is accepted (it is stored over S columns a redo would read again)
-      uint32_t hw[32];
-      auto pass = [&](float m_use, float& tile_max) {
-        float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-        float2 acc[2] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          uint32_t sr[32];
-          FA_LD32(tm_row + s_col + half * 64 + c * 32, sr);
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-          if (mask) {
-#pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (!rvalid || k0 + c * 32 + j >= vis) sr[j] = __float_as_uint(-INFINITY);
-          }
-          fa_softmax32(sr, m_use, mx, acc, hw + c * 16);
-        }
-        tile_max = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
-        return (acc[0].x + acc[0].y) + (acc[1].x + acc[1].y);
-      };
-      float tmax = -INFINITY;
-      float psum = pass(m_run == -INFINITY ? 0.f : m_run, tmax);
-      // the row's tile max over both halves
-      xch[half][r] = tmax;
-      pair_sync();
-      tmax = fmaxf(tmax, xch[half ^ 1][r]);
-      const bool jump = tmax > m_run + 8.f;  // same in both halves of the row
-      const float m_new = jump ? tmax : m_run;
-      if (__any_sync(0xffffffffu, jump)) {  // warp-uniform (.sync.aligned loads)
-        float dummy = -INFINITY;
-        psum = pass(m_new == -INFINITY ? 0.f : m_new, dummy);
-      }
-      // both halves are done reading S(t) before either overwrites it with P
-      pair_sync();
-#pragma unroll
-      for (int c = 0; c < 2; ++c) FA_ST16(tm_row + s_col + half * 32 + c * 16, (hw + c * 16));
-      const float alpha = (m_new == m_run) ? 1.f : exp2f(m_run - m_new);
-      l_run = l_run * alpha + psum;
-      m_run = m_new;
-      // O is only touched when some row's max moved: PV(t-1) must be done
-      // (S(t) complete implies PV(t-3) done: with one barrier per PV parity,
-      // bar_o[(t-1) & 1] is at most one phase behind)
-      if (t > 0 && __any_sync(0xffffffffu, alpha != 1.f)) {
-        fa_wait(&bar_o[(t - 1) & 1], (uint32_t)((t - 1) >> 1) & 1u);
-        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          uint32_t orr[32];
-          FA_LD32(tm_row + o_col + c * 32, orr);
-          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-          for (int j = 0; j < 32; ++j) orr[j] = __float_as_uint(__uint_as_float(orr[j]) * alpha);
-          FA_ST32(tm_row + o_col + c * 32, orr);
-        }
-      }
-      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      mbar_arrive(&bar_p[t % kF3SBufs]);
-    }
-    // l = sum of the two halves' partial sums (same running max history)
-    pair_sync();
-    xch[half][r] = l_run;
-    pair_sync();
-    l_run += xch[half ^ 1][r];
-    if (ntiles > 0) {
-      fa_wait(&bar_fin, 0);
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    }
-    float* orow = p.out + ((b * p.Hq + hkv * g + qhead) * p.Tq + (rvalid ? qtok : 0)) * kFaD + half * 64;
-    const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      uint32_t orr[32];
-      if (ntiles > 0) {
-        FA_LD32(tm_row + o_col + c * 32, orr);
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      } else {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) orr[j] = 0u;
-      }
-      if (rvalid) {
-#pragma unroll
-        for (int j = 0; j < 32; j += 4)
-          *reinterpret_cast<float4*>(orow + c * 32 + j) =
-              make_float4(__uint_as_float(orr[j]) * inv, __uint_as_float(orr[j + 1]) * inv,
-                          __uint_as_float(orr[j + 2]) * inv, __uint_as_float(orr[j + 3]) * inv);
-      }
-    }
-  }
-  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-  __syncthreads();
-  if (warp == 9)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "n"(512));
-}
 
 // ------------------------------------------------------------------------
 // Two-CTAs-per-SM version (default from 4096 keys).  Each CTA is one strictly
@@ -1189,16 +681,6 @@ int decode_fp16_tiles(const hqmq_decode_args* a, int tile_log2, int mn, int64_t 
 
 // Decode-once + tcgen05 flash attention for prefill shapes.  Workspace: the
 // two decoded fp16 tensors (kv layout) + an error word.
-static int prefill_variant() {
-  static const int v = [] {
-    // A/B: 1 = 4-warp kernel, 2 = two-tile 64-key kernel, 3 = one-tile 128-key
-    // kernel, 4 = two-CTAs-per-SM 128-key kernel
-    const char* e = getenv("HQMQ_FA_VARIANT");
-    return e ? atoi(e) : 0;
-  }();
-  return v;
-}
-
 size_t prefill_tc_workspace(const hqmq_attention_args* a) {
   const size_t bh = (size_t)a->batch * a->kv_heads;
   const size_t lin = 2 * bh * a->kv_tokens * kFaD * 2;
@@ -1243,93 +725,57 @@ int launch_prefill_tc(const hqmq_attention_args* a, cudaStream_t st) {
     }
     return (int)HQMQ_OK;
   };
-  if (prefill_variant() == 1) {
-    const int rc = decode_rowmajor();
+  // the two-CTAs-per-SM 128-key kernel for long key ranges (0.62 ms at 8k vs
+  // 0.71 for the two-tile 64-key kernel), the 64-key kernel for short ones
+  // (0.090 vs 0.093 ms at 2k)
+  const bool v4 = a->kv_tokens >= 4096;
+  const int keys = v4 ? kF3Keys : kF2Keys;
+  const uint32_t tile_bytes = v4 ? kF3TileBytes : kF2TileBytes;
+  const int64_t bh = a->batch * a->kv_heads;
+  const int64_t ntk = ceil_div(a->kv_tokens, keys);
+  unsigned char* kt = ws + 2 * nelem * 2;
+  unsigned char* vt = kt + (size_t)bh * ntk * tile_bytes;
+  // the fast decode writes its 16-byte units straight into the tiles; other
+  // streams (Med3x) decode row-major and are re-laid out
+  const int log2k = v4 ? 7 : 6;
+  int rc = decode_fp16_tiles(&dargs[0], log2k, 0, ntk, kt, st);
+  if (rc == HQMQ_OK) rc = decode_fp16_tiles(&dargs[1], log2k, 1, ntk, vt, st);
+  if (rc == HQMQ_OK) {
+    if (a->kv_tokens % keys) {  // keys past T in each row's last tile: zeros
+      const int64_t units = bh * (keys - a->kv_tokens % keys) * 16;
+      fa_pad_kernel<<<(unsigned)std::min<int64_t>(ceil_div(units, 256), 148 * 16), 256, 0, st>>>(
+          reinterpret_cast<uint4*>(kt), reinterpret_cast<uint4*>(vt), bh, a->kv_tokens, ntk, keys);
+    }
+  } else if (rc == HQMQ_ERR_UNSUPPORTED) {
+    rc = decode_rowmajor();
     if (rc != HQMQ_OK) return rc;
+    const int64_t units = bh * ntk * keys * 16;
+    const unsigned grid_t = (unsigned)std::min<int64_t>(ceil_div(units, 256), 148 * 16);
+    fa_tile_kernel<<<grid_t, 256, 0, st>>>(reinterpret_cast<const uint4*>(kd), reinterpret_cast<uint4*>(kt),
+                                           bh, a->kv_tokens, ntk, 0, keys);
+    fa_tile_kernel<<<grid_t, 256, 0, st>>>(reinterpret_cast<const uint4*>(vd), reinterpret_cast<uint4*>(vt),
+                                           bh, a->kv_tokens, ntk, 1, keys);
+  } else {
+    return rc;
   }
-  if (prefill_variant() != 1) {
-    // auto: the two-CTAs-per-SM 128-key kernel for long key ranges (0.62 ms at
-    // 8k vs 0.655 one-tile 128-key, 0.71 two-tile 64-key), the two-tile 64-key
-    // kernel for short ones (0.090 vs 0.093 ms at 2k)
-    const bool v4 = prefill_variant() == 4 || (prefill_variant() == 0 && a->kv_tokens >= 4096);
-    const bool v3 = v4 || prefill_variant() == 3;
-    const int keys = v3 ? kF3Keys : kF2Keys;
-    const uint32_t tile_bytes = v3 ? kF3TileBytes : kF2TileBytes;
-    const int64_t bh = a->batch * a->kv_heads;
-    const int64_t ntk = ceil_div(a->kv_tokens, keys);
-    unsigned char* kt = ws + 2 * nelem * 2;
-    unsigned char* vt = kt + (size_t)bh * ntk * tile_bytes;
-    // the fast decode writes its 16-byte units straight into the tiles; other
-    // streams (Med3x) decode row-major and are re-laid out
-    const int log2k = v3 ? 7 : 6;
-    int rc = decode_fp16_tiles(&dargs[0], log2k, 0, ntk, kt, st);
-    if (rc == HQMQ_OK) rc = decode_fp16_tiles(&dargs[1], log2k, 1, ntk, vt, st);
-    if (rc == HQMQ_OK) {
-      if (a->kv_tokens % keys) {  // keys past T in each row's last tile: zeros
-        const int64_t units = bh * (keys - a->kv_tokens % keys) * 16;
-        fa_pad_kernel<<<(unsigned)std::min<int64_t>(ceil_div(units, 256), 148 * 16), 256, 0, st>>>(
-            reinterpret_cast<uint4*>(kt), reinterpret_cast<uint4*>(vt), bh, a->kv_tokens, ntk, keys);
-      }
-    } else if (rc == HQMQ_ERR_UNSUPPORTED) {
-      rc = decode_rowmajor();
-      if (rc != HQMQ_OK) return rc;
-      const int64_t units = bh * ntk * keys * 16;
-      const unsigned grid_t = (unsigned)std::min<int64_t>(ceil_div(units, 256), 148 * 16);
-      fa_tile_kernel<<<grid_t, 256, 0, st>>>(reinterpret_cast<const uint4*>(kd), reinterpret_cast<uint4*>(kt),
-                                             bh, a->kv_tokens, ntk, 0, keys);
-      fa_tile_kernel<<<grid_t, 256, 0, st>>>(reinterpret_cast<const uint4*>(vd), reinterpret_cast<uint4*>(vt),
-                                             bh, a->kv_tokens, ntk, 1, keys);
-    } else {
-      return rc;
-    }
-    rc = check_launch();
-    if (rc != HQMQ_OK) return rc;
-    if (v4) {
-      Fa2Params q4;
-      q4.B = a->batch; q4.Hq = a->q_heads; q4.Hkv = a->kv_heads; q4.Tq = a->q_tokens;
-      q4.Tkv = a->kv_tokens; q4.ntk = ntk;
-      q4.g = (int)(a->q_heads / a->kv_heads); q4.causal = a->causal;
-      q4.scale_log2 = (float)(a->scale * 1.4426950408889634);
-      q4.q = a->q; q4.kt = kt; q4.vt = vt; q4.out = a->out;
-      cudaFuncSetAttribute(attention_fa4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF4Smem);
-      const dim3 grid((unsigned)bh, (unsigned)ceil_div(a->q_tokens, kFaRows / q4.g));
-      attention_fa4_kernel<<<grid, kF4Threads, kF4Smem, st>>>(q4);
-      return check_launch();
-    }
-    if (v3) {
-      Fa2Params q3;
-      q3.B = a->batch; q3.Hq = a->q_heads; q3.Hkv = a->kv_heads; q3.Tq = a->q_tokens;
-      q3.Tkv = a->kv_tokens; q3.ntk = ntk;
-      q3.g = (int)(a->q_heads / a->kv_heads); q3.causal = a->causal;
-      q3.scale_log2 = (float)(a->scale * 1.4426950408889634);
-      q3.q = a->q; q3.kt = kt; q3.vt = vt; q3.out = a->out;
-      cudaFuncSetAttribute(attention_fa3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF3Smem);
-      const dim3 grid((unsigned)bh, (unsigned)ceil_div(a->q_tokens, kFaRows / q3.g));
-      attention_fa3_kernel<<<grid, kF3Threads, kF3Smem, st>>>(q3);
-      return check_launch();
-    }
-    Fa2Params q2;
-    q2.B = a->batch; q2.Hq = a->q_heads; q2.Hkv = a->kv_heads; q2.Tq = a->q_tokens;
-    q2.Tkv = a->kv_tokens; q2.ntk = ntk;
-    q2.g = (int)(a->q_heads / a->kv_heads); q2.causal = a->causal;
-    q2.scale_log2 = (float)(a->scale * 1.4426950408889634);
-    q2.q = a->q; q2.kt = kt; q2.vt = vt; q2.out = a->out;
-    cudaFuncSetAttribute(attention_fa2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF2Smem);
-    const int64_t tpt = 2 * kFaRows / q2.g;
-    const dim3 grid((unsigned)bh, (unsigned)ceil_div(a->q_tokens, tpt));
-    attention_fa2_kernel<<<grid, kF2Threads, kF2Smem, st>>>(q2);
+  rc = check_launch();
+  if (rc != HQMQ_OK) return rc;
+  Fa2Params q2;
+  q2.B = a->batch; q2.Hq = a->q_heads; q2.Hkv = a->kv_heads; q2.Tq = a->q_tokens;
+  q2.Tkv = a->kv_tokens; q2.ntk = ntk;
+  q2.g = (int)(a->q_heads / a->kv_heads); q2.causal = a->causal;
+  q2.scale_log2 = (float)(a->scale * 1.4426950408889634);
+  q2.q = a->q; q2.kt = kt; q2.vt = vt; q2.out = a->out;
+  if (v4) {
+    cudaFuncSetAttribute(attention_fa4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF4Smem);
+    const dim3 grid((unsigned)bh, (unsigned)ceil_div(a->q_tokens, kFaRows / q2.g));
+    attention_fa4_kernel<<<grid, kF4Threads, kF4Smem, st>>>(q2);
     return check_launch();
   }
-  FaParams p;
-  p.B = a->batch; p.Hq = a->q_heads; p.Hkv = a->kv_heads; p.Tq = a->q_tokens; p.Tkv = a->kv_tokens;
-  p.g = (int)(a->q_heads / a->kv_heads); p.causal = a->causal;
-  p.scale_log2 = (float)(a->scale * 1.4426950408889634);
-  p.q = a->q; p.k = kd; p.v = vd; p.out = a->out;
-  const size_t smem = kQBytes + 5 * (size_t)kKBytes;  // Q, 2 x (K, V), P
-  cudaFuncSetAttribute(attention_fa_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  const int64_t tpt = kFaRows / p.g;
-  const dim3 grid((unsigned)ceil_div(a->q_tokens, tpt), (unsigned)(a->batch * a->kv_heads));
-  attention_fa_tc_kernel<<<grid, kFaThreads, smem, st>>>(p);
+  cudaFuncSetAttribute(attention_fa2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kF2Smem);
+  const int64_t tpt = 2 * kFaRows / q2.g;
+  const dim3 grid((unsigned)bh, (unsigned)ceil_div(a->q_tokens, tpt));
+  attention_fa2_kernel<<<grid, kF2Threads, kF2Smem, st>>>(q2);
   return check_launch();
 }
 

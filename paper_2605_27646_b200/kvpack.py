@@ -78,8 +78,8 @@ def device_crc32(buf, n: int, out) -> None:
 
     L = nat.lib()
     ws = torch.empty(int(L.hqmq_crc32_workspace_bytes(n)), dtype=torch.uint8, device=buf.device)
-    nat.check(L.hqmq_crc32(buf.data_ptr(), n, out.data_ptr(), ws.data_ptr(), ws.numel(),
-                           nat.stream_handle(buf.device)), "hqmq_crc32")
+    nat.launch(buf.device, "hqmq_crc32", L.hqmq_crc32, buf.data_ptr(), n, out.data_ptr(),
+               ws.data_ptr(), ws.numel())
     buf._crc_ws = ws  # keep the workspace alive until the stream has used it
 
 
@@ -230,18 +230,16 @@ def from_bytes(blob: bytes, device="cuda") -> QuantizedTensor:
     pay = dsection(4, 8 * max(1, n_flag))[: 8 * max(1, n_flag)].view(torch.float16).reshape(
         max(1, n_flag), CHUNK_DIM)
     L = nat.lib()
-    stream = nat.stream_handle(device)
     tok = None
     if outlier:
         tok = torch.zeros(max(1, n_tok), dtype=torch.int32, device=device)
         ws = torch.empty(int(L.hqmq_token_offsets_workspace_bytes(n_tok)), dtype=torch.uint8,
                          device=device)
-        nat.check(L.hqmq_token_offsets(n_tok, shape.chunks_per_vector, fw.data_ptr(),
-                                       tok.data_ptr(), ws.data_ptr(), ws.numel(), stream),
-                  "hqmq_token_offsets")
+        nat.launch(device, "hqmq_token_offsets", L.hqmq_token_offsets, n_tok,
+                   shape.chunks_per_vector, fw.data_ptr(), tok.data_ptr(), ws.data_ptr(), ws.numel())
     err = torch.zeros(1, dtype=torch.int32, device=device)
-    nat.check(L.hqmq_validate_indices(iw.data_ptr(), n_coded, w, config.index_count,
-                                      err.data_ptr(), stream), "hqmq_validate_indices")
+    nat.launch(device, "hqmq_validate_indices", L.hqmq_validate_indices, iw.data_ptr(), n_coded,
+               w, config.index_count, err.data_ptr())
     if int(err.item()) & nat.DEVERR_INDEX:
         raise CorruptData("codeword index out of range")
     meta = torch.tensor([n_coded, n_flag, 0, 0], dtype=torch.int64, device=device)

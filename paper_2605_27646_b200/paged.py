@@ -26,7 +26,7 @@ import math
 
 from . import _native as nat
 from .codebook import CodebookBank
-from .codec import CodecConfig, _bank_for, _torch, encode_tensor
+from .codec import CodecConfig, _bank_for, _torch, check_out, encode_tensor
 from .errors import InvalidArgument
 
 PAGE_TOKENS = 128
@@ -145,6 +145,8 @@ class PagedKVCache:
         q = q.to(device=self.device, dtype=torch.float32).contiguous()
         if out is None:
             out = torch.empty_like(q)
+        else:
+            check_out(out, tuple(q.shape), torch.float32, self.device, "attend out")
         c = self.config
         a = nat.PagedAttentionArgs()
         a.batch, a.q_heads, a.kv_heads, a.head_dim = B, HQ, self.kv_heads, D
@@ -168,7 +170,7 @@ class PagedKVCache:
         ws_bytes = int(L.hqmq_paged_attention_workspace_bytes(ctypes.byref(a)))
         ws = torch.empty(max(1, ws_bytes), dtype=torch.uint8, device=self.device)
         a.workspace, a.workspace_bytes = ws.data_ptr(), ws_bytes
-        nat.check(L.hqmq_attention_decode_paged(ctypes.byref(a), nat.stream_handle(self.device)),
-                  "hqmq_attention_decode_paged")
+        nat.launch(self.device, "hqmq_attention_decode_paged", L.hqmq_attention_decode_paged,
+                   ctypes.byref(a))
         out._ws = ws
         return out

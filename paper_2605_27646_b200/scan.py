@@ -27,7 +27,6 @@ def nearest_scan(dirs, codewords, device=None):
     n, m = d.shape[0], cw.shape[0]
     idx = torch.empty(n, dtype=torch.int64, device=d.device)
     cos = torch.empty(n, dtype=torch.float64, device=d.device)
-    nat.check(nat.lib().hqmq_nearest_scan(d.data_ptr(), n, cw.data_ptr(), m, idx.data_ptr(),
-                                          cos.data_ptr(), nat.stream_handle(d.device)),
-              "hqmq_nearest_scan")
+    nat.launch(d.device, "hqmq_nearest_scan", nat.lib().hqmq_nearest_scan, d.data_ptr(), n,
+               cw.data_ptr(), m, idx.data_ptr(), cos.data_ptr())
     return idx, cos

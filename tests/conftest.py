@@ -42,3 +42,14 @@ def cuda():
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     return torch.device("cuda", 0)
+
+
+def adversarial_fixtures():
+    return sorted(os.path.basename(p)[len("adv_"):-4]
+                  for p in glob.glob(os.path.join(GOLDEN, "adv_*.npz")))
+
+
+def load_adversarial(name):
+    z = np.load(os.path.join(GOLDEN, f"adv_{name}.npz"))
+    meta = json.loads(str(z["meta"]))
+    return meta, {k: z[k] for k in z.files if k != "meta"}

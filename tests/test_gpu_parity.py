@@ -431,10 +431,20 @@ def test_attention_golden(cuda, name):
     bank = m.CodebookBank(0, 24)
     pk = m.encode_tensor(z["k"], codec, role="K", bank=bank)
     pv = m.encode_tensor(z["v"], codec, role="V", bank=bank)
+    q = torch.from_numpy(z["q"])
+    assert q.dtype == torch.float64
     for splits in (0, 1, 3):
+        # dtype=None with an fp64 q is the reference's default: the fp64 path,
+        # held to the reference's own 1e-10 (test_attention.py:83-87)
+        out = m.fused_attend(q, pk, pv, bank, cfg, num_splits=splits)
+        assert out.dtype == torch.float64
+        err = np.max(np.abs(out.cpu().numpy() - z["dense"]))
+        assert err <= 1e-10, (splits, err)
+        assert np.max(np.abs(out.cpu().numpy() - z["fused"])) <= 1e-10
         for precise, tol in ((True, 2e-5), (False, 1e-3)):
-            out = m.fused_attend(torch.from_numpy(z["q"]), pk, pv, bank, cfg, num_splits=splits,
-                                 precise=precise)
+            out = m.fused_attend(q, pk, pv, bank, cfg, num_splits=splits, precise=precise,
+                                 dtype=torch.float32)
+            assert out.dtype == torch.float32
             err = np.max(np.abs(out.double().cpu().numpy() - z["dense"]))
             assert err <= tol, (splits, precise, err)
 
@@ -531,3 +541,78 @@ def test_attention_mismatch_errors(cuda):
         m.fused_attend(q[:, :, :, :8], pk, pv, bank, cfg)
     with pytest.raises(m.InvalidArgument):
         m.fused_attend(q, pk, pv, bank, cfg, tile=0)
+
+
+def test_attention_fp64_contract(cuda, oracle):
+    """fused_attend(dtype=float64) meets the reference's fp64 bound (1e-10,
+    test_attention.py:83-87) against the oracle's dense fp64 attention over the
+    fp64 decode: decode steps, chunked / full causal prefill, GQA, Med3x
+    payloads, odd head_dim, many splits, and large-norm Q/K (LLM-scale logits)."""
+    m = hq()
+    rs = np.random.default_rng(64)
+    for (B, HQ, HKV, TQ, T, D, C, qs) in [(2, 8, 2, 1, 700, 128, None, 1.0),
+                                          (1, 4, 4, 37, 300, 64, 3.0, 1.0),
+                                          (1, 6, 2, 5, 129, 20, None, 30.0),
+                                          (1, 32, 8, 1, 5000, 128, None, 8.0)]:
+        k = rs.standard_normal((B, HKV, T, D)) * qs
+        v = rs.standard_normal((B, HKV, T, D))
+        if C:
+            k[:, :, ::13, :4] *= 50.0
+        q = rs.standard_normal((B, HQ, TQ, D)) * qs
+        codec = m.CodecConfig(64, 4, outlier_multiplier=C)
+        bank = m.CodebookBank(0, 64)
+        pk = m.encode_tensor(k, codec, role="K", bank=bank, layer=1)
+        pv = m.encode_tensor(v, codec, role="V", bank=bank, layer=1)
+        kd = m.decode_tensor(pk, bank, dtype=torch.float64).cpu().numpy()
+        vd = m.decode_tensor(pv, bank, dtype=torch.float64).cpu().numpy()
+        dense = oracle.reference_attend(q, kd, vd, HQ // HKV, causal=True)
+        cfg = m.AttentionConfig(B, HQ, HKV, TQ, T, D)
+        for splits in (0, 1, 7):
+            out = m.fused_attend(q, pk, pv, bank, cfg, num_splits=splits, dtype=torch.float64)
+            err = np.max(np.abs(out.cpu().numpy() - dense))
+            assert err <= 1e-10, ((B, HQ, HKV, TQ, T, D, C, qs), splits, err)
+
+
+def test_output_buffer_validation(cuda):
+    """A caller-supplied `out` must match what the kernel writes."""
+    m = hq()
+    x = torch.randn((1, 2, 64, 128), device=cuda).half()
+    cfg = m.CodecConfig(64, 4)
+    bank = m.CodebookBank(0, 64)
+    qt = m.encode_tensor(x, cfg, bank=bank)
+    good = torch.empty((1, 2, 64, 128), device=cuda, dtype=torch.float16)
+    assert m.decode_tensor(qt, bank, out=good) is good  # dtype taken from out
+    assert torch.equal(good, m.decode_tensor(qt, bank, dtype=torch.float16))
+    for bad, kw in [(torch.empty((1, 2, 64, 128), device=cuda, dtype=torch.float16),
+                     dict(dtype=torch.float32)),
+                    (torch.empty((1, 2, 63, 128), device=cuda), {}),
+                    (torch.empty((1, 2, 128, 64), device=cuda).transpose(2, 3), {}),
+                    (torch.empty((1, 2, 64, 128)), {})]:
+        with pytest.raises(m.InvalidArgument):
+            m.decode_tensor(qt, bank, out=bad, **kw)
+    pk = m.encode_tensor(x, cfg, role="K", bank=bank)
+    pv = m.encode_tensor(x, cfg, role="V", bank=bank)
+    acfg = m.AttentionConfig(1, 8, 2, 1, 64, 128)
+    q = torch.randn((1, 8, 1, 128), device=cuda)
+    with pytest.raises(m.InvalidArgument):
+        m.fused_attend(q, pk, pv, bank, acfg, out=torch.empty((1, 8, 1, 128), device=cuda,
+                                                             dtype=torch.float16))
+    with pytest.raises(m.InvalidArgument):
+        m.fused_attend(q, pk, pv, bank, acfg, out=torch.empty((1, 8, 2, 128), device=cuda))
+
+
+def test_encode_on_side_stream_is_ordered(cuda):
+    """encode_tensor(sync=False) on one stream, consumers on another: the
+    consumers wait for the encode's event."""
+    m = hq()
+    cfg = m.CodecConfig(64, 4)
+    bank = m.CodebookBank(0, 64)
+    x = torch.randn((1, 8, 32768, 128), device=cuda).half()
+    ref = m.encode_tensor(x, cfg, bank=bank)
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        qt = m.encode_tensor(x, cfg, bank=bank, sync=False)
+    assert qt.n_coded == ref.n_coded  # synchronize() waits on the encode's event
+    assert torch.equal(m.decode_tensor(qt, bank), m.decode_tensor(ref, bank))
+    assert m.to_bytes(qt) == m.to_bytes(ref)

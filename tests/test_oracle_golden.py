@@ -11,7 +11,7 @@ import os
 import numpy as np
 import pytest
 
-from conftest import GOLDEN, codec_fixtures, load_codec_fixture
+from conftest import GOLDEN, adversarial_fixtures, codec_fixtures, load_adversarial, load_codec_fixture
 
 FROZEN = "12b2dfad207652800819a0ab439f8ef44c1c5ce33eff0f70979bc4e8b2cc1039"
 
@@ -98,3 +98,16 @@ def test_synth_generators(oracle):
     assert abs(n.max() / med - 150.0) < 1e-6
     g = oracle.gen_gaussian((1, 1, 4, 8), seed=0)
     assert g.shape == (1, 1, 4, 8)
+
+
+@pytest.mark.parametrize("name", adversarial_fixtures())
+def test_oracle_adversarial_matches_reference(oracle, name):
+    """Boundary chunks (tests/golden/make_adversarial.py): top-2 score gaps
+    down to 1e-10 (fp16) and exact ties (fp64) resolve like the reference."""
+    meta, g = load_adversarial(name)
+    assert meta["n_gap_below_1e5"] > meta["n_chunks"] // 2  # really on the boundaries
+    enc = oracle.encode(g["data"], meta["codebook_size"], meta["radius_bits"], seed=meta["seed"],
+                        layer=meta["layer"], role=meta["role"])
+    for f in ("scales", "indices", "quanta"):
+        assert np.array_equal(getattr(enc, f), g[f]), f
+    assert hashlib.sha256(oracle.to_bytes(enc)).hexdigest() == meta["digest"]
