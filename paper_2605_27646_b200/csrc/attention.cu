@@ -19,7 +19,7 @@
 #include <cmath>
 #include <cstdlib>
 
-#include "common.cuh"
+#include "attention.cuh"
 
 namespace hqmq {
 
@@ -29,36 +29,6 @@ constexpr int kRows = 4;         // query rows per CTA (one warp each)
 constexpr int kMaxC = 32;        // head_dim <= 128
 constexpr int kKStride = 4 * kMaxC + 4;  // padded smem row (floats)
 
-struct AttView {
-  const uint16_t* scales;
-  const uint32_t* idxw;
-  const uint32_t* radw;
-  const uint32_t* flagw;
-  const uint16_t* payloads;
-  const uint32_t* tokoff;
-  const float4* table;  // [Hkv][24S]
-  const uint2* table16;  // optional fp16 copy [Hkv][24S]
-  const double* table64;  // [Hkv][24S][4] fp64 (the fp64 path)
-};
-
-struct AttParams {
-  int64_t B, Hq, Hkv, Tq, Tkv, D;
-  int C, S, br, w, g, causal;
-  float scale_log2;
-  int splits;
-  int64_t keys_per_split;
-  int nrows;  // g * Tq
-  const float* q;
-  AttView k, v;
-  float* out;
-  float* part_o;   // [B*Hkv][rows][splits][D]
-  float* part_ml;  // [B*Hkv][rows][splits][2]
-  // paged cache (decode serving layout): per-sequence lengths and the block
-  // table of 128-token pages per (sequence, kv head) row
-  const int32_t* kv_lens;
-  const int32_t* block_table;
-  int max_pages;
-};
 
 __device__ __forceinline__ float4 decode_chunk(const AttView& v, const float4* tab, int64_t tok,
                                                int C, int c, int w, int br, int ncw, float rtop) {
@@ -245,7 +215,7 @@ __global__ void combine_kernel(AttParams p) {
       const float m = p.part_ml[2 * (base + s)];
       if (m != -INFINITY) acc += p.part_o[(base + s) * p.D + d] * exp2f(m - M);
     }
-    o[d] = acc / L;
+    o[d] = acc * p.o_scale / L;
   }
 }
 
@@ -500,70 +470,6 @@ __host__ __device__ inline size_t mma_smem_bytes(int S, int w, int br) {
   return tab + (ring > merge ? ring : merge);
 }
 
-// D(16x8 fp32) += A(16x16 fp16, rows 8-15 zero) * B(16x8 fp16)
-__device__ __forceinline__ void mma_rows8(float (&d)[4], uint32_t a0, uint32_t a2, uint32_t b0,
-                                          uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
-      "{%8,%9}, {%0,%1,%2,%3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a0), "r"(0u), "r"(a2), "r"(0u), "r"(b0), "r"(b1));
-}
-__device__ __forceinline__ void mma_full(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
-                                         uint32_t a3, uint32_t b0, uint32_t b1) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
-      "{%8,%9}, {%0,%1,%2,%3};"
-      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
-}
-__device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
-  const __half2 h = __floats2half2_rn(lo, hi);
-  return *reinterpret_cast<const uint32_t*>(&h);
-}
-// (q, q) as fp16x2 for an integer radius code q < 1024, without the
-// quarter-rate I2F: 0x6400 | q is the fp16 1024 + q (exact), minus 1024.
-__device__ __forceinline__ uint32_t code_half2(uint32_t q) {
-  const uint32_t biased = (q * 0x10001u) | 0x64006400u;
-  const __half2 r = __hsub2(*reinterpret_cast<const __half2*>(&biased), __float2half2_rn(1024.f));
-  return *reinterpret_cast<const uint32_t*>(&r);
-}
-__device__ __forceinline__ uint32_t hmul2u(uint32_t a, uint32_t b) {
-  const __half2 r = __hmul2(*reinterpret_cast<const __half2*>(&a), *reinterpret_cast<const __half2*>(&b));
-  return *reinterpret_cast<const uint32_t*>(&r);
-}
-
-// N codes of WIDTH bits starting at bit `bit` of a shared-memory stream
-// (LSB-first 32-bit words): NW words are loaded, aligned by one runtime
-// funnel shift, then every code sits at a compile-time position.
-// The run starts at bit key*32*WIDTH + t*N*WIDTH (t < NT), so its in-word
-// shift is (t*N*WIDTH) & 31 and the worst case is known at compile time.
-__host__ __device__ constexpr int max_run_shift(int n, int width, int nt) {
-  int m = 0;
-  for (int t = 0; t < nt; ++t) m = ((t * n * width) & 31) > m ? ((t * n * width) & 31) : m;
-  return m;
-}
-template <int N, int WIDTH, int NT>
-struct CodeRun {
-  static constexpr int kSpan = max_run_shift(N, WIDTH, NT) + N * WIDTH;  // bits to cover
-  static constexpr int kNW = (kSpan + 31) / 32;                          // words loaded
-  uint32_t r[kNW];
-  __device__ __forceinline__ void load(const uint32_t* __restrict__ s, uint32_t bit) {
-    const uint32_t* p = s + (bit >> 5);
-    const uint32_t sh = bit & 31;
-    uint32_t w[kNW + 1];
-#pragma unroll
-    for (int i = 0; i < kNW; ++i) w[i] = p[i];
-    w[kNW] = 0u;
-#pragma unroll
-    for (int i = 0; i < kNW; ++i) r[i] = __funnelshift_r(w[i], w[i + 1], sh);
-  }
-  __device__ __forceinline__ uint32_t get(int i) const {
-    const int b = i * WIDTH, wi = b >> 5, sh = b & 31;
-    uint32_t v = sh == 0 ? r[wi] : __funnelshift_r(r[wi], wi + 1 < kNW ? r[wi + 1] : 0u, sh);
-    return WIDTH == 32 ? v : (v & ((1u << WIDTH) - 1u));
-  }
-};
 
 template <int W, int BR, bool kPaged = false>
 __global__ void __launch_bounds__(kMThreads, 2) attention_mma_kernel(AttParams p) {
@@ -841,6 +747,24 @@ __global__ void __launch_bounds__(kMThreads, 2) attention_mma_kernel(AttParams p
 size_t prefill_tc_workspace(const hqmq_attention_args* a);
 bool prefill_tc_applicable(const hqmq_attention_args* a);
 int launch_prefill_tc(const hqmq_attention_args* a, cudaStream_t st);
+// attention_cluster.cu: the K/V CTA-pair decode kernel
+bool pair_applicable(int64_t head_dim, int64_t nrows, int64_t tkv, int S, int w, int br,
+                     bool flags, const void* t16k, const void* t16v);
+size_t pair_workspace(int64_t bhkv, int64_t nrows, int64_t tkv);
+int launch_pair_attention(AttParams p, int64_t max_tkv, cudaStream_t st);
+static bool al16(const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; }
+static bool pair_ok(const hqmq_attention_args* a) {
+#ifdef HQMQ_DISABLE_PAIR
+  return false;
+#endif
+  const int64_t nrows = a->q_heads / a->kv_heads * a->q_tokens;
+  return !a->precise &&
+         pair_applicable(a->head_dim, nrows, a->kv_tokens, a->codebook_size, a->index_bits,
+                         a->radius_bits, a->k.flag_words || a->v.flag_words, a->k.joint_f16,
+                         a->v.joint_f16) &&
+         al16(a->k.index_words) && al16(a->k.radius_words) && al16(a->k.scales) &&
+         al16(a->v.index_words) && al16(a->v.radius_words) && al16(a->v.scales);
+}
 
 namespace {
 
@@ -887,6 +811,7 @@ bool plan_att(const hqmq_attention_args* a, AttPlan& pl) {
   const size_t elt = a->precise == 2 ? sizeof(double) : sizeof(float);
   pl.ws = pl.splits > 1 ? (size_t)parts * (a->head_dim + 2) * elt + 256 : 0;
   if (prefill_tc_applicable(a)) pl.ws = std::max(pl.ws, prefill_tc_workspace(a));
+  if (pair_ok(a)) pl.ws = std::max(pl.ws, pair_workspace(a->batch * a->kv_heads, nrows, a->kv_tokens));
   return true;
 }
 
@@ -917,6 +842,7 @@ int hqmq_attention_decode(const hqmq_attention_args* a, void* stream) {
   p.C = (int)(a->head_dim / 4); p.S = a->codebook_size; p.br = a->radius_bits; p.w = a->index_bits;
   p.g = (int)(a->q_heads / a->kv_heads); p.causal = a->causal;
   p.scale_log2 = (float)(a->scale * 1.4426950408889634);
+  p.o_scale = 1.0f;
   p.splits = pl.splits; p.keys_per_split = pl.keys_per_split;
   p.nrows = (int)(p.g * a->q_tokens);
   p.kv_lens = nullptr; p.block_table = nullptr; p.max_pages = 0;
@@ -958,7 +884,6 @@ int hqmq_attention_decode(const hqmq_attention_args* a, void* stream) {
   p.part_ml = ws ? ws + parts * a->head_dim : nullptr;
   const size_t tab_bytes = 2 * (size_t)kGroupOrder * a->codebook_size * sizeof(float4);
   const dim3 grid((unsigned)pl.splits, (unsigned)(a->batch * a->kv_heads), (unsigned)pl.row_groups);
-  auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
   const size_t msmem = mma_smem_bytes(a->codebook_size, a->index_bits, a->radius_bits);
   const bool mma_path = a->head_dim == 128 && !a->k.flag_words && !a->v.flag_words &&
                         p.nrows <= 8 && a->kv_tokens % 8 == 0 && pl.keys_per_split % 64 == 0 &&
@@ -980,6 +905,10 @@ int hqmq_attention_decode(const hqmq_attention_args* a, void* stream) {
     default: break;
   }
   if (prefill_tc_applicable(a)) return launch_prefill_tc(a, st);
+  if (pair_ok(a)) {
+    p.part_o = ws;
+    return launch_pair_attention(p, a->kv_tokens, st);
+  }
   if (mma_path && mk) {
     cudaFuncSetAttribute(mk, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     mk<<<dim3((unsigned)pl.splits, (unsigned)(a->batch * a->kv_heads)), kMThreads, msmem, st>>>(p);
@@ -1005,6 +934,13 @@ struct PagedPlan {
   int64_t keys_per_split;
   size_t ws;
 };
+bool paged_pair_ok(const hqmq_paged_attention_args* a) {
+#ifdef HQMQ_DISABLE_PAIR
+  return false;
+#endif
+  return hqmq::pair_applicable(a->head_dim, a->q_heads / a->kv_heads, a->max_kv_tokens, a->codebook_size,
+                         a->index_bits, a->radius_bits, false, a->k.joint_f16, a->v.joint_f16);
+}
 bool plan_paged(const hqmq_paged_attention_args* a, PagedPlan& pl) {
   using namespace hqmq;
   if (!a || a->batch < 1 || a->q_heads < 1 || a->kv_heads < 1 || a->head_dim != 128) return false;
@@ -1030,6 +966,7 @@ bool plan_paged(const hqmq_paged_attention_args* a, PagedPlan& pl) {
   pl.splits = (int)ceil_div(a->max_kv_tokens, pl.keys_per_split);
   const int64_t nrows = a->q_heads / a->kv_heads;
   pl.ws = pl.splits > 1 ? (size_t)ctas * nrows * pl.splits * (128 + 2) * sizeof(float) + 256 : 0;
+  if (paged_pair_ok(a)) pl.ws = std::max(pl.ws, pair_workspace(ctas, nrows, a->max_kv_tokens));
   return true;
 }
 }  // namespace
@@ -1054,6 +991,7 @@ int hqmq_attention_decode_paged(const hqmq_paged_attention_args* a, void* stream
   p.D = 128; p.C = 32; p.S = a->codebook_size; p.br = a->radius_bits; p.w = a->index_bits;
   p.g = (int)(a->q_heads / a->kv_heads); p.causal = 1;
   p.scale_log2 = (float)(a->scale * 1.4426950408889634);
+  p.o_scale = 1.0f;
   p.splits = pl.splits; p.keys_per_split = pl.keys_per_split;
   p.nrows = p.g;
   p.q = a->q;
@@ -1074,6 +1012,7 @@ int hqmq_attention_decode_paged(const hqmq_paged_attention_args* a, void* stream
   p.part_o = ws;
   p.part_ml = ws ? ws + parts * 128 : nullptr;
   p.kv_lens = a->kv_lens; p.block_table = a->block_table; p.max_pages = a->max_pages;
+  if (paged_pair_ok(a)) return launch_pair_attention(p, a->max_kv_tokens, st);
   void (*mk)(AttParams) = nullptr;
   switch (a->index_bits * 16 + a->radius_bits) {
     case 9 * 16 + 4: mk = attention_mma_kernel<9, 4, true>; break;

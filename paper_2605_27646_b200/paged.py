@@ -60,10 +60,14 @@ class PagedKVCache:
         self.pages = {}
         for role in ("K", "V"):
             self.pages[role] = {
-                "index": torch.zeros((self.num_pages, PAGE_TOKENS * w), dtype=torch.int32, device=dev),
-                "radius": torch.zeros((self.num_pages, PAGE_TOKENS * br), dtype=torch.int32,
+                # + one spare page: the attention kernels read a few words past a
+                # token's codes, also for the last token of the last page
+                "index": torch.zeros((self.num_pages + 1, PAGE_TOKENS * w), dtype=torch.int32,
+                                     device=dev),
+                "radius": torch.zeros((self.num_pages + 1, PAGE_TOKENS * br), dtype=torch.int32,
                                       device=dev),
-                "scales": torch.zeros((self.num_pages, PAGE_TOKENS), dtype=torch.float16, device=dev),
+                "scales": torch.zeros((self.num_pages + 1, PAGE_TOKENS), dtype=torch.float16,
+                                      device=dev),
             }
         self.block_table = torch.full((batch, kv_heads, self.max_pages), -1, dtype=torch.int32,
                                       device=dev)

@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 __global__ void st_plain(uint4* p, size_t n) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
@@ -38,8 +39,9 @@ __global__ void rd_wr(const uint4* a, uint4* b, size_t n) {
     b[i] = a[i];
 }
 
-int main() {
-  const size_t bytes = 256ull << 20;
+int main(int argc, char** argv) {
+  const size_t bytes = (argc > 1 ? (size_t)atoll(argv[1]) : 256ull) << 20;  // MiB
+  printf("buffer %zu MiB\n", bytes >> 20);
   char *a, *b;
   cudaMalloc(&a, bytes);
   cudaMalloc(&b, bytes);
