@@ -118,6 +118,12 @@ __device__ __forceinline__ uint2 lds64(uint32_t addr) {
   asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
   return v;
 }
+// 2^x on the MUFU (flushes denormal results to 0: fine for softmax weights)
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 __device__ __forceinline__ uint32_t hmul2_raw(uint32_t a, uint32_t b) {
   uint32_t r;
   asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
@@ -250,26 +256,37 @@ template <bool kPaged>
 __device__ __forceinline__ int64_t block_token(const AttParams& p, const Item& it, int k0) {
   return token_of<kPaged>(p, it, k0);
 }
+// per-lane word offsets of a K block (block-relative keys ka, kb)
+struct KOffs {
+  uint32_t ia, ib, ra, rb, ka, kb;
+};
 template <int W, int BR>
-__device__ __forceinline__ void k_load(KRegs<W, BR>& r, const AttParams& p, int64_t tok0, int ka, int kb,
-                                       int t4) {
+__device__ __forceinline__ KOffs k_offs(int ka, int kb, int t4) {
+  const uint32_t wo = ((uint32_t)t4 * 8u * W) >> 5, ro = ((uint32_t)t4 * 8u * BR) >> 5;
+  return KOffs{(uint32_t)ka * W + wo, (uint32_t)kb * W + wo, (uint32_t)ka * BR + ro,
+               (uint32_t)kb * BR + ro, (uint32_t)ka, (uint32_t)kb};
+}
+template <int W, int BR>
+__device__ __forceinline__ void k_load(KRegs<W, BR>& r, const AttParams& p, int64_t tok0, const KOffs& o) {
   using R = KRegs<W, BR>;
-  const uint32_t* ib = p.k.idxw + tok0 * W + (((uint32_t)t4 * 8u * W) >> 5);
-  const uint32_t* rb = p.k.radw + tok0 * BR + (((uint32_t)t4 * 8u * BR) >> 5);
+  const uint32_t* ib = p.k.idxw + tok0 * W;  // warp-uniform block bases
+  const uint32_t* rb = p.k.radw + tok0 * BR;
+  const __half* ks = reinterpret_cast<const __half*>(p.k.scales) + tok0;
+  const __half* vs = reinterpret_cast<const __half*>(p.v.scales) + tok0;
 #pragma unroll
   for (int i = 0; i < R::Run::kNW; ++i) {
-    r.ia[i] = __ldg(ib + ka * W + i);
-    r.ib[i] = __ldg(ib + kb * W + i);
+    r.ia[i] = ib[o.ia + i];
+    r.ib[i] = ib[o.ib + i];
   }
 #pragma unroll
   for (int i = 0; i < R::kRW; ++i) {
-    r.ra[i] = __ldg(rb + ka * BR + i);
-    r.rb[i] = __ldg(rb + kb * BR + i);
+    r.ra[i] = rb[o.ra + i];
+    r.rb[i] = rb[o.rb + i];
   }
-  r.ska = __ldg(reinterpret_cast<const __half*>(p.k.scales) + tok0 + ka);
-  r.skb = __ldg(reinterpret_cast<const __half*>(p.k.scales) + tok0 + kb);
-  r.sva = __ldg(reinterpret_cast<const __half*>(p.v.scales) + tok0 + ka);
-  r.svb = __ldg(reinterpret_cast<const __half*>(p.v.scales) + tok0 + kb);
+  r.ska = ks[o.ka];
+  r.skb = ks[o.kb];
+  r.sva = vs[o.ka];
+  r.svb = vs[o.kb];
 }
 
 // --------------------------------------------------------------- V block
@@ -280,20 +297,34 @@ struct VRegs {
   uint32_t iw[4][Run::kNW];
   uint32_t rw[4][2];
 };
+// per-lane word offsets of a V block: keys 2t4, 2t4+1, 2t4+8, 2t4+9 (clamped)
+struct VOffs {
+  uint32_t i[4], r[4];
+};
 template <int W, int BR>
-__device__ __forceinline__ void v_load(VRegs<W, BR>& r, const AttParams& p, int64_t tok0, int klast,
-                                       int g4, int t4) {
-  using R = VRegs<W, BR>;
-  const uint32_t rbit = (uint32_t)g4 * 4u * BR;
-  const uint32_t* ib = p.v.idxw + tok0 * W + (((uint32_t)g4 * 4u * W) >> 5);
-  const uint32_t* rb = p.v.radw + tok0 * BR + (rbit >> 5);
+__device__ __forceinline__ VOffs v_offs(int klast, int g4, int t4) {
+  VOffs o;
+  const uint32_t wo = ((uint32_t)g4 * 4u * W) >> 5, ro = ((uint32_t)g4 * 4u * BR) >> 5;
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
-    const int k = min((e >> 1) * 8 + t4 * 2 + (e & 1), klast);  // block-relative key
+    const int k = min((e >> 1) * 8 + t4 * 2 + (e & 1), klast);
+    o.i[e] = (uint32_t)k * W + wo;
+    o.r[e] = (uint32_t)k * BR + ro;
+  }
+  return o;
+}
+template <int W, int BR>
+__device__ __forceinline__ void v_load(VRegs<W, BR>& r, const AttParams& p, int64_t tok0, const VOffs& o,
+                                       bool two) {
+  using R = VRegs<W, BR>;
+  const uint32_t* ib = p.v.idxw + tok0 * W;  // warp-uniform block bases
+  const uint32_t* rb = p.v.radw + tok0 * BR;
 #pragma unroll
-    for (int i = 0; i < R::Run::kNW; ++i) r.iw[e][i] = __ldg(ib + k * W + i);
-    r.rw[e][0] = __ldg(rb + k * BR);
-    r.rw[e][1] = BR * 4 + (rbit & 31) > 32 ? __ldg(rb + k * BR + 1) : 0u;
+  for (int e = 0; e < 4; ++e) {
+#pragma unroll
+    for (int i = 0; i < R::Run::kNW; ++i) r.iw[e][i] = ib[o.i[e] + i];
+    r.rw[e][0] = rb[o.r[e]];
+    r.rw[e][1] = two ? rb[o.r[e] + 1] : 0u;
   }
 }
 
@@ -380,10 +411,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCThreads, 1)
         vis_min = clampv(off);
       }
       const uint32_t sh_i = ((uint32_t)t4 * 8u * W) & 31u, sh_r = ((uint32_t)t4 * 8u * BR) & 31u;
-      float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;  // l: this lane's partial sums
+      // running maxima start at a finite floor so that fully masked rows give
+      // p = 2^-inf = 0 without special cases
+      float m0 = -1e30f, m1 = -1e30f, l0 = 0.f, l1 = 0.f;  // l: this lane's partial sums
+      const KOffs ko_full = k_offs<W, BR>(g4, g4 + 8, t4);
       auto kload = [&](R& r, int jb) {
         const int k0 = jb * kBK, klast = it.kend_rel - 1 - k0;
-        k_load<W, BR>(r, p, block_token<kPaged>(p, it, k0), min(g4, klast), min(g4 + 8, klast), t4);
+        if (klast >= kBK - 1)
+          k_load<W, BR>(r, p, block_token<kPaged>(p, it, k0), ko_full);
+        else  // the item's partial last block: clamp to its last key
+          k_load<W, BR>(r, p, block_token<kPaged>(p, it, k0), k_offs<W, BR>(min(g4, klast), min(g4 + 8, klast), t4));
       };
       R nx;
       if (warp < it.nblk) kload(nx, warp);
@@ -465,22 +502,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCThreads, 1)
         // (P stays <= 2^8 in fp16 and most blocks need no rescale)
         float a0 = 1.f, a1 = 1.f;
         if (x0 > m0 + kLazy) {
-          a0 = m0 == -INFINITY ? 0.f : exp2f(m0 - x0);
+          a0 = ex2(m0 - x0);
           m0 = x0;
         }
         if (x1 > m1 + kLazy) {
-          a1 = m1 == -INFINITY ? 0.f : exp2f(m1 - x1);
+          a1 = ex2(m1 - x1);
           m1 = x1;
         }
-        float p00 = 0.f, p10 = 0.f, p01 = 0.f, p11 = 0.f;
-        if (m0 != -INFINITY) {
-          p00 = exp2f(s00 - m0);
-          p10 = exp2f(s10 - m0);
-        }
-        if (m1 != -INFINITY) {
-          p01 = exp2f(s01 - m1);
-          p11 = exp2f(s11 - m1);
-        }
+        const float p00 = ex2(s00 - m0), p10 = ex2(s10 - m0);
+        const float p01 = ex2(s01 - m1), p11 = ex2(s11 - m1);
         l0 = l0 * a0 + (p00 + p10);
         l1 = l1 * a1 + (p01 + p11);
         // P (with sigma_v; 2^9 / top is applied by the combine) to the V twin
@@ -517,9 +547,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCThreads, 1)
 #pragma unroll
       for (int i = 0; i < 8; ++i) oT[i][0] = oT[i][1] = oT[i][2] = oT[i][3] = 0.f;
       const uint32_t sh_i = ((uint32_t)g4 * 4u * W) & 31u, sh_r = ((uint32_t)g4 * 4u * BR) & 31u;
+      const bool two = BR * 4 + (((uint32_t)g4 * 4u * BR) & 31u) > 32u;  // radius run spans 2 words
+      const VOffs vo_full = v_offs<W, BR>(kBK - 1, g4, t4);
       auto vload = [&](R& r, int jb) {
-        const int k0 = jb * kBK;
-        v_load<W, BR>(r, p, block_token<kPaged>(p, it, k0), it.kend_rel - 1 - k0, g4, t4);
+        const int k0 = jb * kBK, klast = it.kend_rel - 1 - k0;
+        if (klast >= kBK - 1)
+          v_load<W, BR>(r, p, block_token<kPaged>(p, it, k0), vo_full, two);
+        else
+          v_load<W, BR>(r, p, block_token<kPaged>(p, it, k0), v_offs<W, BR>(klast, g4, t4), two);
       };
       R nx;
       if (warp < it.nblk) vload(nx, warp);
