@@ -748,7 +748,7 @@ size_t prefill_tc_workspace(const hqmq_attention_args* a);
 bool prefill_tc_applicable(const hqmq_attention_args* a);
 int launch_prefill_tc(const hqmq_attention_args* a, cudaStream_t st);
 // attention_cluster.cu: the K/V CTA-pair decode kernel
-bool pair_applicable(int64_t head_dim, int64_t nrows, int64_t tkv, int S, int w, int br,
+bool pair_applicable(int64_t bhkv, int64_t head_dim, int64_t nrows, int64_t tkv, int S, int w, int br,
                      bool flags, const void* t16k, const void* t16v);
 size_t pair_workspace(int64_t bhkv, int64_t nrows, int64_t tkv);
 int launch_pair_attention(AttParams p, int64_t max_tkv, cudaStream_t st);
@@ -759,7 +759,7 @@ static bool pair_ok(const hqmq_attention_args* a) {
 #endif
   const int64_t nrows = a->q_heads / a->kv_heads * a->q_tokens;
   return !a->precise &&
-         pair_applicable(a->head_dim, nrows, a->kv_tokens, a->codebook_size, a->index_bits,
+         pair_applicable(a->batch * a->kv_heads, a->head_dim, nrows, a->kv_tokens, a->codebook_size, a->index_bits,
                          a->radius_bits, a->k.flag_words || a->v.flag_words, a->k.joint_f16,
                          a->v.joint_f16) &&
          al16(a->k.index_words) && al16(a->k.radius_words) && al16(a->k.scales) &&
@@ -938,7 +938,7 @@ bool paged_pair_ok(const hqmq_paged_attention_args* a) {
 #ifdef HQMQ_DISABLE_PAIR
   return false;
 #endif
-  return hqmq::pair_applicable(a->head_dim, a->q_heads / a->kv_heads, a->max_kv_tokens, a->codebook_size,
+  return hqmq::pair_applicable(a->batch * a->kv_heads, a->head_dim, a->q_heads / a->kv_heads, a->max_kv_tokens, a->codebook_size,
                          a->index_bits, a->radius_bits, false, a->k.joint_f16, a->v.joint_f16);
 }
 bool plan_paged(const hqmq_paged_attention_args* a, PagedPlan& pl) {

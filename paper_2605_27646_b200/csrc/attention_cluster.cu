@@ -678,9 +678,13 @@ void pair_plan(int64_t rows, int64_t tkv, int& nsplit, int64_t& kps) {
   nsplit = (int)ceil_div(tkv, kps);
 }
 
-bool pair_applicable(int64_t head_dim, int64_t nrows, int64_t tkv, int S, int w, int br,
+bool pair_applicable(int64_t bhkv, int64_t head_dim, int64_t nrows, int64_t tkv, int S, int w, int br,
                      bool flags, const void* t16k, const void* t16v) {
   if (head_dim != 128 || flags || nrows > 8 || tkv < 1 || !t16k || !t16v) return false;
+  // each CTA replicates its table into 192 KB of shared memory: worth it from
+  // ~4M cached keys (B = 32 x 8 heads x 16k); smaller caches keep the
+  // single-CTA kernel (measured: B=1 x 8 x 32k 0.047 vs 0.134 ms)
+  if (bhkv * tkv < (int64_t(1) << 22)) return false;
   if ((int64_t)kGroupOrder * S > kMaxCw) return false;
   switch (w * 16 + br) {
     case 9 * 16 + 4: case 10 * 16 + 4: case 11 * 16 + 4: case 11 * 16 + 6: case 11 * 16 + 3:

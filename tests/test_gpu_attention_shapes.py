@@ -99,3 +99,67 @@ def test_c3_med3x_decode_attention(cuda, oracle):
     check_rows(m, oracle, q, fast, pk, pv, bank, rows, HQ // HKV, 1e-3, rel=True)
     exact = m.fused_attend(q.double(), pk, pv, bank, acfg)
     check_rows(m, oracle, q, exact, pk, pv, bank, rows, HQ // HKV, 1e-10)
+
+
+@pytest.mark.parametrize("B,HQ,HKV,TQ,T,causal", [
+    (16, 32, 8, 2, 32768, True),    # T_q = 2 (speculative decode): 8 rows, causal offsets
+    (8, 64, 8, 1, 65536, True),     # GQA 8
+    (32, 8, 8, 1, 16392, False),    # no GQA, T % 16 != 0 (partial last block), non-causal
+])
+def test_pair_kernel_shapes(cuda, oracle, B, HQ, HKV, TQ, T, causal):
+    """Shapes above the K/V CTA-pair kernel's size threshold (>= 4M cached
+    keys) with the row / block edge cases it must mask."""
+    import paper_2605_27646_b200 as m
+
+    D = 128
+    g = torch.Generator(device=cuda).manual_seed(B * T + HQ)
+    cfg = m.CodecConfig(64, 4)
+    bank = m.CodebookBank(0, 64)
+    k = torch.randn((B, HKV, T, D), generator=g, device=cuda, dtype=torch.float16)
+    pk = m.encode_tensor(k, cfg, role="K", bank=bank, layer=3)
+    del k
+    v = torch.randn((B, HKV, T, D), generator=g, device=cuda, dtype=torch.float16)
+    pv = m.encode_tensor(v, cfg, role="V", bank=bank, layer=3)
+    del v
+    q = torch.randn((B, HQ, TQ, D), generator=g, device=cuda)
+    acfg = m.AttentionConfig(B, HQ, HKV, TQ, T, D, causal=causal)
+    out = m.fused_attend(q, pk, pv, bank, acfg)
+    rows = [0, B - 1]
+    kd = decoded_rows(m, pk, bank, rows)
+    vd = decoded_rows(m, pv, bank, rows)
+    dense = oracle.reference_attend(q[rows].double().cpu().numpy(), kd, vd, HQ // HKV, causal=causal)
+    err = np.abs(out[rows].double().cpu().numpy() - dense).max()
+    assert err <= 1e-3, err
+
+
+def test_pair_kernel_paged_ragged(cuda, oracle):
+    """The serving layout through the pair kernel: 128-token pages in random
+    order, ragged sequence lengths (partial last pages, lengths not a multiple
+    of 16), against the oracle per sequence."""
+    import paper_2605_27646_b200 as m
+
+    B, HQ, HKV, D = 24, 32, 8, 128
+    g = torch.Generator(device=cuda).manual_seed(11)
+    cfg = m.CodecConfig(64, 4)
+    bank = m.CodebookBank(0, 64)
+    lens = [int(x) for x in torch.randint(16000, 32768, (B,), generator=g, device=cuda).tolist()]
+    lens[0], lens[1] = 32768, 20001
+    cache = m.PagedKVCache(cfg, B, HKV, max_tokens=32768, bank=bank, page_order_seed=5, device=cuda)
+    assert B * HKV * max(lens) >= 1 << 22  # the pair kernel's regime
+    seqs_k, seqs_v = {}, {}
+    for b, n in enumerate(lens):
+        k = torch.randn((1, HKV, n, D), generator=g, device=cuda).half()
+        v = torch.randn((1, HKV, n, D), generator=g, device=cuda).half()
+        cache.append(k, v, seqs=[b])
+        if b in (0, 1, B - 1):
+            seqs_k[b], seqs_v[b] = k, v
+    q = torch.randn((B, HQ, 1, D), generator=g, device=cuda)
+    out = cache.attend(q)
+    for b in seqs_k:
+        pk = m.encode_tensor(seqs_k[b], cfg, role="K", bank=bank)
+        pv = m.encode_tensor(seqs_v[b], cfg, role="V", bank=bank)
+        kd = m.decode_tensor(pk, bank, dtype=torch.float64).cpu().numpy()
+        vd = m.decode_tensor(pv, bank, dtype=torch.float64).cpu().numpy()
+        dense = oracle.reference_attend(q[b:b + 1].double().cpu().numpy(), kd, vd, HQ // HKV, causal=True)
+        err = np.abs(out[b:b + 1].double().cpu().numpy() - dense).max()
+        assert err <= 1e-3, (b, err)
