@@ -99,7 +99,7 @@ int hqmq_nearest_scan(const double* dirs, int64_t n, const double* codewords, in
  * >= ceil(n_chunks*radius_bits/32)+1, flag_words >= ceil(n_chunks/32)+1,
  * payloads >= n_chunks rows (or the caller's bound), all zero-filled by
  * hqmq_encode itself.  counters[0] = n_coded, counters[1] = n_payload rows
- * (int64, device).  Tables are prepared by the host from the numpy codebooks
+ * (int64, device); counters and error_word are zeroed by hqmq_encode.  Tables are prepared by the host from the numpy codebooks
  * (codebook.py:53-81):
  *   rot_f32   [heads][S][16] fp32: the conj(secondary) rotation as 8 float2
  *             pairs (see csrc/encode.cu)

@@ -173,7 +173,13 @@ def check(status: int, what: str) -> None:
         raise NativeError(f"{what}: {msg} {last}".strip())
 
 
+_cuda_ok = False
+
+
 def require_cuda(device) -> None:
+    global _cuda_ok
+    if _cuda_ok:
+        return
     import torch
 
     if not torch.cuda.is_available():
@@ -181,6 +187,7 @@ def require_cuda(device) -> None:
             "no CUDA device: the HQMQ codec runs only on the sm_100a kernels (no CPU fallback)"
         )
     lib()
+    _cuda_ok = True
 
 
 def stream_handle(device=None) -> int:
@@ -196,8 +203,12 @@ def launch(device, what: str, fn, *args) -> None:
     thread whose current device is cuda:0)."""
     import torch
 
-    dev = torch.device(device)
-    if dev.index is None:
-        dev = torch.device("cuda", torch.cuda.current_device())
-    with torch.cuda.device(dev):
-        check(fn(*args, torch.cuda.current_stream(dev).cuda_stream), what)
+    dev = device if isinstance(device, torch.device) else torch.device(device)
+    cur = torch.cuda.current_device()
+    if dev.index is None or dev.index == cur:  # the common case: no device switch
+        status = fn(*args, torch.cuda.current_stream().cuda_stream)
+    else:
+        with torch.cuda.device(dev):
+            status = fn(*args, torch.cuda.current_stream(dev).cuda_stream)
+    if status:
+        check(status, what)

@@ -142,21 +142,27 @@ class QuantizedTensor:
         self._n_fixup = None
         self._dense = None
         self._ready = None  # CUDA event recorded on the encode's stream
+        self._ready_stream = None  # ... and that stream's handle
+        self._dc = None  # decode fast path: (bank, DecodeArgs template, tables, error word)
 
     # ------------------------------------------------------------ sync
     def wait(self) -> None:
         """Order the current stream of this tensor's device after the encode
-        (a no-op when the encode ran on the same stream).  Every device
-        consumer (decode, attention, packing, append) calls it first."""
-        if self._ready is not None:
-            _torch().cuda.current_stream(self.device).wait_event(self._ready)
+        (a no-op when the encode ran on the same stream or has been waited
+        for).  Every device consumer (decode, attention, packing, append)
+        calls it first."""
+        ev = self._ready
+        if ev is not None:
+            s = _torch().cuda.current_stream(self.device)
+            if s.cuda_stream != self._ready_stream:
+                s.wait_event(ev)
 
     def synchronize(self) -> "QuantizedTensor":
         """Wait for the encode, read its counters and raise its errors."""
         if self._n_coded is None:
             if self._ready is not None:
                 self._ready.synchronize()
-            self.wait()
+                self._ready = None  # complete: later consumers need no ordering
             meta = self._meta.cpu().tolist()
             self._n_coded, self._n_payload, self._n_fixup = int(meta[0]), int(meta[1]), int(meta[2])
             err = int(meta[3]) & 0xFFFFFFFF
@@ -240,9 +246,12 @@ class QuantizedTensor:
         return a
 
     def packed_view(self, bank: CodebookBank) -> nat.PackedView:
+        self.wait()
+        pv = self.__dict__.get("_pv")
+        if pv is not None and pv[0] is bank:
+            return pv[1]
         tabs = bank.device_tables(self.layer, self.head_base, self.shape.heads, self.role,
                                   self.device)
-        self.wait()
         v = nat.PackedView()
         v.scales = self.scales.data_ptr()
         v.index_words = self.index_words.data_ptr()
@@ -253,6 +262,7 @@ class QuantizedTensor:
         v.joint_f32 = tabs["joint_f32"].data_ptr()
         v.joint_f16 = tabs["joint_f16"].data_ptr()
         v.joint_f64 = tabs["joint_f64"].data_ptr()
+        self._pv = (bank, v, tabs)
         return v
 
     # ---------------------------------------------------------- sections
@@ -337,6 +347,8 @@ class QuantizedTensor:
 # --------------------------------------------------------------- helpers
 def same_device(a, b) -> bool:
     """torch.device equality with an index-less 'cuda' meaning the current device."""
+    if a == b:
+        return True
     torch = _torch()
     a, b = torch.device(a), torch.device(b)
     if a.type != b.type:
@@ -358,7 +370,7 @@ def check_out(out, shape, dtype, device, what: str = "out") -> None:
         raise InvalidArgument(f"{what} has dtype {out.dtype}, expected {dtype}")
     if tuple(out.shape) != tuple(shape):
         raise InvalidArgument(f"{what} has shape {tuple(out.shape)}, expected {tuple(shape)}")
-    if not out.is_cuda or not same_device(out.device, device):
+    if not out.is_cuda or (out.device != device and not same_device(out.device, device)):
         raise InvalidArgument(f"{what} must live on {device}, got {out.device}")
     if not out.is_contiguous():
         raise InvalidArgument(f"{what} must be contiguous")
@@ -387,8 +399,11 @@ def _as_device_4d(data, device):
     nat.require_cuda(device)
     if device is None:
         device = data.device if data.is_cuda else torch.device("cuda", torch.cuda.current_device())
+    device = torch.device(device)
+    if device.index is None:
+        device = torch.device("cuda", torch.cuda.current_device())
     data = data.to(device=device, non_blocking=True).contiguous()
-    return data, TensorShape(*data.shape), torch.device(device)
+    return data, TensorShape(*data.shape), device
 
 
 SEARCH_PATHS = {"auto": nat.SEARCH_AUTO, "cuda_core": nat.SEARCH_CUDA_CORE,
@@ -433,7 +448,7 @@ def encode_tensor(data, config: CodecConfig, layer: int = 0, role: str = "K",
     else:
         cap = 1
     pay = torch.empty((cap, 4), dtype=torch.float16, device=device)
-    meta = torch.zeros(4, dtype=torch.int64, device=device)
+    meta = torch.empty(4, dtype=torch.int64, device=device)  # zeroed by hqmq_encode
     tabs = bank.device_tables(layer, head_base, shape.heads, role, device)
     a = nat.EncodeArgs()
     a.batch, a.heads, a.tokens, a.head_dim = shape.batch, shape.heads, shape.tokens, shape.head_dim
@@ -457,29 +472,33 @@ def encode_tensor(data, config: CodecConfig, layer: int = 0, role: str = "K",
     a.flag_capacity_words = fw.numel() if ext else 0
     L = nat.lib()
     ws_bytes = int(L.hqmq_encode_workspace_bytes(ctypes.byref(a)))
-    ws = torch.empty(max(1, ws_bytes), dtype=torch.uint8, device=device)
-    a.workspace, a.workspace_bytes = ws.data_ptr(), ws_bytes
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=device) if ws_bytes else None
+    a.workspace, a.workspace_bytes = (ws.data_ptr() if ws is not None else None), ws_bytes
     nat.launch(device, "hqmq_encode", L.hqmq_encode, ctypes.byref(a))
     qt = QuantizedTensor(shape, config, layer, role, head_base, scales, iw, rw, fw, pay, tok,
                          meta, device)
     qt._keepalive = (data, ws)
+    st = torch.cuda.current_stream(device)
     qt._ready = torch.cuda.Event()
-    qt._ready.record(torch.cuda.current_stream(device))
+    qt._ready.record(st)
+    qt._ready_stream = st.cuda_stream
     if sync:
         qt.synchronize()
     return qt
 
 
-_OUT_CODES = None
+_OUT_CODES = {}
 
 
 def _out_code(dtype):
-    torch = _torch()
-    table = {torch.float32: nat.F32, torch.float16: nat.F16, torch.bfloat16: nat.BF16,
-             torch.float64: nat.F64}
-    if dtype not in table:
+    if not _OUT_CODES:
+        torch = _torch()
+        _OUT_CODES.update({torch.float32: nat.F32, torch.float16: nat.F16,
+                           torch.bfloat16: nat.BF16, torch.float64: nat.F64})
+    code = _OUT_CODES.get(dtype)
+    if code is None:
         raise InvalidArgument("decode dtype must be float16, bfloat16, float32 or float64")
-    return table[dtype]
+    return code
 
 
 def decode_token_range(packed: QuantizedTensor, bank: CodebookBank, start: int, stop: int,
@@ -502,11 +521,20 @@ def decode_token_range(packed: QuantizedTensor, bank: CodebookBank, start: int, 
         check_out(out, want, dtype, dev, "decode out")
     if stop == start:
         return out
-    tabs = bank.device_tables(packed.layer, packed.head_base, s.heads, packed.role, dev)
+    # per-(tensor, bank) argument block, tables and error word, built once: the
+    # error word only accumulates bits (a corrupt index stays corrupt), so it
+    # is never reset
+    dc = packed._dc
+    if dc is None or dc[0] is not bank:
+        tabs = bank.device_tables(packed.layer, packed.head_base, s.heads, packed.role, dev)
+        err = torch.zeros(1, dtype=torch.int32, device=dev)
+        args = packed._decode_args(0, 0, code, None, err, tabs["joint_f32"], tabs["joint_f64"],
+                                   tabs["joint_f16"])
+        dc = packed._dc = (bank, args, tabs, err)
+    args, err = dc[1], dc[3]
+    args.token_start, args.token_stop, args.out_dtype = start, stop, code
+    args.out = out.data_ptr()
     packed.wait()
-    err = torch.zeros(1, dtype=torch.int32, device=dev)
-    args = packed._decode_args(start, stop, code, out, err,
-                               tabs["joint_f32"], tabs["joint_f64"], tabs["joint_f16"])
     nat.launch(dev, "hqmq_decode", nat.lib().hqmq_decode, ctypes.byref(args))
     if check and int(err.item()) & nat.DEVERR_INDEX:
         raise CorruptData("codeword index out of range")

@@ -1494,6 +1494,7 @@ int launch_encode(const hqmq_encode_args* a, const Layout& L, cudaStream_t st) {
   if (!L.warp_path && a->flag_words && a->flag_capacity_words)
     cudaMemsetAsync(a->flag_words, 0, a->flag_capacity_words * 4, st);
   cudaMemsetAsync(a->counters, 0, 3 * sizeof(int64_t), st);
+  if (a->error_word) cudaMemsetAsync(a->error_word, 0, sizeof(uint32_t), st);
   if (L.n_chunks == 0) {
     set_counts_kernel<<<1, 32, 0, st>>>(0, a->counters);
     e = cudaGetLastError();

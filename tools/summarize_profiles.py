@@ -41,6 +41,9 @@ METRICS = [
     "smsp__issue_active.avg.pct_of_peak_sustained_active",
     "sm__warps_active.avg.pct_of_peak_sustained_active",
     "smsp__inst_executed.sum",
+    "l1tex__data_pipe_lsu_wavefronts_mem_shared_op_ld.sum",
+    "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
+    "lts__t_sectors_srcunit_tex_op_write.sum",
     "launch__registers_per_thread",
     "launch__grid_size",
     "launch__block_size",
