@@ -259,42 +259,42 @@ def run_ours(args, wl, world, rank, local):
     per_encode = 3 if wl["C"] is None else 11
     per_decode = 1
 
-    def step(record=None, single=False):
+    def step(single=False):
         """One pass over the rank's units; units rotate over the streams so one
         unit's prep / decode overlaps another's FMA-bound search (single: all on
         the current stream, e.g. for graph capture)."""
         qts = []
         for i, ((layer, role), x) in enumerate(zip(units, inputs)):
-            st = (streams[i % nstream] if record is None and not single
-                  else torch.cuda.current_stream(dev))
+            st = streams[i % nstream] if not single else torch.cuda.current_stream(dev)
             with torch.cuda.stream(st):
-                if record is not None:
-                    e0 = torch.cuda.Event(enable_timing=True)
-                    e1 = torch.cuda.Event(enable_timing=True)
-                    e2 = torch.cuda.Event(enable_timing=True)
-                    e0.record()
                 qt = hq.encode_tensor(x, cfg, layer=layer, role=role, bank=bank, sync=False)
-                if record is not None:
-                    e1.record()
                 hq.decode_tensor(qt, bank, dtype=torch.float16, out=outs[i % len(outs)],
                                  check=False)
-                if record is not None:
-                    e2.record()
-                    record.append((e0, e1, e2))
             launches["n"] += per_encode + per_decode
             qts.append(qt)
         return qts
 
     # per-kernel split (roofline denominators) first, on a fresh allocator pool:
-    # single-stream passes, each unit's encode and decode bracketed by events on
-    # the launching stream (the first pass warms the pool and the tables)
+    # every unit's encode back to back on one stream between one event pair,
+    # then every decode between a second pair.  The host enqueues the whole
+    # pass ahead of the device (the encodes alone keep it busy for tens of ms),
+    # so no host launch gap lands inside either span.  The first pass warms the
+    # allocator pool and the tables.
+    cur_split = torch.cuda.current_stream(dev)
     for _ in range(2):
-        recs = []
-        step(recs)
         torch.cuda.synchronize()
-    enc_ms = sum(a.elapsed_time(b) for a, b, _ in recs)
-    dec_ms = sum(b.elapsed_time(c) for _, b, c in recs)
-    del recs
+        se = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
+        se[0].record(cur_split)
+        qts_split = [hq.encode_tensor(x, cfg, layer=layer, role=role, bank=bank, sync=False)
+                     for (layer, role), x in zip(units, inputs)]
+        se[1].record(cur_split)
+        for i, qt in enumerate(qts_split):
+            hq.decode_tensor(qt, bank, dtype=torch.float16, out=outs[i % len(outs)], check=False)
+        se[2].record(cur_split)
+        torch.cuda.synchronize()
+        enc_ms = se[0].elapsed_time(se[1])
+        dec_ms = se[1].elapsed_time(se[2])
+        del qts_split
     for _ in range(args.warmup):
         qts = step()
     torch.cuda.synchronize()
@@ -457,7 +457,9 @@ def run_ours(args, wl, world, rank, local):
         traffic = next((v for k, v in tr.get("per_kernel", {}).items() if "encode_tc" in k), None)
 
     split_note = ("CUDA-graph replays: encode-only graph, decode = step graph - encode"
-                  if graph is not None else "single-stream pass, per-unit CUDA events")
+                  if graph is not None else
+                  "single stream: all encodes back to back between one CUDA event pair, "
+                  "then all decodes between a second pair")
     S = cfg.codebook_size
     tc = S % 32 == 0 or (S % 16 == 0 and S >= 48)
     search_kernel = "tcgen05 encode_tc_kernel" if tc else "FFMA2 encode_warp_kernel<...,2>"

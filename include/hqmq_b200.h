@@ -134,6 +134,15 @@ typedef struct {
                           the fp16/bf16 head_dim-128 path (results are
                           bit-identical either way; AUTO picks the faster) */
   int32_t _pad1;
+  /* Med3x threshold control (extension for incremental caches; the reference
+   * always pools the call, codec.py:208-219).  G = heads with per-head
+   * pooling, else 1.  fixed_thresholds (device, G doubles, NULL = compute the
+   * exact C * lower median of the call): flag = r > fixed_thresholds[g], the
+   * reference's strict comparison against a frozen threshold.
+   * thresholds_out (device, G doubles, optional) receives the thresholds the
+   * encode used. */
+  const double* fixed_thresholds;
+  double* thresholds_out;
 } hqmq_encode_args;
 
 typedef enum {
@@ -180,6 +189,17 @@ int hqmq_decode(const hqmq_decode_args* args, void* stream);
  * (batch, heads, tokens, chunks); entries at flagged positions are zero. */
 int hqmq_unpack(const hqmq_decode_args* args, int32_t* indices, uint8_t* quanta,
                 uint8_t* flags, void* stream);
+
+/* Med3x compact sections -> fixed per-token code slots (the paged cache's
+ * Med3x layout, hqmq_paged_view): for every token t of the (head_dim 128)
+ * tensor, index codes at bits [t*32*w + c*w, +w) of index_slots (w words per
+ * token), radius codes likewise in radius_slots, 0 in flagged chunks' slots,
+ * and payload_offsets[t] = payload_base + the payload row of the token's
+ * first flagged chunk (t*32 - token_offsets[t]).  No reference counterpart:
+ * the reference keeps one dense tensor per call (codec.py:124-147). */
+int hqmq_expand_tokens(const hqmq_decode_args* args, uint32_t* index_slots,
+                       uint32_t* radius_slots, uint32_t* payload_offsets,
+                       uint32_t payload_base, void* stream);
 
 /* Pack dense arrays (indices int32, quanta uint8, flags uint8 or NULL) into
  * the section streams (the inverse of hqmq_unpack; kvpack.py:134-146).
@@ -243,11 +263,14 @@ typedef struct {
 
 size_t hqmq_attention_workspace_bytes(const hqmq_attention_args* args);
 int hqmq_attention_decode(const hqmq_attention_args* args, void* stream);
+/* The kernel hqmq_attention_decode would run for `args` (static string; for
+ * tests and benchmark reports). */
+const char* hqmq_attention_kernel_name(const hqmq_attention_args* args);
 
 /* ------------------------------------------------------ paged attention */
 /* Decode-step attention over a PAGED compressed cache (the serving layout;
  * SURVEY.md §8(f) rank 2): a page holds page_tokens (= 128) consecutive tokens
- * of ONE (sequence, kv head) row in the token-aligned stream format (no Med3x):
+ * of ONE (sequence, kv head) row in the token-aligned stream format:
  * page_tokens*index_bits index words, page_tokens*radius_bits radius words,
  * page_tokens fp16 scales.  block_table[(b*kv_heads + h)*max_pages + i] is the
  * page id holding tokens [128 i, 128 i + 128) of row (b, h); kv_lens[b] is
@@ -259,6 +282,14 @@ typedef struct {
   const uint16_t* scale_pages;  /* [num_pages][page_tokens] */
   const float* joint_f32;       /* [kv_heads][24*S][4] */
   const uint16_t* joint_f16;    /* optional fp16 copy */
+  /* Med3x caches (all three NULL without extraction).  Each token keeps its
+   * fixed code slots (a flagged chunk's index / radius codes are ignored);
+   * flag_pages[page][t] is the token's 32-bit chunk flag word and
+   * payoff_pages[page][t] the row in `payloads` of its first flagged chunk
+   * (the token's flagged chunks are consecutive rows in chunk order). */
+  const uint32_t* flag_pages;   /* [num_pages][page_tokens] */
+  const uint32_t* payoff_pages; /* [num_pages][page_tokens] */
+  const uint16_t* payloads;     /* [rows][4] fp16 */
 } hqmq_paged_view;
 
 typedef struct {

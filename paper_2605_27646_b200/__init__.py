@@ -6,7 +6,7 @@ streams).  Compute: hand-written sm_100a CUDA kernels behind the C ABI in
 include/hqmq_b200.h, loaded from paper_2605_27646_b200/_lib/libhqmq_b200.so.
 """
 
-from .attention import AttentionConfig, fused_attend, reference_attend
+from .attention import AttentionConfig, attention_kernel, fused_attend, reference_attend
 from .codebook import (
     CodebookBank,
     JointCodebook,

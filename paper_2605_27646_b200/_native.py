@@ -44,6 +44,7 @@ class EncodeArgs(ctypes.Structure):
         ("radius_capacity_words", ctypes.c_size_t),
         ("flag_capacity_words", ctypes.c_size_t),
         ("search_path", c_i32), ("_pad1", c_i32),
+        ("fixed_thresholds", c_vp), ("thresholds_out", c_vp),
     ]
 
 
@@ -88,6 +89,7 @@ class PagedView(ctypes.Structure):
     _fields_ = [
         ("index_pages", c_vp), ("radius_pages", c_vp), ("scale_pages", c_vp),
         ("joint_f32", c_vp), ("joint_f16", c_vp),
+        ("flag_pages", c_vp), ("payoff_pages", c_vp), ("payloads", c_vp),
     ]
 
 
@@ -116,6 +118,8 @@ SIGNATURES = {
     "hqmq_encode": ([ctypes.POINTER(EncodeArgs), c_vp], c_i32),
     "hqmq_decode": ([ctypes.POINTER(DecodeArgs), c_vp], c_i32),
     "hqmq_unpack": ([ctypes.POINTER(DecodeArgs), c_vp, c_vp, c_vp, c_vp], c_i32),
+    "hqmq_expand_tokens": ([ctypes.POINTER(DecodeArgs), c_vp, c_vp, c_vp, ctypes.c_uint32, c_vp],
+                           c_i32),
     "hqmq_pack": ([c_i64, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                    ctypes.c_size_t, c_vp], c_i32),
     "hqmq_pack_workspace_bytes": ([c_i64], ctypes.c_size_t),
@@ -124,6 +128,7 @@ SIGNATURES = {
     "hqmq_validate_indices": ([c_vp, c_i64, c_i32, c_i64, c_vp, c_vp], c_i32),
     "hqmq_attention_workspace_bytes": ([ctypes.POINTER(AttentionArgs)], ctypes.c_size_t),
     "hqmq_attention_decode": ([ctypes.POINTER(AttentionArgs), c_vp], c_i32),
+    "hqmq_attention_kernel_name": ([ctypes.POINTER(AttentionArgs)], ctypes.c_char_p),
     "hqmq_paged_attention_workspace_bytes": ([ctypes.POINTER(PagedAttentionArgs)], ctypes.c_size_t),
     "hqmq_attention_decode_paged": ([ctypes.POINTER(PagedAttentionArgs), c_vp], c_i32),
     "hqmq_crc32_workspace_bytes": ([ctypes.c_uint64], ctypes.c_size_t),

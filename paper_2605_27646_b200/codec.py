@@ -191,6 +191,16 @@ class QuantizedTensor:
         return self._payload_buf[: self.n_payload]
 
     @property
+    def outlier_thresholds(self):
+        """(G,) float64 device tensor of the Med3x thresholds C * median the
+        encode flagged against (G = heads with per-head pooling, else 1), or
+        None without extraction."""
+        thr = self.__dict__.get("_thresholds")
+        if thr is not None:
+            self.wait()
+        return thr
+
+    @property
     def outlier_fraction(self) -> float:
         n = self.shape.n_chunks
         return self.n_payload / n if n else 0.0
@@ -412,7 +422,8 @@ SEARCH_PATHS = {"auto": nat.SEARCH_AUTO, "cuda_core": nat.SEARCH_CUDA_CORE,
 
 def encode_tensor(data, config: CodecConfig, layer: int = 0, role: str = "K",
                   bank: CodebookBank | None = None, head_base: int = 0, *,
-                  device=None, sync: bool = True, search_path: str = "auto") -> QuantizedTensor:
+                  device=None, sync: bool = True, search_path: str = "auto",
+                  outlier_thresholds=None) -> QuantizedTensor:
     """Quantize a (batch, heads, tokens, head_dim) tensor (codec.py:232-287).
 
     Runs Med3x, the fused encode kernel and the section packing on the GPU.
@@ -422,6 +433,14 @@ def encode_tensor(data, config: CodecConfig, layer: int = 0, role: str = "K",
     the nearest-codeword search of the fp16/bf16 head_dim-128 kernels
     ("auto", "cuda_core" = FFMA2, "tensor_core" = tcgen05 rotations when
     S % 16 == 0); every path is certified and bit-identical to the reference.
+
+    outlier_thresholds (extension, Med3x only): freeze the outlier thresholds
+    instead of pooling this call's median -- a float or a (G,) float64 tensor,
+    G = heads with per-head pooling else 1; chunks with r > threshold are
+    extracted (the reference's strict test, codec.py:208-219, against a given
+    threshold).  The thresholds an encode used are on
+    QuantizedTensor.outlier_thresholds, so a cache's prefill encode can freeze
+    them for its appends (PagedKVCache).
     """
     torch = _torch()
     if role not in ROLE_TAGS:
@@ -449,6 +468,18 @@ def encode_tensor(data, config: CodecConfig, layer: int = 0, role: str = "K",
         cap = 1
     pay = torch.empty((cap, 4), dtype=torch.float16, device=device)
     meta = torch.empty(4, dtype=torch.int64, device=device)  # zeroed by hqmq_encode
+    thr_out = fixed = None
+    if ext:
+        G = shape.heads if c.median_pooling == "per_head" else 1
+        thr_out = torch.empty(G, dtype=torch.float64, device=device)
+        if outlier_thresholds is not None:
+            fixed = torch.as_tensor(outlier_thresholds, dtype=torch.float64)
+            fixed = (fixed.reshape(1).expand(G) if fixed.numel() == 1 else fixed.reshape(-1))
+            if fixed.numel() != G:
+                raise InvalidArgument(f"outlier_thresholds needs {G} values, got {fixed.numel()}")
+            fixed = fixed.to(device=device).contiguous()
+    elif outlier_thresholds is not None:
+        raise InvalidArgument("outlier_thresholds requires outlier extraction (outlier_multiplier)")
     tabs = bank.device_tables(layer, head_base, shape.heads, role, device)
     a = nat.EncodeArgs()
     a.batch, a.heads, a.tokens, a.head_dim = shape.batch, shape.heads, shape.tokens, shape.head_dim
@@ -470,6 +501,8 @@ def encode_tensor(data, config: CodecConfig, layer: int = 0, role: str = "K",
     a.index_capacity_words, a.radius_capacity_words = iw.numel(), rw.numel()
     a.search_path = SEARCH_PATHS[search_path]
     a.flag_capacity_words = fw.numel() if ext else 0
+    a.fixed_thresholds = fixed.data_ptr() if fixed is not None else None
+    a.thresholds_out = thr_out.data_ptr() if thr_out is not None else None
     L = nat.lib()
     ws_bytes = int(L.hqmq_encode_workspace_bytes(ctypes.byref(a)))
     ws = torch.empty(ws_bytes, dtype=torch.uint8, device=device) if ws_bytes else None
@@ -477,7 +510,8 @@ def encode_tensor(data, config: CodecConfig, layer: int = 0, role: str = "K",
     nat.launch(device, "hqmq_encode", L.hqmq_encode, ctypes.byref(a))
     qt = QuantizedTensor(shape, config, layer, role, head_base, scales, iw, rw, fw, pay, tok,
                          meta, device)
-    qt._keepalive = (data, ws)
+    qt._keepalive = (data, ws, fixed)
+    qt._thresholds = thr_out
     st = torch.cuda.current_stream(device)
     qt._ready = torch.cuda.Event()
     qt._ready.record(st)

@@ -446,32 +446,61 @@ constexpr int kMConsumers = 8;
 constexpr int kMThreads = kMConsumers * 32;
 
 struct RingGeom {
-  uint32_t ki, kr, ks, vi, vr, vs, bytes;
+  uint32_t ki, kr, ks, vi, vr, vs, kf, ka, vf, va, bytes;
 };
 
-__host__ __device__ inline RingGeom ring_geom(int w, int br) {
-  auto up = [](uint32_t x) { return (x + 127u) / 128u * 128u; };
+// One ring stage: K and V index / radius words and fp16 scales of a 128-key
+// tile; with Med3x (kFlags) also each key's flag word and its aux word (the
+// token's coded offset in the contiguous layout, its payload row in the paged
+// one), and slack for the 16-byte-aligned start of a compact code range.
+__host__ __device__ inline RingGeom ring_geom(int w, int br, bool flags = false) {
+  // (the Med3x stage packs its regions at 16 bytes, the bulk-copy alignment,
+  // so that two CTAs still fit an SM at S = 64)
+  const uint32_t al = flags ? 16u : 128u;
+  auto up = [al](uint32_t x) { return (x + al - 1u) / al * al; };
+  const uint32_t slack = flags ? 64u : 16u;
   RingGeom g;
   uint32_t o = 0;
-  g.ki = o; o += up(kMT * w * 4 + 16);
-  g.kr = o; o += up(kMT * br * 4 + 16);
+  g.ki = o; o += up(kMT * w * 4 + slack);
+  g.kr = o; o += up(kMT * br * 4 + slack);
   g.ks = o; o += up(kMT * 2);
-  g.vi = o; o += up(kMT * w * 4 + 16);
-  g.vr = o; o += up(kMT * br * 4 + 16);
+  g.vi = o; o += up(kMT * w * 4 + slack);
+  g.vr = o; o += up(kMT * br * 4 + slack);
   g.vs = o; o += up(kMT * 2);
+  g.kf = g.ka = g.vf = g.va = 0;
+  if (flags) {
+    g.kf = o; o += kMT * 4;
+    g.ka = o; o += kMT * 4;
+    g.vf = o; o += kMT * 4;
+    g.va = o; o += kMT * 4;
+  }
   g.bytes = o;
   return g;
 }
 
-__host__ __device__ inline size_t mma_smem_bytes(int S, int w, int br) {
-  const size_t tab = 2 * (size_t)kGroupOrder * S * 8;
-  const size_t ring = kMStages * (size_t)ring_geom(w, br).bytes;
+// Med3x extras after the ring: Q rows in fp32 (pre-scaled, natural dim order)
+// for the outlier-chunk score corrections, and per-warp P tiles for the
+// outlier-chunk PV corrections.
+constexpr size_t kFlagExtra = (size_t)8 * 128 * 4 + (size_t)kMConsumers * 8 * 16 * 4 + 8 * 32 * 8;
+
+constexpr size_t kMaxDynSmem = 220 * 1024;  // under sm_100's 227 KB per CTA, static shared memory included
+constexpr int kMStagesFlags = 2;  // Med3x ring depth (room for the residual tables)
+
+__host__ __device__ inline size_t mma_smem_bytes(int S, int w, int br, bool flags = false) {
+  const size_t tab = (flags ? 4 : 2) * (size_t)kGroupOrder * S * 8;
+  const size_t ring = (flags ? kMStagesFlags : kMStages) * (size_t)ring_geom(w, br, flags).bytes;
   const size_t merge = (size_t)kMConsumers * 8 * 130 * 4;  // O + (m, l) per warp/row
-  return tab + (ring > merge ? ring : merge);
+  return tab + (ring > merge ? ring : merge) + (flags ? kFlagExtra : 0);
 }
 
-
-template <int W, int BR, bool kPaged = false>
+// Med3x (kFlags): flagged chunks carry no code; their fp16 payload row is the
+// value.  The MMAs see them as zero (radius code forced to 0) and each is
+// added in fp32 on the CUDA cores: q . payload into the score of its key
+// (lane-local: the S-accumulator lane of (row, key) does it) and
+// p(row, key) * payload into O (the O^T lane owning the chunk's dims, with P
+// from a per-warp shared tile).  Codes of the unflagged chunks are found from
+// the key's coded offset (contiguous: token_offsets; paged: fixed slots).
+template <int W, int BR, bool kPaged = false, bool kFlags = false>
 __global__ void __launch_bounds__(kMThreads, 2) attention_mma_kernel(AttParams p) {
   extern __shared__ __align__(128) unsigned char sm[];
   __shared__ __align__(8) uint64_t full[kMStages];
@@ -480,11 +509,26 @@ __global__ void __launch_bounds__(kMThreads, 2) attention_mma_kernel(AttParams p
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ncw = kGroupOrder * p.S;
   constexpr int w = W, br = BR;
-  const bool tab_tma = p.k.table16 != nullptr && p.v.table16 != nullptr;
-  const RingGeom gm = ring_geom(w, br);
+  constexpr int NS = kFlags ? kMStagesFlags : kMStages;  // ring depth
+  // Med3x: tables are converted in-kernel (V needs its fp16 hi / lo pair)
+  const bool tab_tma = !kFlags && p.k.table16 != nullptr && p.v.table16 != nullptr;
+  const RingGeom gm = ring_geom(w, br, kFlags);
   uint2* ktab = reinterpret_cast<uint2*>(sm);
   uint2* vtab = ktab + ncw;
-  unsigned char* ring = reinterpret_cast<unsigned char*>(vtab + ncw);
+  // Med3x: fp16 residual tables cw - fp16(cw) of K and V (split-fp16 S and P V)
+  uint2* vtab_lo = vtab + ncw;
+  uint2* ktab_lo = vtab + 2 * ncw;
+  unsigned char* ring = reinterpret_cast<unsigned char*>(vtab + (kFlags ? 3 : 1) * ncw);
+  // Med3x extras (kFlags only): after the ring (or the merge area)
+  float* qs = nullptr;   // [8][128] fp32, scale_log2 folded in
+  float* pws = nullptr;  // [warp][8 rows][16 keys]
+  uint2* qlo_s = nullptr;  // [ks][lane]: fp16 residual of the Q A-fragments
+  if constexpr (kFlags) {
+    const size_t rb = NS * (size_t)gm.bytes, mb = (size_t)kMConsumers * 8 * 130 * 4;
+    qs = reinterpret_cast<float*>(ring + (rb > mb ? rb : mb));
+    pws = qs + 8 * 128;
+    qlo_s = reinterpret_cast<uint2*>(pws + kMConsumers * 128);
+  }
 
   const int64_t bh = blockIdx.y;
   const int64_t b = bh / p.Hkv, hkv = bh % p.Hkv;
@@ -495,7 +539,7 @@ __global__ void __launch_bounds__(kMThreads, 2) attention_mma_kernel(AttParams p
   const int64_t tokrow = bh * p.Tkv;
 
   if (tid == 0) {
-    for (int s = 0; s < kMStages; ++s) {
+    for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], 1);
       released[s] = 0u;
     }
@@ -504,6 +548,8 @@ __global__ void __launch_bounds__(kMThreads, 2) attention_mma_kernel(AttParams p
   }
   __syncthreads();
 
+  // first 16-byte-aligned word of a compact code range starting at code c0
+  auto range_lo = [](uint64_t c0, int width) -> uint64_t { return ((c0 * width) >> 5) & ~3ull; };
   auto issue = [&](int64_t k, int stage) {
     int64_t t = tokrow + kbeg + k * kMT;
     int ntok = (int)min((int64_t)kMT, kend - (kbeg + k * kMT));
@@ -512,22 +558,60 @@ __global__ void __launch_bounds__(kMThreads, 2) attention_mma_kernel(AttParams p
       ntok = kMT;
     }
     unsigned char* s = ring + (size_t)stage * gm.bytes;
-    const uint32_t ib = ntok * w * 4, rb = ntok * br * 4, sb = ntok * 2;
+    const uint32_t sb = ntok * 2;
+    if constexpr (kFlags && !kPaged) {
+      // compact streams: the tile's codes are [c0, c1) of the coded order
+      const uint32_t fb = ntok * 4;  // ntok % 8 == 0 (T_kv % 8 == 0): 16-byte multiple
+      uint32_t ib[2], rbb[2];
+      uint64_t iw0[2], rw0[2];
+      const AttView* vw[2] = {&p.k, &p.v};
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        const uint64_t c0 = __ldg(vw[r]->tokoff + t);
+        const uint64_t c1 = (uint64_t)__ldg(vw[r]->tokoff + t + ntok - 1) + 32u -
+                            (uint64_t)__popc(__ldg(vw[r]->flagw + t + ntok - 1));
+        iw0[r] = range_lo(c0, w);
+        rw0[r] = range_lo(c0, br);
+        ib[r] = (uint32_t)((((c1 * w + 31) >> 5) - iw0[r] + 3) & ~3ull) * 4u;
+        rbb[r] = (uint32_t)((((c1 * br + 31) >> 5) - rw0[r] + 3) & ~3ull) * 4u;
+      }
+      fence_proxy_async();
+      mbar_arrive_expect_tx(&full[stage], ib[0] + rbb[0] + ib[1] + rbb[1] + 2 * (sb + 2 * fb));
+      bulk_g2s(s + gm.ki, p.k.idxw + iw0[0], ib[0], &full[stage]);
+      bulk_g2s(s + gm.kr, p.k.radw + rw0[0], rbb[0], &full[stage]);
+      bulk_g2s(s + gm.ks, p.k.scales + t, sb, &full[stage]);
+      bulk_g2s(s + gm.kf, p.k.flagw + t, fb, &full[stage]);
+      bulk_g2s(s + gm.ka, p.k.tokoff + t, fb, &full[stage]);
+      bulk_g2s(s + gm.vi, p.v.idxw + iw0[1], ib[1], &full[stage]);
+      bulk_g2s(s + gm.vr, p.v.radw + rw0[1], rbb[1], &full[stage]);
+      bulk_g2s(s + gm.vs, p.v.scales + t, sb, &full[stage]);
+      bulk_g2s(s + gm.vf, p.v.flagw + t, fb, &full[stage]);
+      bulk_g2s(s + gm.va, p.v.tokoff + t, fb, &full[stage]);
+      return;
+    }
+    const uint32_t ib = ntok * w * 4, rb = ntok * br * 4;
+    const uint32_t fb = kFlags ? ntok * 4 : 0;
     fence_proxy_async();
-    mbar_arrive_expect_tx(&full[stage], 2 * (ib + rb + sb));
+    mbar_arrive_expect_tx(&full[stage], 2 * (ib + rb + sb + 2 * fb));
     bulk_g2s(s + gm.ki, p.k.idxw + t * w, ib, &full[stage]);
     bulk_g2s(s + gm.kr, p.k.radw + t * br, rb, &full[stage]);
     bulk_g2s(s + gm.ks, p.k.scales + t, sb, &full[stage]);
     bulk_g2s(s + gm.vi, p.v.idxw + t * w, ib, &full[stage]);
     bulk_g2s(s + gm.vr, p.v.radw + t * br, rb, &full[stage]);
     bulk_g2s(s + gm.vs, p.v.scales + t, sb, &full[stage]);
+    if constexpr (kFlags) {  // paged Med3x: flag words and payload rows per token
+      bulk_g2s(s + gm.kf, p.k.flagw + t, fb, &full[stage]);
+      bulk_g2s(s + gm.ka, p.k.tokoff + t, fb, &full[stage]);
+      bulk_g2s(s + gm.vf, p.v.flagw + t, fb, &full[stage]);
+      bulk_g2s(s + gm.va, p.v.tokoff + t, fb, &full[stage]);
+    }
   };
-  // release a stage; the last of the 8 warps refills it with tile k + kMStages
+  // release a stage; the last of the 8 warps refills it with tile k + NS
   auto release = [&](int64_t k, int stage) {
     if (lane == 0) {
       if (atomicAdd(&released[stage], 1u) == kMConsumers - 1) {
         released[stage] = 0u;
-        if (k + kMStages < ntile) issue(k + kMStages, stage);
+        if (k + NS < ntile) issue(k + NS, stage);
       }
     }
   };
@@ -540,22 +624,44 @@ __global__ void __launch_bounds__(kMThreads, 2) attention_mma_kernel(AttParams p
       bulk_g2s(ktab, p.k.table16 + hkv * ncw, tb, &tab_bar);
       bulk_g2s(vtab, p.v.table16 + hkv * ncw, tb, &tab_bar);
     }
-    for (int s = 0; s < kMStages && s < ntile; ++s) issue(s, s);
+    for (int s = 0; s < NS && s < ntile; ++s) issue(s, s);
+  }
+  const int g4 = lane >> 2, t4 = lane & 3;  // mma fragment coordinates
+  if constexpr (kFlags) {  // fp32 Q rows (natural dims) for the outlier corrections
+    for (int i = tid; i < 8 * 128; i += kMThreads) {
+      const int r = i >> 7, d = i & 127;
+      float v = 0.f;
+      if (r < p.nrows) {
+        const int gi = r / (int)p.Tq, qi = r - gi * (int)p.Tq;
+        v = __ldg(p.q + ((b * p.Hq + hkv * p.g + gi) * p.Tq + qi) * 128 + d) * p.scale_log2;
+      }
+      qs[i] = v;
+    }
   }
   if (tab_tma) {
     mbar_wait(&tab_bar, 0u);
+    if constexpr (kFlags) __syncthreads();
   } else {
     const float4* gk = p.k.table + hkv * ncw;
     const float4* gv = p.v.table + hkv * ncw;
     for (int i = tid; i < ncw; i += kMThreads) {
       const float4 a = __ldg(gk + i), c = __ldg(gv + i);
-      ktab[i] = make_uint2(pack_half2(a.x, a.y), pack_half2(a.z, a.w));
-      vtab[i] = make_uint2(pack_half2(c.x, c.y), pack_half2(c.z, c.w));
+      const uint2 h = make_uint2(pack_half2(c.x, c.y), pack_half2(c.z, c.w));
+      const uint2 hk = make_uint2(pack_half2(a.x, a.y), pack_half2(a.z, a.w));
+      ktab[i] = hk;
+      vtab[i] = h;
+      if constexpr (kFlags) {
+        const float2 h01 = __half22float2(*reinterpret_cast<const __half2*>(&h.x));
+        const float2 h23 = __half22float2(*reinterpret_cast<const __half2*>(&h.y));
+        vtab_lo[i] = make_uint2(pack_half2(c.x - h01.x, c.y - h01.y), pack_half2(c.z - h23.x, c.w - h23.y));
+        const float2 k01 = __half22float2(*reinterpret_cast<const __half2*>(&hk.x));
+        const float2 k23 = __half22float2(*reinterpret_cast<const __half2*>(&hk.y));
+        ktab_lo[i] = make_uint2(pack_half2(a.x - k01.x, a.y - k01.y), pack_half2(a.z - k23.x, a.w - k23.y));
+      }
     }
     __syncthreads();
   }
 
-  const int g4 = lane >> 2, t4 = lane & 3;  // mma fragment coordinates
   const uint32_t cwmax = (uint32_t)ncw - 1u;
   float m_run = -INFINITY, l_run = 0.f;
   // O^T accumulators, m-tile 2j+h: c0/c1 = (dim 4(4g4+j)+2h, rows 2t4 / 2t4+1),
@@ -578,15 +684,24 @@ __global__ void __launch_bounds__(kMThreads, 2) attention_mma_kernel(AttParams p
       if (row_valid) v = __ldg(qrow + 8 * t4 + ks);
       qa[ks][0] = pack_half2(v.x * p.scale_log2, v.y * p.scale_log2);
       qa[ks][1] = pack_half2(v.z * p.scale_log2, v.w * p.scale_log2);
+      if constexpr (kFlags) {  // Q residual fragments (every warp holds the same Q)
+        if (warp == 0) {
+          const float2 h01 = __half22float2(*reinterpret_cast<const __half2*>(&qa[ks][0]));
+          const float2 h23 = __half22float2(*reinterpret_cast<const __half2*>(&qa[ks][1]));
+          qlo_s[ks * 32 + lane] = make_uint2(pack_half2(v.x * p.scale_log2 - h01.x, v.y * p.scale_log2 - h01.y),
+                                             pack_half2(v.z * p.scale_log2 - h23.x, v.w * p.scale_log2 - h23.y));
+        }
+      }
     }
+    if constexpr (kFlags) __syncthreads();
   }
   int64_t vis = tkv;  // keys j < vis are visible to row g4
   if (row_valid && p.causal) vis = (g4 % (int)p.Tq) + (tkv - p.Tq) + 1;
   const float rtop = 1.0f / (float)((1 << br) - 1);
 
   for (int64_t k = 0; k < ntile; ++k) {
-    const int stage = (int)(k % kMStages);
-    mbar_wait(&full[stage], (uint32_t)((k / kMStages) & 1));
+    const int stage = (int)(k % NS);
+    mbar_wait(&full[stage], (uint32_t)((k / NS) & 1));
     const unsigned char* s = ring + (size_t)stage * gm.bytes;
     const uint32_t* kiw = reinterpret_cast<const uint32_t*>(s + gm.ki);
     const uint32_t* krw = reinterpret_cast<const uint32_t*>(s + gm.kr);
@@ -594,8 +709,34 @@ __global__ void __launch_bounds__(kMThreads, 2) attention_mma_kernel(AttParams p
     const uint32_t* viw = reinterpret_cast<const uint32_t*>(s + gm.vi);
     const uint32_t* vrw = reinterpret_cast<const uint32_t*>(s + gm.vr);
     const uint16_t* vsc = reinterpret_cast<const uint16_t*>(s + gm.vs);
+    const uint32_t* kfl = reinterpret_cast<const uint32_t*>(s + gm.kf);
+    const uint32_t* kax = reinterpret_cast<const uint32_t*>(s + gm.ka);
+    const uint32_t* vfl = reinterpret_cast<const uint32_t*>(s + gm.vf);
+    const uint32_t* vax = reinterpret_cast<const uint32_t*>(s + gm.va);
     const int kw0 = warp * 16;                       // this warp's first key in the tile
     const int64_t t0 = kbeg + k * kMT + kw0;         // ... as a key index
+    const int64_t tile_key0 = kbeg + k * kMT;
+    // Med3x: bit base of the tile's compact ranges, the tile's first global token
+    uint64_t kib0 = 0, krb0 = 0, vib0 = 0, vrb0 = 0;
+    const int64_t gtok0 = tokrow + tile_key0;
+    int nvalid = kMT;
+    if constexpr (kFlags) {
+      nvalid = (int)min((int64_t)kMT, kend - tile_key0);
+      if constexpr (!kPaged) {
+        kib0 = range_lo(kax[0], w) * 32u;
+        krb0 = range_lo(kax[0], br) * 32u;
+        vib0 = range_lo(vax[0], w) * 32u;
+        vrb0 = range_lo(vax[0], br) * 32u;
+      }
+    }
+    // flag word / payload row of a key of the tile (0 / unused past the valid keys)
+    auto kflag = [&](int key) -> uint32_t { return key < nvalid ? kfl[key] : 0u; };
+    auto vflag = [&](int key) -> uint32_t { return key < nvalid ? vfl[key] : 0u; };
+    auto pay_row = [&](const uint32_t* ax, int key, uint32_t fw, int c) -> uint64_t {
+      const uint64_t below = (uint64_t)__popc(fw & ((1u << c) - 1u));
+      if constexpr (kPaged) return (uint64_t)ax[key] + below;
+      return (uint64_t)(gtok0 + key) * 32u - (uint64_t)ax[key] + below;
+    };
     if (t0 < kend) {
       // ---- S = Q K^T: lane decodes chunks 8*t4 .. 8*t4+7 of key kw0 + 8*nt + g4
       float sc[2][4];
@@ -603,15 +744,70 @@ __global__ void __launch_bounds__(kMThreads, 2) attention_mma_kernel(AttParams p
       for (int nt = 0; nt < 2; ++nt) {
         sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
         const uint32_t key = (uint32_t)(kw0 + nt * 8 + g4);
-        CodeRun<8, W, 4> ic;
-        CodeRun<8, BR, 4> rc;
-        ic.load(kiw, key * 32u * W + (uint32_t)t4 * 8u * W);
-        rc.load(krw, key * 32u * BR + (uint32_t)t4 * 8u * BR);
+        if constexpr (!kFlags) {
+          CodeRun<8, W, 4> ic;
+          CodeRun<8, BR, 4> rc;
+          ic.load(kiw, key * 32u * W + (uint32_t)t4 * 8u * W);
+          rc.load(krw, key * 32u * BR + (uint32_t)t4 * 8u * BR);
 #pragma unroll
-        for (int ks = 0; ks < 8; ++ks) {
-          const uint2 cw = ktab[min(ic.get(ks), cwmax)];
-          const uint32_t qq = code_half2(rc.get(ks));
-          mma_rows8(sc[nt], qa[ks][0], qa[ks][1], hmul2u(qq, cw.x), hmul2u(qq, cw.y));
+          for (int ks = 0; ks < 8; ++ks) {
+            const uint2 cw = ktab[min(ic.get(ks), cwmax)];
+            const uint32_t qq = code_half2(rc.get(ks));
+            mma_rows8(sc[nt], qa[ks][0], qa[ks][1], hmul2u(qq, cw.x), hmul2u(qq, cw.y));
+          }
+        } else {
+          const uint32_t fk = kflag((int)key);
+          const uint32_t lo = (uint32_t)t4 * 8u;
+          const uint32_t frun = (fk >> lo) & 0xffu;
+          uint32_t ibit, rbit;
+          if constexpr (kPaged) {
+            ibit = key * 32u * W + lo * W;
+            rbit = key * 32u * BR + lo * BR;
+          } else {
+            const uint64_t c = (int)key < nvalid
+                                   ? (uint64_t)kax[key] + lo - (uint64_t)__popc(fk & ((1u << lo) - 1u))
+                                   : (uint64_t)kax[0];
+            ibit = (uint32_t)(c * W - kib0);
+            rbit = (uint32_t)(c * BR - krb0);
+          }
+          CodeRunDyn<8, W> ic;
+          CodeRunDyn<8, BR> rc;
+          ic.load(kiw, ibit);
+          rc.load(krw, rbit);
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks) {
+            uint32_t ci, cq;
+            if constexpr (kPaged) {  // fixed slots: flagged codes are ignored
+              ci = ic.get(ks);
+              cq = (frun >> ks) & 1u ? 0u : rc.get(ks);
+            } else if (frun == 0u) {
+              ci = ic.get(ks);
+              cq = rc.get(ks);
+            } else {
+              const int j = ks - __popc(frun & ((1u << ks) - 1u));
+              const bool fl = (frun >> ks) & 1u;
+              ci = fl ? 0u : ic.get_dyn(j);
+              cq = fl ? 0u : rc.get_dyn(j);
+            }
+            // K = q * cw to ~fp32 as fp16 hi + lo; S += Qh Kh + Qh Kl + Ql Kh
+            const uint2 ch = ktab[min(ci, cwmax)], cl = ktab_lo[min(ci, cwmax)];
+            const float qf = (float)cq;
+            const float2 h01 = __half22float2(*reinterpret_cast<const __half2*>(&ch.x));
+            const float2 h23 = __half22float2(*reinterpret_cast<const __half2*>(&ch.y));
+            const float2 l01 = __half22float2(*reinterpret_cast<const __half2*>(&cl.x));
+            const float2 l23 = __half22float2(*reinterpret_cast<const __half2*>(&cl.y));
+            const float k0 = qf * (h01.x + l01.x), k1 = qf * (h01.y + l01.y);
+            const float k2 = qf * (h23.x + l23.x), k3 = qf * (h23.y + l23.y);
+            const uint32_t kh0 = pack_half2(k0, k1), kh1 = pack_half2(k2, k3);
+            const float2 r01 = __half22float2(*reinterpret_cast<const __half2*>(&kh0));
+            const float2 r23 = __half22float2(*reinterpret_cast<const __half2*>(&kh1));
+            const uint32_t kl0 = pack_half2(k0 - r01.x, k1 - r01.y);
+            const uint32_t kl1 = pack_half2(k2 - r23.x, k3 - r23.y);
+            const uint2 ql = qlo_s[ks * 32 + lane];
+            mma_rows8(sc[nt], qa[ks][0], qa[ks][1], kh0, kh1);
+            mma_rows8(sc[nt], qa[ks][0], qa[ks][1], kl0, kl1);
+            mma_rows8(sc[nt], ql.x, ql.y, kh0, kh1);
+          }
         }
       }
       // per-key scales sigma/top of this lane's 4 keys (2t4, 2t4+1, 2t4+8, 2t4+9)
@@ -624,7 +820,23 @@ __global__ void __launch_bounds__(kMThreads, 2) attention_mma_kernel(AttParams p
         kst[e] = __half2float(__ushort_as_half(ksc[kk])) * rtop;
         vst[e] = in ? __half2float(__ushort_as_half(vsc[kk])) * rtop : 0.f;
         const bool ok = row_valid && in && key < vis;
-        sv[e] = ok ? sc[e >> 1][e & 1] * kst[e] : -INFINITY;
+        float corr = 0.f;
+        if constexpr (kFlags) {  // outlier chunks of this key: q . payload in fp32
+          const uint32_t fk = kflag(kk);
+          uint32_t rem = fk;
+          while (rem) {
+            const int c = __ffs(rem) - 1;
+            rem &= rem - 1u;
+            const ushort4 hv =
+                __ldg(reinterpret_cast<const ushort4*>(p.k.payloads) + pay_row(kax, kk, fk, c));
+            const float4 qv = *reinterpret_cast<const float4*>(qs + g4 * 128 + 4 * c);
+            corr += qv.x * __half2float(__ushort_as_half(hv.x)) +
+                    qv.y * __half2float(__ushort_as_half(hv.y)) +
+                    qv.z * __half2float(__ushort_as_half(hv.z)) +
+                    qv.w * __half2float(__ushort_as_half(hv.w));
+          }
+        }
+        sv[e] = ok ? sc[e >> 1][e & 1] * kst[e] + corr : -INFINITY;
       }
       // ---- online softmax for row g4 over this warp's 16 keys (log2 domain)
       float mx = fmaxf(fmaxf(sv[0], sv[1]), fmaxf(sv[2], sv[3]));
@@ -656,33 +868,150 @@ __global__ void __launch_bounds__(kMThreads, 2) attention_mma_kernel(AttParams p
       const uint32_t pb0 = pack_half2(pe[0] * vst[0], pe[1] * vst[1]);
       const uint32_t pb1 = pack_half2(pe[2] * vst[2], pe[3] * vst[3]);
       // ---- O^T += V^T P^T: lane decodes chunks 4*g4 .. 4*g4+3 of its 4 keys
-      uint2 vv[4][4];  // [key e][chunk j] -> 4 halves
+      if constexpr (!kFlags) {
+        uint2 vv[4][4];  // [key e][chunk j] -> 4 halves
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const uint32_t key = (uint32_t)(kw0 + (e >> 1) * 8 + t4 * 2 + (e & 1));
-        CodeRun<4, W, 8> ic;
-        CodeRun<4, BR, 8> rc;
-        ic.load(viw, key * 32u * W + (uint32_t)g4 * 4u * W);
-        rc.load(vrw, key * 32u * BR + (uint32_t)g4 * 4u * BR);
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t key = (uint32_t)(kw0 + (e >> 1) * 8 + t4 * 2 + (e & 1));
+          CodeRun<4, W, 8> ic;
+          CodeRun<4, BR, 8> rc;
+          ic.load(viw, key * 32u * W + (uint32_t)g4 * 4u * W);
+          rc.load(vrw, key * 32u * BR + (uint32_t)g4 * 4u * BR);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint2 cw = vtab[min(ic.get(j), cwmax)];
+            const uint32_t qq = code_half2(rc.get(j));
+            vv[e][j] = make_uint2(hmul2u(qq, cw.x), hmul2u(qq, cw.y));
+          }
+        }
+        release(k, stage);
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const uint2 cw = vtab[min(ic.get(j), cwmax)];
-          const uint32_t qq = code_half2(rc.get(j));
-          vv[e][j] = make_uint2(hmul2u(qq, cw.x), hmul2u(qq, cw.y));
+          // m-tile 2j: (m = g4, g4+8) = elements (0, 1); m-tile 2j+1: elements (2, 3)
+          // a0 = keys (2t4, 2t4+1) at m = g4 ; a1 = same keys at m = g4+8
+          // a2 = keys (2t4+8, 2t4+9) at m = g4 ; a3 = same keys at m = g4+8
+          const uint32_t x0 = vv[0][j].x, x1 = vv[1][j].x, x2 = vv[2][j].x, x3 = vv[3][j].x;
+          const uint32_t y0 = vv[0][j].y, y1 = vv[1][j].y, y2 = vv[2][j].y, y3 = vv[3][j].y;
+          mma_full(oT[2 * j], __byte_perm(x0, x1, 0x5410), __byte_perm(x0, x1, 0x7632),
+                   __byte_perm(x2, x3, 0x5410), __byte_perm(x2, x3, 0x7632), pb0, pb1);
+          mma_full(oT[2 * j + 1], __byte_perm(y0, y1, 0x5410), __byte_perm(y0, y1, 0x7632),
+                   __byte_perm(y2, y3, 0x5410), __byte_perm(y2, y3, 0x7632), pb0, pb1);
+        }
+      } else {
+        // Med3x: split-fp16 P and V (P = Ph + Pl, V = Vh + Vl, O += Vh Ph + Vl Ph +
+        // Vh Pl): outlier caches give peaked softmax rows, where one fp16 V
+        // rounding would show up at the 1e-3 level
+        const float2 ph01 = __half22float2(*reinterpret_cast<const __half2*>(&pb0));
+        const float2 ph23 = __half22float2(*reinterpret_cast<const __half2*>(&pb1));
+        const uint32_t pl0 = pack_half2(pe[0] * vst[0] - ph01.x, pe[1] * vst[1] - ph01.y);
+        const uint32_t pl1 = pack_half2(pe[2] * vst[2] - ph23.x, pe[3] * vst[3] - ph23.y);
+        CodeRunDyn<4, W> icv[4];
+        CodeRunDyn<4, BR> rcv[4];
+        uint32_t frv[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t key = (uint32_t)(kw0 + (e >> 1) * 8 + t4 * 2 + (e & 1));
+          const uint32_t fv = vflag((int)key);
+          const uint32_t lo = (uint32_t)g4 * 4u;
+          frv[e] = (fv >> lo) & 0xfu;
+          uint32_t ibit, rbit;
+          if constexpr (kPaged) {
+            ibit = key * 32u * W + lo * W;
+            rbit = key * 32u * BR + lo * BR;
+          } else {
+            const uint64_t c = (int)key < nvalid
+                                   ? (uint64_t)vax[key] + lo - (uint64_t)__popc(fv & ((1u << lo) - 1u))
+                                   : (uint64_t)vax[0];
+            ibit = (uint32_t)(c * W - vib0);
+            rbit = (uint32_t)(c * BR - vrb0);
+          }
+          icv[e].load(viw, ibit);
+          rcv[e].load(vrw, rbit);
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          uint32_t hx[4], hy[4], lx[4], ly[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const uint32_t frun = frv[e];
+            uint32_t ci, cq;
+            if constexpr (kPaged) {
+              ci = icv[e].get(j);
+              cq = (frun >> j) & 1u ? 0u : rcv[e].get(j);
+            } else if (frun == 0u) {
+              ci = icv[e].get(j);
+              cq = rcv[e].get(j);
+            } else {
+              const int jj = j - __popc(frun & ((1u << j) - 1u));
+              const bool fl = (frun >> j) & 1u;
+              ci = fl ? 0u : icv[e].get_dyn(jj);
+              cq = fl ? 0u : rcv[e].get_dyn(jj);
+            }
+            const uint2 ch = vtab[min(ci, cwmax)], cl = vtab_lo[min(ci, cwmax)];
+            const float qf = (float)cq;
+            const float2 h01 = __half22float2(*reinterpret_cast<const __half2*>(&ch.x));
+            const float2 h23 = __half22float2(*reinterpret_cast<const __half2*>(&ch.y));
+            const float2 l01 = __half22float2(*reinterpret_cast<const __half2*>(&cl.x));
+            const float2 l23 = __half22float2(*reinterpret_cast<const __half2*>(&cl.y));
+            const float v0 = qf * (h01.x + l01.x), v1 = qf * (h01.y + l01.y);
+            const float v2 = qf * (h23.x + l23.x), v3 = qf * (h23.y + l23.y);
+            hx[e] = pack_half2(v0, v1);
+            hy[e] = pack_half2(v2, v3);
+            const float2 r01 = __half22float2(*reinterpret_cast<const __half2*>(&hx[e]));
+            const float2 r23 = __half22float2(*reinterpret_cast<const __half2*>(&hy[e]));
+            lx[e] = pack_half2(v0 - r01.x, v1 - r01.y);
+            ly[e] = pack_half2(v2 - r23.x, v3 - r23.y);
+          }
+          mma_full(oT[2 * j], __byte_perm(hx[0], hx[1], 0x5410), __byte_perm(hx[0], hx[1], 0x7632),
+                   __byte_perm(hx[2], hx[3], 0x5410), __byte_perm(hx[2], hx[3], 0x7632), pb0, pb1);
+          mma_full(oT[2 * j], __byte_perm(lx[0], lx[1], 0x5410), __byte_perm(lx[0], lx[1], 0x7632),
+                   __byte_perm(lx[2], lx[3], 0x5410), __byte_perm(lx[2], lx[3], 0x7632), pb0, pb1);
+          mma_full(oT[2 * j], __byte_perm(hx[0], hx[1], 0x5410), __byte_perm(hx[0], hx[1], 0x7632),
+                   __byte_perm(hx[2], hx[3], 0x5410), __byte_perm(hx[2], hx[3], 0x7632), pl0, pl1);
+          mma_full(oT[2 * j + 1], __byte_perm(hy[0], hy[1], 0x5410), __byte_perm(hy[0], hy[1], 0x7632),
+                   __byte_perm(hy[2], hy[3], 0x5410), __byte_perm(hy[2], hy[3], 0x7632), pb0, pb1);
+          mma_full(oT[2 * j + 1], __byte_perm(ly[0], ly[1], 0x5410), __byte_perm(ly[0], ly[1], 0x7632),
+                   __byte_perm(ly[2], ly[3], 0x5410), __byte_perm(ly[2], ly[3], 0x7632), pb0, pb1);
+          mma_full(oT[2 * j + 1], __byte_perm(hy[0], hy[1], 0x5410), __byte_perm(hy[0], hy[1], 0x7632),
+                   __byte_perm(hy[2], hy[3], 0x5410), __byte_perm(hy[2], hy[3], 0x7632), pl0, pl1);
         }
       }
-      release(k, stage);
+      if constexpr (kFlags) {
+        // ---- outlier V chunks: O[row][dims of chunk c] += p(row, key) * payload
+        const uint32_t fvl = lane < 16 ? vflag(kw0 + lane) : 0u;
+        if (__any_sync(0xffffffffu, fvl != 0u)) {
+          float* pw = pws + warp * 128;  // [row][16 keys]
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        // m-tile 2j: (m = g4, g4+8) = elements (0, 1); m-tile 2j+1: elements (2, 3)
-        // a0 = keys (2t4, 2t4+1) at m = g4 ; a1 = same keys at m = g4+8
-        // a2 = keys (2t4+8, 2t4+9) at m = g4 ; a3 = same keys at m = g4+8
-        const uint32_t x0 = vv[0][j].x, x1 = vv[1][j].x, x2 = vv[2][j].x, x3 = vv[3][j].x;
-        const uint32_t y0 = vv[0][j].y, y1 = vv[1][j].y, y2 = vv[2][j].y, y3 = vv[3][j].y;
-        mma_full(oT[2 * j], __byte_perm(x0, x1, 0x5410), __byte_perm(x0, x1, 0x7632),
-                 __byte_perm(x2, x3, 0x5410), __byte_perm(x2, x3, 0x7632), pb0, pb1);
-        mma_full(oT[2 * j + 1], __byte_perm(y0, y1, 0x5410), __byte_perm(y0, y1, 0x7632),
-                 __byte_perm(y2, y3, 0x5410), __byte_perm(y2, y3, 0x7632), pb0, pb1);
+          for (int e = 0; e < 4; ++e) pw[g4 * 16 + (e >> 1) * 8 + t4 * 2 + (e & 1)] = pe[e];
+          __syncwarp();
+          for (int kk = 0; kk < 16; ++kk) {
+            const uint32_t fv = vflag(kw0 + kk);
+            uint32_t bits = (fv >> (4 * g4)) & 0xfu;
+            if (!bits) continue;
+            const float p0 = pw[(2 * t4) * 16 + kk], p1 = pw[(2 * t4 + 1) * 16 + kk];
+            while (bits) {
+              const int j = __ffs(bits) - 1;
+              bits &= bits - 1u;
+              const ushort4 hv = __ldg(reinterpret_cast<const ushort4*>(p.v.payloads) +
+                                       pay_row(vax, kw0 + kk, fv, 4 * g4 + j));
+              const float x[4] = {__half2float(__ushort_as_half(hv.x)),
+                                  __half2float(__ushort_as_half(hv.y)),
+                                  __half2float(__ushort_as_half(hv.z)),
+                                  __half2float(__ushort_as_half(hv.w))};
+#pragma unroll
+              for (int jj = 0; jj < 4; ++jj) {
+                if (jj != j) continue;  // register-resident oT: compile-time indices
+#pragma unroll
+                for (int d = 0; d < 4; ++d) {
+                  oT[2 * jj + (d >> 1)][(d & 1) * 2 + 0] += p0 * x[d];
+                  oT[2 * jj + (d >> 1)][(d & 1) * 2 + 1] += p1 * x[d];
+                }
+              }
+            }
+          }
+          __syncwarp();
+        }
+        release(k, stage);
       }
     } else {
       release(k, stage);
@@ -818,12 +1147,98 @@ bool plan_att(const hqmq_attention_args* a, AttPlan& pl) {
 }  // namespace
 }  // namespace hqmq
 
+namespace hqmq {
+namespace {
+enum AttKind { kAttF64, kAttPrefillTc, kAttPair, kAttMma, kAttMmaMed3x, kAttSplitSmem, kAttSplit };
+struct AttChoice {
+  AttKind kind;
+  void (*mk)(AttParams);
+  size_t msmem;
+};
+const char* att_kind_name(AttKind k) {
+  switch (k) {
+    case kAttF64: return "attention_f64_kernel";
+    case kAttPrefillTc: return "prefill_tc (tcgen05 flash attention)";
+    case kAttPair: return "attention_pair_kernel (K/V CTA pair)";
+    case kAttMma: return "attention_mma_kernel";
+    case kAttMmaMed3x: return "attention_mma_kernel<Med3x>";
+    case kAttSplitSmem: return "attention_split_kernel<smem>";
+    default: return "attention_split_kernel";
+  }
+}
+// Which kernel hqmq_attention_decode runs for `a` (the plan already checked).
+AttChoice choose_att(const hqmq_attention_args* a, const AttPlan& pl) {
+  AttChoice ch{kAttSplit, nullptr, 0};
+  if (a->precise == 2) {
+    ch.kind = kAttF64;
+    return ch;
+  }
+  const int64_t nrows = a->q_heads / a->kv_heads * a->q_tokens;
+  const size_t tab_bytes = 2 * (size_t)kGroupOrder * a->codebook_size * sizeof(float4);
+  // Med3x caches take the same tensor-core kernel (kFlags): both tensors must
+  // carry the flag bitmap, token offsets and payload rows
+  const bool flags = a->k.flag_words && a->v.flag_words && a->k.token_offsets &&
+                     a->v.token_offsets && a->k.payloads && a->v.payloads;
+  const bool flags_mixed = (a->k.flag_words != nullptr) != (a->v.flag_words != nullptr);
+  const size_t msmem = mma_smem_bytes(a->codebook_size, a->index_bits, a->radius_bits, flags);
+  const bool mma_path = a->head_dim == 128 && !flags_mixed &&
+                        (flags || (!a->k.flag_words && !a->v.flag_words)) &&
+                        nrows <= 8 && a->kv_tokens % 8 == 0 && pl.keys_per_split % 64 == 0 &&
+                        msmem <= kMaxDynSmem && al16(a->k.index_words) && al16(a->k.radius_words) &&
+                        al16(a->k.scales) && al16(a->v.index_words) && al16(a->v.radius_words) &&
+                        al16(a->v.scales) && !a->precise &&
+                        (!flags || (al16(a->k.flag_words) && al16(a->k.token_offsets) &&
+                                    al16(a->v.flag_words) && al16(a->v.token_offsets)));
+  // (index_bits, radius_bits) instances of the tensor-core kernel
+  void (*mk)(AttParams) = nullptr;
+  const int wb = a->index_bits * 16 + a->radius_bits;
+  if (flags) {
+    switch (wb) {
+      case 9 * 16 + 4: mk = attention_mma_kernel<9, 4, false, true>; break;
+      case 11 * 16 + 4: mk = attention_mma_kernel<11, 4, false, true>; break;
+      case 11 * 16 + 6: mk = attention_mma_kernel<11, 6, false, true>; break;  // C3 (Qwen)
+      case 13 * 16 + 4: mk = attention_mma_kernel<13, 4, false, true>; break;
+      default: break;
+    }
+  } else switch (wb) {
+    case 9 * 16 + 4: mk = attention_mma_kernel<9, 4>; break;    // S = 16..21, b_r 4
+    case 10 * 16 + 4: mk = attention_mma_kernel<10, 4>; break;
+    case 11 * 16 + 4: mk = attention_mma_kernel<11, 4>; break;  // S = 43..85 (S=64), b_r 4
+    case 12 * 16 + 4: mk = attention_mma_kernel<12, 4>; break;
+    case 13 * 16 + 4: mk = attention_mma_kernel<13, 4>; break;  // S = 171..341 (S=256)
+    case 11 * 16 + 6: mk = attention_mma_kernel<11, 6>; break;  // Qwen config b_r 6
+    case 11 * 16 + 3: mk = attention_mma_kernel<11, 3>; break;
+    case 12 * 16 + 3: mk = attention_mma_kernel<12, 3>; break;
+    default: break;
+  }
+  if (prefill_tc_applicable(a)) {
+    ch.kind = kAttPrefillTc;
+  } else if (pair_ok(a)) {
+    ch.kind = kAttPair;
+  } else if (mma_path && mk) {
+    ch.kind = flags ? kAttMmaMed3x : kAttMma;
+    ch.mk = mk;
+    ch.msmem = msmem;
+  } else {
+    ch.kind = tab_bytes <= 160 * 1024 ? kAttSplitSmem : kAttSplit;
+  }
+  return ch;
+}
+}  // namespace
+}  // namespace hqmq
+
 extern "C" {
 
 size_t hqmq_attention_workspace_bytes(const hqmq_attention_args* a) {
   hqmq::AttPlan pl;
   if (!hqmq::plan_att(a, pl)) return 0;
   return pl.ws;
+}
+
+const char* hqmq_attention_kernel_name(const hqmq_attention_args* a) {
+  hqmq::AttPlan pl;
+  if (!hqmq::plan_att(a, pl)) return "invalid";
+  return hqmq::att_kind_name(hqmq::choose_att(a, pl).kind);
 }
 
 int hqmq_attention_decode(const hqmq_attention_args* a, void* stream) {
@@ -882,37 +1297,18 @@ int hqmq_attention_decode(const hqmq_attention_args* a, void* stream) {
   const int64_t parts = a->batch * a->kv_heads * p.nrows * pl.splits;
   p.part_o = ws;
   p.part_ml = ws ? ws + parts * a->head_dim : nullptr;
-  const size_t tab_bytes = 2 * (size_t)kGroupOrder * a->codebook_size * sizeof(float4);
   const dim3 grid((unsigned)pl.splits, (unsigned)(a->batch * a->kv_heads), (unsigned)pl.row_groups);
-  const size_t msmem = mma_smem_bytes(a->codebook_size, a->index_bits, a->radius_bits);
-  const bool mma_path = a->head_dim == 128 && !a->k.flag_words && !a->v.flag_words &&
-                        p.nrows <= 8 && a->kv_tokens % 8 == 0 && pl.keys_per_split % 64 == 0 &&
-                        msmem <= 200 * 1024 && al16(a->k.index_words) && al16(a->k.radius_words) &&
-                        al16(a->k.scales) && al16(a->v.index_words) && al16(a->v.radius_words) &&
-                        al16(a->v.scales) && !a->precise;
-  // (index_bits, radius_bits) instances of the tensor-core kernel
-  void (*mk)(AttParams) = nullptr;
-  const int wb = a->index_bits * 16 + a->radius_bits;
-  switch (wb) {
-    case 9 * 16 + 4: mk = attention_mma_kernel<9, 4>; break;    // S = 16..21, b_r 4
-    case 10 * 16 + 4: mk = attention_mma_kernel<10, 4>; break;
-    case 11 * 16 + 4: mk = attention_mma_kernel<11, 4>; break;  // S = 43..85 (S=64), b_r 4
-    case 12 * 16 + 4: mk = attention_mma_kernel<12, 4>; break;
-    case 13 * 16 + 4: mk = attention_mma_kernel<13, 4>; break;  // S = 171..341 (S=256)
-    case 11 * 16 + 6: mk = attention_mma_kernel<11, 6>; break;  // Qwen config b_r 6
-    case 11 * 16 + 3: mk = attention_mma_kernel<11, 3>; break;
-    case 12 * 16 + 3: mk = attention_mma_kernel<12, 3>; break;
-    default: break;
-  }
-  if (prefill_tc_applicable(a)) return launch_prefill_tc(a, st);
-  if (pair_ok(a)) {
+  const AttChoice ch = choose_att(a, pl);
+  if (ch.kind == kAttPrefillTc) return launch_prefill_tc(a, st);
+  if (ch.kind == kAttPair) {
     p.part_o = ws;
     return launch_pair_attention(p, a->kv_tokens, st);
   }
-  if (mma_path && mk) {
-    cudaFuncSetAttribute(mk, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    mk<<<dim3((unsigned)pl.splits, (unsigned)(a->batch * a->kv_heads)), kMThreads, msmem, st>>>(p);
-  } else if (tab_bytes <= 160 * 1024) {
+  if (ch.kind == kAttMma || ch.kind == kAttMmaMed3x) {
+    cudaFuncSetAttribute(ch.mk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem);
+    ch.mk<<<dim3((unsigned)pl.splits, (unsigned)(a->batch * a->kv_heads)), kMThreads, ch.msmem, st>>>(p);
+  } else if (ch.kind == kAttSplitSmem) {
+    const size_t tab_bytes = 2 * (size_t)kGroupOrder * a->codebook_size * sizeof(float4);
     cudaFuncSetAttribute(attention_split_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          160 * 1024);
     attention_split_kernel<true><<<grid, kAttThreads, tab_bytes, st>>>(p);
@@ -939,7 +1335,8 @@ bool paged_pair_ok(const hqmq_paged_attention_args* a) {
   return false;
 #endif
   return hqmq::pair_applicable(a->batch * a->kv_heads, a->head_dim, a->q_heads / a->kv_heads, a->max_kv_tokens, a->codebook_size,
-                         a->index_bits, a->radius_bits, false, a->k.joint_f16, a->v.joint_f16);
+                         a->index_bits, a->radius_bits, a->k.flag_pages || a->v.flag_pages,
+                         a->k.joint_f16, a->v.joint_f16);
 }
 bool plan_paged(const hqmq_paged_attention_args* a, PagedPlan& pl) {
   using namespace hqmq;
@@ -998,7 +1395,9 @@ int hqmq_attention_decode_paged(const hqmq_paged_attention_args* a, void* stream
   auto view = [](const hqmq_paged_view& v) {
     AttView o;
     o.scales = v.scale_pages; o.idxw = v.index_pages; o.radw = v.radius_pages;
-    o.flagw = nullptr; o.payloads = nullptr; o.tokoff = nullptr;
+    // Med3x pages: flag words, and the payload row of each token's first
+    // flagged chunk in the aux (token offset) slot
+    o.flagw = v.flag_pages; o.payloads = v.payloads; o.tokoff = v.payoff_pages;
     o.table = reinterpret_cast<const float4*>(v.joint_f32);
     o.table16 = reinterpret_cast<const uint2*>(v.joint_f16);
     o.table64 = nullptr;
@@ -1014,16 +1413,26 @@ int hqmq_attention_decode_paged(const hqmq_paged_attention_args* a, void* stream
   p.kv_lens = a->kv_lens; p.block_table = a->block_table; p.max_pages = a->max_pages;
   if (paged_pair_ok(a)) return launch_pair_attention(p, a->max_kv_tokens, st);
   void (*mk)(AttParams) = nullptr;
-  switch (a->index_bits * 16 + a->radius_bits) {
+  const bool flags = a->k.flag_pages != nullptr;
+  if (flags != (a->v.flag_pages != nullptr)) return HQMQ_ERR_INVALID_ARGUMENT;
+  if (flags && (!a->k.payoff_pages || !a->v.payoff_pages || !a->k.payloads || !a->v.payloads ||
+                !al16(a->k.flag_pages) || !al16(a->v.flag_pages) || !al16(a->k.payoff_pages) ||
+                !al16(a->v.payoff_pages)))
+    return HQMQ_ERR_INVALID_ARGUMENT;
+  switch (a->index_bits * 16 + a->radius_bits + (flags ? 1024 : 0)) {
     case 9 * 16 + 4: mk = attention_mma_kernel<9, 4, true>; break;
     case 11 * 16 + 4: mk = attention_mma_kernel<11, 4, true>; break;
     case 13 * 16 + 4: mk = attention_mma_kernel<13, 4, true>; break;
     case 11 * 16 + 6: mk = attention_mma_kernel<11, 6, true>; break;
+    case 1024 + 9 * 16 + 4: mk = attention_mma_kernel<9, 4, true, true>; break;
+    case 1024 + 11 * 16 + 4: mk = attention_mma_kernel<11, 4, true, true>; break;
+    case 1024 + 13 * 16 + 4: mk = attention_mma_kernel<13, 4, true, true>; break;
+    case 1024 + 11 * 16 + 6: mk = attention_mma_kernel<11, 6, true, true>; break;
     default: return HQMQ_ERR_UNSUPPORTED;
   }
-  const size_t msmem = mma_smem_bytes(a->codebook_size, a->index_bits, a->radius_bits);
-  if (msmem > 200 * 1024) return HQMQ_ERR_UNSUPPORTED;
-  cudaFuncSetAttribute(mk, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  const size_t msmem = mma_smem_bytes(a->codebook_size, a->index_bits, a->radius_bits, flags);
+  if (msmem > kMaxDynSmem) return HQMQ_ERR_UNSUPPORTED;
+  cudaFuncSetAttribute(mk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDynSmem);
   mk<<<dim3((unsigned)pl.splits, (unsigned)(a->batch * a->kv_heads)), kMThreads, msmem, st>>>(p);
   int rc = check_launch();
   if (rc != HQMQ_OK) return rc;

@@ -106,6 +106,44 @@ struct CodeRun {
   }
 };
 
+// N codes of WIDTH bits from an arbitrary bit of a shared-memory stream (the
+// Med3x layout: a token's codes start wherever its coded offset puts them).
+// get(i) reads code i at a compile-time position; get_dyn(j) a runtime one
+// (code j of the run after flagged chunks were skipped) through a select
+// chain over the loaded words (no local memory).
+template <int N, int WIDTH>
+struct CodeRunDyn {
+  static constexpr int kNW = (31 + N * WIDTH + 31) / 32;
+  uint32_t r[kNW];
+  __device__ __forceinline__ void load(const uint32_t* __restrict__ s, uint32_t bit) {
+    const uint32_t* p = s + (bit >> 5);
+    const uint32_t sh = bit & 31;
+    uint32_t w[kNW + 1];
+#pragma unroll
+    for (int i = 0; i < kNW; ++i) w[i] = p[i];
+    w[kNW] = 0u;
+#pragma unroll
+    for (int i = 0; i < kNW; ++i) r[i] = __funnelshift_r(w[i], w[i + 1], sh);
+  }
+  __device__ __forceinline__ uint32_t get(int i) const {
+    const int b = i * WIDTH, wi = b >> 5, sh = b & 31;
+    uint32_t v = sh == 0 ? r[wi] : __funnelshift_r(r[wi], wi + 1 < kNW ? r[wi + 1] : 0u, sh);
+    return WIDTH == 32 ? v : (v & ((1u << WIDTH) - 1u));
+  }
+  __device__ __forceinline__ uint32_t get_dyn(int j) const {
+    const uint32_t b = (uint32_t)j * WIDTH, wi = b >> 5, sh = b & 31;
+    uint32_t lo = r[0], hi = kNW > 1 ? r[1] : 0u;
+#pragma unroll
+    for (int i = 1; i < kNW; ++i)
+      if (wi == (uint32_t)i) {
+        lo = r[i];
+        hi = i + 1 < kNW ? r[i + 1] : 0u;
+      }
+    const uint32_t v = __funnelshift_r(lo, hi, sh);
+    return WIDTH == 32 ? v : (v & ((1u << WIDTH) - 1u));
+  }
+};
+
 // split-KV merge of per-(row, part) partial (m, l, O) (attention.cu)
 __global__ void combine_kernel(AttParams p);
 

@@ -313,7 +313,7 @@ __host__ __device__ inline size_t fd_table_bytes(int ncw) {
 }
 
 template <typename OutT, int W, int BR, bool kTile = false>
-__global__ void __launch_bounds__(256) decode_fast_kernel(DecParams p) {
+__global__ void __launch_bounds__(256, 7) decode_fast_kernel(DecParams p) {
   extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ __align__(8) uint64_t full[kFDStages];
   __shared__ __align__(8) uint64_t tab_bar;
@@ -856,6 +856,38 @@ bool fill(const hqmq_decode_args* a, DecParams& p, bool need_range) {
   return true;
 }
 
+// CTAs per row for a persistent-style launch over ntile tiles per row: as many
+// as are co-resident in ONE wave (occupancy query, cached per kernel / smem /
+// device), so that no CTA waits for a second wave while the rest idle.
+template <typename K>
+int64_t one_wave_ctas_per_row(K kern, size_t smem, int64_t rows, int64_t ntile) {
+  struct Entry {
+    const void* k;
+    size_t smem;
+    int dev, slots;
+  };
+  static thread_local Entry cache[8] = {};
+  static thread_local int next = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  // the whole unified L1 / shared array as shared memory, so that the
+  // occupancy the grid is sized for is the one the launch gets
+  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout,
+                       (int)cudaSharedmemCarveoutMaxShared);
+  int slots = 0;
+  for (const Entry& e : cache)
+    if (e.k == reinterpret_cast<const void*>(kern) && e.smem == smem && e.dev == dev) slots = e.slots;
+  if (!slots) {
+    int per_sm = 0, sms = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    slots = std::max(1, per_sm) * std::max(1, sms);
+    cache[next] = Entry{reinterpret_cast<const void*>(kern), smem, dev, slots};
+    next = (next + 1) % 8;
+  }
+  return std::max<int64_t>(1, std::min<int64_t>(slots / rows, ntile));
+}
+
 template <typename OutT>
 int launch_decode(DecParams& p, const hqmq_decode_args* a, cudaStream_t st) {
   const int64_t rows = p.B * p.H;
@@ -871,10 +903,8 @@ int launch_decode(DecParams& p, const hqmq_decode_args* a, cudaStream_t st) {
     const size_t fsmem = fd_table_bytes<OutT>(kGroupOrder * p.S) + (size_t)kFlStages * g.stage_bytes;
     cudaFuncSetAttribute(decode_flag_tma_kernel<OutT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
-    const int64_t ntile = ceil_div(p.nt, kFlTok);
-    const int per_sm = std::max<int>(1, std::min<int>(8, (int)((227 * 1024) / (fsmem + 1024))));
-    const int64_t want = std::max<int64_t>(1, ceil_div((int64_t)148 * per_sm, rows));
-    const int64_t bx = std::max<int64_t>(1, std::min<int64_t>(want, ntile));
+    const int64_t bx =
+        one_wave_ctas_per_row(decode_flag_tma_kernel<OutT>, fsmem, rows, ceil_div(p.nt, kFlTok));
     decode_flag_tma_kernel<OutT><<<dim3((unsigned)bx, (unsigned)rows), 256, fsmem, st>>>(p);
     return check();
   }
@@ -904,10 +934,7 @@ int launch_decode(DecParams& p, const hqmq_decode_args* a, cudaStream_t st) {
       default: break;
     }
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    const int64_t ntile = ceil_div(p.nt, kFDTok);
-    const int per_sm = std::max<int>(1, std::min<int>(8, (int)((227 * 1024) / (fsmem + 1024))));
-    const int64_t want = std::max<int64_t>(1, ceil_div((int64_t)148 * per_sm, rows));
-    const int64_t bx = std::max<int64_t>(1, std::min<int64_t>(want, ntile));
+    const int64_t bx = one_wave_ctas_per_row(kern, fsmem, rows, ceil_div(p.nt, kFDTok));
     kern<<<dim3((unsigned)bx, (unsigned)rows), 256, fsmem, st>>>(p);
     return check();
   }
@@ -916,17 +943,50 @@ int launch_decode(DecParams& p, const hqmq_decode_args* a, cudaStream_t st) {
   const int64_t bx = std::max<int64_t>(1, std::min<int64_t>(want, ceil_div(nck, kDecThreads * kDecR)));
   const dim3 grid((unsigned)bx, (unsigned)rows);
   if (use_smem) {
-    static thread_local bool set = false;
-    if (!set) {
-      cudaFuncSetAttribute(decode_kernel<OutT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)kDecSmemLimit);
-      set = true;
-    }
+    // set on every launch: the attribute is per device, and a process may drive several
+    cudaFuncSetAttribute(decode_kernel<OutT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kDecSmemLimit);
     decode_kernel<OutT, true><<<grid, kDecThreads, smem, st>>>(p);
   } else {
     decode_kernel<OutT, false><<<grid, kDecThreads, 0, st>>>(p);
   }
   return check();
+}
+
+// Med3x compact layout -> fixed per-token code slots (the paged cache's
+// layout): warp = token, lane = chunk (head_dim 128).  Token t's index codes
+// go to bits [32*w*t + lane*w, +w) of `islots` (w words per token), radius
+// codes likewise; a flagged chunk's slot is 0.  payoff[t] = payload_base +
+// the token's first payload row (t*32 - token_offsets[t]).
+__global__ void __launch_bounds__(256) expand_kernel(DecParams p, uint32_t* __restrict__ islots,
+                                                     uint32_t* __restrict__ rslots,
+                                                     uint32_t* __restrict__ payoff,
+                                                     uint32_t payload_base, int64_t ntok) {
+  __shared__ uint32_t sw[8][16 + 8];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int w = p.w, br = p.br;
+  for (int64_t tok = (int64_t)blockIdx.x * 8 + warp; tok < ntok; tok += (int64_t)gridDim.x * 8) {
+    const uint32_t fw = __ldg(p.flagw + tok);
+    const bool fl = (fw >> lane) & 1u;
+    const uint32_t base = __ldg(p.tokoff + tok);
+    const uint64_t pos = (uint64_t)base + lane - __popc(fw & ((1u << lane) - 1u));
+    const uint32_t idx = fl ? 0u : read_bits(p.idxw, pos * (uint64_t)w, w);
+    const uint32_t q = fl ? 0u : read_bits(p.radw, pos * (uint64_t)br, br);
+    if (lane < 24) sw[warp][lane] = 0u;
+    __syncwarp();
+    auto put = [&](uint32_t* dst, uint32_t v, int width) {
+      const uint32_t bit = (uint32_t)lane * width;
+      atomicOr(dst + (bit >> 5), v << (bit & 31));
+      if ((bit & 31) + width > 32) atomicOr(dst + (bit >> 5) + 1, v >> (32 - (bit & 31)));
+    };
+    put(sw[warp], idx, w);
+    put(sw[warp] + 16, q, br);
+    __syncwarp();
+    if (lane < w) islots[tok * w + lane] = sw[warp][lane];
+    if (lane < br) rslots[tok * br + lane] = sw[warp][16 + lane];
+    if (lane == 0) payoff[tok] = payload_base + (uint32_t)(tok * 32 - (int64_t)base);
+    __syncwarp();
+  }
 }
 }  // namespace
 
@@ -962,10 +1022,7 @@ int decode_fp16_tiles(const hqmq_decode_args* a, int tile_log2, int mn, int64_t 
     default: break;
   }
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-  const int64_t ntile = ceil_div(p.nt, kFDTok);
-  const int per_sm = std::max<int>(1, std::min<int>(8, (int)((227 * 1024) / (fsmem + 1024))));
-  const int64_t want = std::max<int64_t>(1, ceil_div((int64_t)148 * per_sm, rows));
-  const int64_t bx = std::max<int64_t>(1, std::min<int64_t>(want, ntile));
+  const int64_t bx = one_wave_ctas_per_row(kern, fsmem, rows, ceil_div(p.nt, kFDTok));
   kern<<<dim3((unsigned)bx, (unsigned)rows), 256, fsmem, st>>>(p);
   return check();
 }
@@ -993,6 +1050,22 @@ int hqmq_decode(const hqmq_decode_args* a, void* stream) {
     }
     default: return HQMQ_ERR_INVALID_ARGUMENT;
   }
+}
+
+int hqmq_expand_tokens(const hqmq_decode_args* a, uint32_t* index_slots, uint32_t* radius_slots,
+                       uint32_t* payload_offsets, uint32_t payload_base, void* stream) {
+  using namespace hqmq;
+  DecParams p;
+  if (!fill(a, p, false)) return HQMQ_ERR_INVALID_ARGUMENT;
+  if (p.D != 128 || !p.flagw || !p.tokoff || p.w > 16 || p.br > 8 || !index_slots ||
+      !radius_slots || !payload_offsets)
+    return HQMQ_ERR_INVALID_ARGUMENT;
+  const int64_t ntok = p.B * p.H * p.T;
+  if (ntok == 0) return HQMQ_OK;
+  const int64_t blocks = std::min<int64_t>(ceil_div(ntok, 8), 148 * 16);
+  expand_kernel<<<(unsigned)blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      p, index_slots, radius_slots, payload_offsets, payload_base, ntok);
+  return check();
 }
 
 int hqmq_unpack(const hqmq_decode_args* a, int32_t* indices, uint8_t* quanta, uint8_t* flags,

@@ -1162,6 +1162,7 @@ struct RadixParams {
   uint32_t* hist;  // [G][kBins]
   unsigned int* done;
   int G;
+  int norms_only;  // pass 0 stores the squared norms and builds no histogram (fixed thresholds)
 };
 
 // Shared-memory histogram add.  (Pass 0's digits -- exponent + top mantissa
@@ -1267,6 +1268,7 @@ __global__ void __launch_bounds__(kHistThreads) radix_hist_kernel(RadixParams p)
         }
       }
 #pragma unroll
+      if (p.norms_only) continue;
       for (int j = 0; j < kRB; ++j) {
         const int64_t i = i0 + j * kHistThreads + threadIdx.x;
         const unsigned long long key = (unsigned long long)__double_as_longlong(rr[j]);
@@ -1290,7 +1292,7 @@ __global__ void __launch_bounds__(kHistThreads) radix_hist_kernel(RadixParams p)
       }
     }
   }
-  if (p.pass == 2) return;  // compaction only; passes 2-4 finish in radix_tail_kernel
+  if (p.pass == 2 || p.norms_only) return;  // compaction only / norms only
   __syncthreads();
   const int g = p.per_head ? (int)(blockIdx.y % p.H) : 0;
   uint32_t* hg = p.hist + (int64_t)g * kBins;
@@ -1362,6 +1364,16 @@ __global__ void __launch_bounds__(kTailThreads) radix_tail_kernel(RadixParams p)
     p.groups[g].threshold =
         __dmul_rn(p.multiplier, __dsqrt_rn(__longlong_as_double((long long)s_pref)));
   }
+}
+
+// Frozen thresholds (incremental Med3x caches): groups[g].threshold = fixed[g].
+__global__ void set_thresholds_kernel(RadixGroup* groups, const double* fixed, int G) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g < G) groups[g].threshold = fixed[g];
+}
+__global__ void copy_thresholds_kernel(const RadixGroup* groups, double* out, int G) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g < G) out[g] = groups[g].threshold;
 }
 
 __global__ void radix_init_kernel(RadixGroup* groups, unsigned int* cand_n, int G,
@@ -1524,11 +1536,20 @@ int launch_encode(const hqmq_encode_args* a, const Layout& L, cudaStream_t st) {
     const int64_t bx_full = std::max<int64_t>(
         1, std::min<int64_t>(ceil_div((int64_t)148 * 4, L.rows), ceil_div(row_chunks, kHistThreads * 8)));
 
-    for (int pass = 0; pass <= 2; ++pass) {
-      rp.pass = pass;
+    rp.norms_only = a->fixed_thresholds != nullptr;
+    if (rp.norms_only) {  // frozen thresholds: the norms pass only
+      rp.pass = 0;
       radix_hist_kernel<InT><<<dim3((unsigned)bx_full, (unsigned)L.rows), kHistThreads, 0, st>>>(rp);
+      set_thresholds_kernel<<<(L.G + 127) / 128, 128, 0, st>>>(groups, a->fixed_thresholds, L.G);
+    } else {
+      for (int pass = 0; pass <= 2; ++pass) {
+        rp.pass = pass;
+        radix_hist_kernel<InT><<<dim3((unsigned)bx_full, (unsigned)L.rows), kHistThreads, 0, st>>>(rp);
+      }
+      radix_tail_kernel<<<L.G, kTailThreads, 0, st>>>(rp);
     }
-    radix_tail_kernel<<<L.G, kTailThreads, 0, st>>>(rp);
+    if (a->thresholds_out)
+      copy_thresholds_kernel<<<(L.G + 127) / 128, 128, 0, st>>>(groups, a->thresholds_out, L.G);
     uint32_t* counts = reinterpret_cast<uint32_t*>(ws + L.off_counts);
     size_t cub_bytes = L.cub_bytes;
     if (L.warp_path) {

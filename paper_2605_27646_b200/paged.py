@@ -5,9 +5,9 @@ decode-attention kernel).
 The reference keeps one dense tensor per (layer, role) and has no append
 (codec.py:232-287).  Here a cache for one layer holds K and V as pools of
 128-token pages; a page is one (sequence, kv head) row's tokens
-[128 i, 128 i + 128) in the token-aligned stream format the encoder already
-produces without Med3x (index_bits words of index codes, radius_bits words of
-radius codes and one fp16 scale per token), so appending is:
+[128 i, 128 i + 128) in fixed per-token code slots (index_bits words of index
+codes, radius_bits words of radius codes and one fp16 scale per token), so
+appending is:
 
   1. encode_tensor of the new tokens (the sm_100a encode, bit-identical to the
      reference on those tokens: without extraction the codec is token-local);
@@ -15,8 +15,25 @@ radius codes and one fp16 scale per token), so appending is:
      (device index_copy); pages are taken from a free list as rows grow.
 
 attend() runs the decode-attention kernel with a block table
-(hqmq_attention_decode_paged).  Med3x is not supported here: its median
-pools the whole (layer, role) call, which an append cannot reproduce.
+(hqmq_attention_decode_paged).
+
+Med3x (outlier_multiplier set).  The reference pools the median over the
+whole (layer, role) call (codec.py:208-219; outliers.py:50-55) and has no
+incremental form (PAPER.md:138 names an EMA or frozen median as the options).
+This cache uses a FROZEN threshold: the first append of each role (the
+prefill) is encoded exactly as the reference's encode_tensor of that call --
+its own C * lower median, bit-identical -- and its thresholds
+(QuantizedTensor.outlier_thresholds; one per head with per-head pooling) are
+kept; every later append flags chunks with r > that frozen threshold (the
+reference's strict test) instead of re-pooling.  Deviation from a one-shot
+encode of the concatenation: appended tokens are flagged against the prefill's
+median rather than the median of everything cached so far.  The appended
+encode is then token-local (appending tokens one by one equals appending them
+at once) and bit-exact against the oracle's encode with the same thresholds.
+Thresholds can also be given up front (outlier_thresholds=).  Storage: each
+token keeps its fixed code slots (a flagged chunk's slot is 0), a 32-bit flag
+word and the row of its first payload in a per-role fp16 payload pool
+(hqmq_expand_tokens converts the encoder's compact sections).
 """
 
 from __future__ import annotations
@@ -38,10 +55,11 @@ class PagedKVCache:
     def __init__(self, config: CodecConfig, batch: int, kv_heads: int, max_tokens: int,
                  layer: int = 0, bank: CodebookBank | None = None, head_base: int = 0,
                  head_dim: int = 128, num_pages: int | None = None, device="cuda",
-                 page_order_seed: int | None = None):
+                 page_order_seed: int | None = None, outlier_thresholds=None):
         torch = _torch()
-        if config.outlier_multiplier is not None:
-            raise InvalidArgument("paged caches hold token-aligned streams: no outlier extraction")
+        self.med3x = config.outlier_multiplier is not None
+        if outlier_thresholds is not None and not self.med3x:
+            raise InvalidArgument("outlier_thresholds requires outlier extraction")
         if head_dim != 128:
             raise InvalidArgument("paged caches support head_dim 128")
         if batch < 1 or kv_heads < 1 or max_tokens < 1:
@@ -69,6 +87,21 @@ class PagedKVCache:
                 "scales": torch.zeros((self.num_pages + 1, PAGE_TOKENS), dtype=torch.float16,
                                       device=dev),
             }
+            if self.med3x:
+                self.pages[role]["flags"] = torch.zeros((self.num_pages + 1, PAGE_TOKENS),
+                                                        dtype=torch.int32, device=dev)
+                self.pages[role]["payoff"] = torch.zeros((self.num_pages + 1, PAGE_TOKENS),
+                                                         dtype=torch.int32, device=dev)
+        # Med3x: per-role fp16 payload pools (rows in use) and frozen thresholds
+        self.payloads = {r: torch.zeros((1024, 4), dtype=torch.float16, device=dev)
+                         for r in ("K", "V")} if self.med3x else None
+        self.n_payload = {"K": 0, "V": 0}
+        self.thresholds = {"K": None, "V": None}
+        if outlier_thresholds is not None:
+            for r in ("K", "V"):
+                thr = outlier_thresholds[r] if isinstance(outlier_thresholds, dict) \
+                    else outlier_thresholds
+                self.thresholds[r] = torch.as_tensor(thr, dtype=torch.float64).reshape(-1).to(dev)
         self.block_table = torch.full((batch, kv_heads, self.max_pages), -1, dtype=torch.int32,
                                       device=dev)
         self._table_host = [[[-1] * self.max_pages for _ in range(kv_heads)] for _ in range(batch)]
@@ -126,15 +159,49 @@ class PagedKVCache:
         w, br = self.config.index_bits, self.config.radius_bits
         for role, x in (("K", k), ("V", v)):
             qt = encode_tensor(x, self.config, layer=self.layer, role=role, bank=self.bank,
-                               head_base=self.head_base, device=self.device)
+                               head_base=self.head_base, device=self.device,
+                               outlier_thresholds=self.thresholds[role] if self.med3x else None)
             pool = self.pages[role]
-            pool["index"].view(-1, w).index_copy_(0, slots, qt.index_words[: n_tok * w].view(n_tok, w))
-            pool["radius"].view(-1, br).index_copy_(0, slots,
-                                                    qt.radius_words[: n_tok * br].view(n_tok, br))
+            if self.med3x:
+                if self.thresholds[role] is None:  # the prefill freezes its thresholds
+                    self.thresholds[role] = qt.outlier_thresholds.clone()
+                iw, rw, payoff = self._expand(role, qt, n_tok)
+                pool["flags"].view(-1).index_copy_(0, slots, qt.flag_words[:n_tok])
+                pool["payoff"].view(-1).index_copy_(0, slots, payoff)
+            else:
+                iw, rw = qt.index_words[: n_tok * w], qt.radius_words[: n_tok * br]
+            pool["index"].view(-1, w).index_copy_(0, slots, iw.view(n_tok, w))
+            pool["radius"].view(-1, br).index_copy_(0, slots, rw.view(n_tok, br))
             pool["scales"].view(-1).index_copy_(0, slots, qt.scales.reshape(-1))
         for b in seqs:
             self.lengths[b] += n_new
         self.kv_lens.copy_(torch.tensor(self.lengths, dtype=torch.int32))
+
+    def _expand(self, role, qt, n_tok):
+        """Med3x: the encoder's compact sections -> fixed per-token slots and
+        payload-row offsets, the payload rows appended to the role's pool
+        (hqmq_expand_tokens)."""
+        torch = _torch()
+        c, dev = self.config, self.device
+        n_pay = qt.n_payload
+        base = self.n_payload[role]
+        if base + n_pay >= 2 ** 32:
+            raise InvalidArgument("Med3x payload pool exceeds 2^32 rows")
+        pool = self.payloads[role]
+        if base + n_pay > pool.shape[0]:  # grow geometrically
+            grown = torch.zeros((max(2 * pool.shape[0], base + n_pay), 4), dtype=torch.float16,
+                                device=dev)
+            grown[:base].copy_(pool[:base])
+            self.payloads[role] = pool = grown
+        pool[base:base + n_pay].copy_(qt.payloads)
+        self.n_payload[role] = base + n_pay
+        iw = torch.empty(n_tok * c.index_bits, dtype=torch.int32, device=dev)
+        rw = torch.empty(n_tok * c.radius_bits, dtype=torch.int32, device=dev)
+        payoff = torch.empty(n_tok, dtype=torch.int32, device=dev)
+        args = qt._decode_args(0, qt.shape.tokens, nat.F32, None, None, None, None)
+        nat.launch(dev, "hqmq_expand_tokens", nat.lib().hqmq_expand_tokens, ctypes.byref(args),
+                   iw.data_ptr(), rw.data_ptr(), payoff.data_ptr(), base)
+        return iw, rw, payoff
 
     # ------------------------------------------------------------ attend
     def attend(self, q, scale: float | None = None, out=None, num_splits: int = 0):
@@ -169,6 +236,10 @@ class PagedKVCache:
             view.scale_pages = pool["scales"].data_ptr()
             view.joint_f32 = tabs["joint_f32"].data_ptr()
             view.joint_f16 = tabs["joint_f16"].data_ptr()
+            if self.med3x:
+                view.flag_pages = pool["flags"].data_ptr()
+                view.payoff_pages = pool["payoff"].data_ptr()
+                view.payloads = self.payloads[role].data_ptr()
         a.num_splits = num_splits
         L = nat.lib()
         ws_bytes = int(L.hqmq_paged_attention_workspace_bytes(ctypes.byref(a)))

@@ -51,7 +51,7 @@ def test_struct_layouts_match_header():
     """ctypes mirrors of the C structs have the C layout (sizes from the header order)."""
     from paper_2605_27646_b200 import _native
 
-    assert ctypes.sizeof(_native.EncodeArgs) == 208
+    assert ctypes.sizeof(_native.EncodeArgs) == 224
     assert _native.EncodeArgs.outlier_multiplier.offset == 48
     assert _native.EncodeArgs.data.offset == 64
     assert ctypes.sizeof(_native.DecodeArgs) == 152
