@@ -27,6 +27,7 @@ from .codec import (
     encode_tensor,
     quantize_dequantize,
 )
+from .covering import CoveringEstimate, estimate_covering
 from .errors import (
     ConfigMismatch,
     CorruptData,

@@ -5,9 +5,13 @@ dequantize subcommands (cli.py:99-173) running on the sm_100a kernels.
     python -m paper_2605_27646_b200.cli dequantize in.kvpack out.raw [--dtype f16]
 
 Same arguments, files (kvpack v1, KVRW raw) and exit codes as the reference:
-0 ok, 2 usage (argparse), 3 invalid / corrupt input (cli.py:250-256).  The
-reference's analysis subcommands (sweep, bench, covering, bits,
-verify-group) are outside this build's scope.
+0 ok, 2 usage (argparse), 3 invalid / corrupt input (cli.py:250-256).
+`covering` (cli.py:136-141,200-210) runs the Monte-Carlo covering estimates
+with the nearest-codeword scan on the GPU (covering.py).  The reference's
+other analysis subcommands (sweep, bench, bits, verify-group) are outside
+this build's scope.
+
+    python -m paper_2605_27646_b200.cli covering --sizes 1,4,16,64,256 --probes 100000
 """
 
 from __future__ import annotations
@@ -43,7 +47,21 @@ def build_parser() -> argparse.ArgumentParser:
     p.add_argument("input")
     p.add_argument("output")
     p.add_argument("--dtype", choices=["f32", "f16"], default="f32")
+    p = sub.add_parser("covering", help="Monte-Carlo covering estimates, CSV out")
+    p.add_argument("--sizes", type=_int_list, default=[1, 4, 16, 64, 256])
+    p.add_argument("--seed", type=int, default=0)
+    p.add_argument("--probes", type=int, default=100_000)
+    p.add_argument("--probe-seed", type=int, default=0)
+    p.add_argument("--out", default=None)
     return parser
+
+
+def _int_list(text: str) -> list:
+    """cli.py: comma-separated integers."""
+    try:
+        return [int(v) for v in text.split(",") if v.strip()]
+    except ValueError as exc:
+        raise argparse.ArgumentTypeError(f"expected comma-separated integers, got {text!r}") from exc
 
 
 def _quantize(args) -> int:
@@ -69,10 +87,24 @@ def _dequantize(args) -> int:
     return 0
 
 
+def _covering(args) -> int:
+    from .covering import covering_csv, fit_covering_rate
+
+    _, estimates = fit_covering_rate(args.sizes, seed=args.seed, n_probes=args.probes,
+                                     probe_seed=args.probe_seed)
+    if args.out:
+        with open(args.out, "w", newline="") as f:
+            covering_csv(estimates, f)
+    else:
+        covering_csv(estimates, sys.stdout)
+    return 0
+
+
 def main(argv=None) -> int:
     args = build_parser().parse_args(argv)
     try:
-        return {"quantize": _quantize, "dequantize": _dequantize}[args.command](args)
+        return {"quantize": _quantize, "dequantize": _dequantize,
+                "covering": _covering}[args.command](args)
     except (CorruptData, UnsupportedVersion, InvalidArgument, FileNotFoundError,
             IsADirectoryError) as exc:
         print(f"hqmq-b200: error: {exc}", file=sys.stderr)

@@ -111,3 +111,21 @@ def test_oracle_adversarial_matches_reference(oracle, name):
     for f in ("scales", "indices", "quanta"):
         assert np.array_equal(getattr(enc, f), g[f]), f
     assert hashlib.sha256(oracle.to_bytes(enc)).hexdigest() == meta["digest"]
+
+
+def test_oracle_covering_matches_reference(oracle):
+    """The oracle's covering estimate (packing.py:59-83) reproduces the
+    reference's golden values bit for bit (small cases; the GPU test runs all)."""
+    import json
+
+    cases = json.load(open(os.path.join(GOLDEN, "covering.json")))
+    for c in cases:
+        if c["S"] > 16:
+            continue
+        if c["S"] == 0:
+            cw = oracle.hamilton(oracle.primary_2t()[:, None, :],
+                                 np.array([[[1.0, 0.0, 0.0, 0.0]]])).reshape(-1, 4)
+        else:
+            cw = oracle.joint(c["seed"], c["layer"], c["head"], c["role"], c["S"])
+        rho, mean = oracle.estimate_covering(cw, c["n_probes"], c["probe_seed"])
+        assert rho == float.fromhex(c["rho_hat"]) and mean == float.fromhex(c["mean_angle"])
