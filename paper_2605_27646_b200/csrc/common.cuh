@@ -6,6 +6,8 @@
 // __ddiv_rn / __dsqrt_rn) so nvcc can never contract it into an FMA.
 #pragma once
 
+#include <utility>
+
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -167,6 +169,31 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
       "@P1 bra DONE;\n\tbra LAB_WAIT;\n\tDONE:\n\t}" ::"r"(smem_u32(bar)),
       "r"(phase), "r"(0x989680u)
       : "memory");
+}
+
+// Programmatic dependent launch (PDL): a kernel launched with launch_pdl may
+// start while the previous kernel of its stream drains; it sets itself up
+// (barriers, constant tables) and then calls pdl_wait() before it touches
+// anything an earlier kernel produced.  pdl_trigger() lets the next
+// PDL-launched kernel of the stream start its own set-up early.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t st, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
 // Records the CUDA error text for hqmq_last_error() and returns HQMQ_ERR_CUDA.

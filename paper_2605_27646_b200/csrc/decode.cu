@@ -360,6 +360,13 @@ __global__ void __launch_bounds__(256, 7) decode_fast_kernel(DecParams p) {
       mbar_arrive_expect_tx(&tab_bar, tb);
       bulk_g2s(tab, p.table16 + (int64_t)h * ncw, tb, &tab_bar);
     }
+  }
+  // the table load above reads constant codebook data; the code streams come
+  // from an earlier kernel (the encode): wait for it (PDL), then let the next
+  // kernel of the stream begin its own set-up
+  pdl_wait();
+  pdl_trigger();
+  if (tid == 0) {
     int s = 0;
     for (int64_t tile = blockIdx.x; tile < ntile && s < kFDStages; tile += gridDim.x, ++s)
       issue(tile, s);
@@ -935,8 +942,8 @@ int launch_decode(DecParams& p, const hqmq_decode_args* a, cudaStream_t st) {
     }
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     const int64_t bx = one_wave_ctas_per_row(kern, fsmem, rows, ceil_div(p.nt, kFDTok));
-    kern<<<dim3((unsigned)bx, (unsigned)rows), 256, fsmem, st>>>(p);
-    return check();
+    const cudaError_t e = launch_pdl(kern, dim3((unsigned)bx, (unsigned)rows), dim3(256), fsmem, st, p);
+    return e == cudaSuccess ? check() : record_cuda_error(e);
   }
   const int64_t nck = p.nt * p.C;
   const int64_t want = std::max<int64_t>(1, (148 * 4 + rows - 1) / rows);

@@ -537,6 +537,9 @@ __global__ void __launch_bounds__(kWThreads, kMinB) encode_warp_kernel(EncParams
   for (int i = lane; i < kWT * 32 + 2; i += 32) stage_i[warp][i] = 0u;
   for (int i = lane; i < kWT * 8 + 2; i += 32) stage_r[warp][i] = 0u;
   __syncthreads();
+  // (PDL) inputs, thresholds and offsets come from earlier kernels
+  pdl_wait();
+  pdl_trigger();
 
   const double top = (double)((1 << br) - 1);
   const double thr = p.groups ? p.groups[p.per_head ? h : 0].threshold : INFINITY;
@@ -939,6 +942,10 @@ __global__ void __launch_bounds__(kTcThreads, kMinB) encode_tc_kernel(EncParams 
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  // (PDL) the set-up above overlaps the previous kernel's tail; the inputs and
+  // the prep pass's flags / offsets are read only after it completes
+  pdl_wait();
+  pdl_trigger();
   const uint32_t tmem = tmem_slot + (uint32_t)(grp * kN) + ((uint32_t)(wl * 32) << 16);
   const uint32_t tmem_grp = tmem_slot + (uint32_t)(grp * kN);
   unsigned char* at = asm_base + grp * 4096;
@@ -1601,7 +1608,7 @@ int launch_encode(const hqmq_encode_args* a, const Layout& L, cudaStream_t st) {
         const int64_t ntiles = ceil_div(a->tokens, wt);
         const int64_t want = ceil_div((int64_t)148 * minb, L.rows);
         const int64_t bx = std::max<int64_t>(1, std::min<int64_t>(want, ceil_div(ntiles, kWWarps)));
-        kern<<<dim3((unsigned)bx, (unsigned)L.rows), kWThreads, smem, st>>>(p);
+        launch_pdl(kern, dim3((unsigned)bx, (unsigned)L.rows), dim3(kWThreads), smem, st, p);
       };
       switch (a->search_path) {
         case HQMQ_SEARCH_CUDA_CORE:  // prep pass, then the FFMA2 search pass
@@ -1631,7 +1638,7 @@ int launch_encode(const hqmq_encode_args* a, const Layout& L, cudaStream_t st) {
             const int64_t ntiles = ceil_div(a->tokens, 4);
             const int64_t want = std::max<int64_t>(1, ceil_div((int64_t)148 * 2, L.rows));
             const int64_t bx = std::max<int64_t>(1, std::min<int64_t>(want, ceil_div(ntiles, 2)));
-            kern<<<dim3((unsigned)bx, (unsigned)L.rows), kTcThreads, tsmem, st>>>(p);
+            launch_pdl(kern, dim3((unsigned)bx, (unsigned)L.rows), dim3(kTcThreads), tsmem, st, p);
           };
           // (64-secondary blocks at 1 CTA/SM measured 2x slower: occupancy wins)
           if (tc32) tc(encode_tc_kernel<InT, kTcBlk, 2>);
