@@ -336,7 +336,7 @@ class QuantizedTensor:
                               else payloads).to(device=device, dtype=torch.float16).reshape(-1, 4)
         if pay.shape[0] != n_flag:
             raise CorruptData("payload count does not match the flags")
-        pay_buf = torch.zeros((max(1, n_flag), 4), dtype=torch.float16, device=device)
+        pay_buf = torch.zeros((n_flag + 2, 4), dtype=torch.float16, device=device)
         pay_buf[:n_flag] = pay
         meta = torch.tensor([n - n_flag, n_flag, 0, 0], dtype=torch.int64, device=device)
         return cls(s, c, layer, role, head_base, sc, iw, rw, fw, pay_buf, tok, meta, device,

@@ -554,8 +554,11 @@ constexpr int kFlTok = 64;
 constexpr int kFlStages = 4;
 
 struct FlagGeom {
-  uint32_t idx_off, rad_off, fl_off, to_off, sc_off, stage_bytes;
+  uint32_t idx_off, rad_off, fl_off, to_off, sc_off, pay_off, stage_bytes;
 };
+// payload rows a stage can hold (the tile's outlier rows are one contiguous
+// range of the payload section; a tile with more falls back to global loads)
+constexpr int kFlPayRows = 256;
 __host__ __device__ inline FlagGeom fl_geom(int w, int br) {
   auto up = [](uint32_t x) { return (x + 127u) / 128u * 128u; };
   FlagGeom g;
@@ -565,21 +568,32 @@ __host__ __device__ inline FlagGeom fl_geom(int w, int br) {
   g.fl_off = o; o += up(kFlTok * 4);
   g.to_off = o; o += up(kFlTok * 4);
   g.sc_off = o; o += up(kFlTok * 2);
+  g.pay_off = o; o += up((kFlPayRows + 2) * 8);
   g.stage_bytes = o;
   return g;
 }
 
-template <typename OutT>
-__global__ void __launch_bounds__(256) decode_flag_tma_kernel(DecParams p) {
+// Med3x layout (head_dim 128): TMA ring of 64-token tiles holding the tile's
+// compact index / radius words, flag words, coded offsets, scales and its
+// outlier payload rows.  Two tokens per warp instruction (half-warp = token,
+// lane = 2 chunks, 16-byte stores for fp16); a flagged chunk reads its fp16
+// payload row from the stage.
+template <typename OutT, int W = 0, int BR = 0>
+__global__ void __launch_bounds__(256, 6) decode_flag_tma_kernel(DecParams p) {
   extern __shared__ __align__(128) unsigned char dsm[];
   __shared__ __align__(8) uint64_t full[kFlStages];
   __shared__ __align__(8) uint64_t tab_bar;
   __shared__ unsigned int released[kFlStages];
-  __shared__ uint32_t base_w[kFlStages][2];  // first index / radius word of the stage
+  // per stage: bit of the tile's first code in the staged index / radius
+  // words, first staged payload row (64-bit), staged payload row count
+  // (0 = the tile's rows are not staged: global loads)
+  __shared__ uint32_t base_w[kFlStages][2];
+  __shared__ unsigned long long pay_base[kFlStages];
+  __shared__ uint32_t pay_n[kFlStages];
   const int64_t row = blockIdx.y;
   const int h = (int)(row % p.H);
   const int ncw = kGroupOrder * p.S;
-  const int w = p.w, br = p.br;
+  const int w = W ? W : p.w, br = BR ? BR : p.br;  // compile-time for the model configs
   const FlagGeom g = fl_geom(w, br);
   constexpr bool k16 = sizeof(OutT) == 2;
   float4* tab = reinterpret_cast<float4*>(dsm);
@@ -595,23 +609,33 @@ __global__ void __launch_bounds__(256) decode_flag_tma_kernel(DecParams p) {
     const int ntok = (int)min((int64_t)kFlTok, p.nt - tile * kFlTok);
     unsigned char* s = ring + (size_t)stage * g.stage_bytes;
     const uint64_t c0 = __ldg(p.tokoff + t);
-    const uint64_t c1 = (uint64_t)__ldg(p.tokoff + t + ntok - 1) +
-                        (uint64_t)__popc(~__ldg(p.flagw + t + ntok - 1));
+    const uint64_t cl = __ldg(p.tokoff + t + ntok - 1);
+    const uint32_t fl_last = __ldg(p.flagw + t + ntok - 1);
+    const uint64_t c1 = cl + (uint64_t)__popc(~fl_last);
     const uint64_t iw0 = ((c0 * (uint64_t)w) >> 5) & ~3ull;
     const uint64_t iw1 = (((c1 * (uint64_t)w + 31) >> 5) + 3) & ~3ull;
     const uint64_t rw0 = ((c0 * (uint64_t)br) >> 5) & ~3ull;
     const uint64_t rw1 = (((c1 * (uint64_t)br + 31) >> 5) + 3) & ~3ull;
-    base_w[stage][0] = (uint32_t)iw0;  // low 32 bits suffice for relative offsets
-    base_w[stage][1] = (uint32_t)rw0;
+    base_w[stage][0] = (uint32_t)(c0 * (uint64_t)w - iw0 * 32u);   // c0's bit in the staged words
+    base_w[stage][1] = (uint32_t)(c0 * (uint64_t)br - rw0 * 32u);
+    // payload rows of the tile: [t*32 - c0, (t+ntok-1)*32 - cl + flagged(last))
+    const uint64_t p0 = (uint64_t)t * 32u - c0;
+    const uint64_t p1 = (uint64_t)(t + ntok - 1) * 32u - cl + (uint64_t)__popc(fl_last);
+    const uint64_t pa0 = p0 & ~1ull, pa1 = (p1 + 1) & ~1ull;  // 16-byte aligned range
+    const bool stage_pay = p1 > p0 && pa1 - pa0 <= (uint64_t)kFlPayRows + 2;
+    pay_base[stage] = pa0;
+    pay_n[stage] = stage_pay ? (uint32_t)(pa1 - pa0) : 0u;
+    const uint32_t pb = stage_pay ? (uint32_t)(pa1 - pa0) * 8u : 0u;
     const uint32_t ib = (uint32_t)(iw1 - iw0) * 4, rb = (uint32_t)(rw1 - rw0) * 4;
     const uint32_t fb = ntok * 4, sb = ntok * 2;
     fence_proxy_async();
-    mbar_arrive_expect_tx(&full[stage], ib + rb + 2 * fb + sb);
+    mbar_arrive_expect_tx(&full[stage], ib + rb + 2 * fb + sb + pb);
     if (ib) bulk_g2s(s + g.idx_off, p.idxw + iw0, ib, &full[stage]);
     if (rb) bulk_g2s(s + g.rad_off, p.radw + rw0, rb, &full[stage]);
     bulk_g2s(s + g.fl_off, p.flagw + t, fb, &full[stage]);
     bulk_g2s(s + g.to_off, p.tokoff + t, fb, &full[stage]);
     bulk_g2s(s + g.sc_off, p.scales + t, sb, &full[stage]);
+    if (pb) bulk_g2s(s + g.pay_off, p.payloads + pa0 * 4, pb, &full[stage]);
   };
 
   if (tid == 0) {
@@ -624,13 +648,15 @@ __global__ void __launch_bounds__(256) decode_flag_tma_kernel(DecParams p) {
   }
   __syncthreads();
   const float4* __restrict__ gtab = reinterpret_cast<const float4*>(p.table) + (int64_t)h * ncw;
+  if (tid == 0 && tab_tma) {
+    const uint32_t tb = (uint32_t)ncw * 8u;
+    fence_proxy_async();
+    mbar_arrive_expect_tx(&tab_bar, tb);
+    bulk_g2s(tab, p.table16 + (int64_t)h * ncw, tb, &tab_bar);
+  }
+  pdl_wait();  // the sections come from the encode (PDL)
+  pdl_trigger();
   if (tid == 0) {
-    if (tab_tma) {
-      const uint32_t tb = (uint32_t)ncw * 8u;
-      fence_proxy_async();
-      mbar_arrive_expect_tx(&tab_bar, tb);
-      bulk_g2s(tab, p.table16 + (int64_t)h * ncw, tb, &tab_bar);
-    }
     int st = 0;
     for (int64_t tile = blockIdx.x; tile < ntile && st < kFlStages; tile += gridDim.x, ++st)
       issue(tile, st);
@@ -652,7 +678,11 @@ __global__ void __launch_bounds__(256) decode_flag_tma_kernel(DecParams p) {
   const uint32_t imask = w == 32 ? 0xffffffffu : ((1u << w) - 1u);
   const uint32_t rmask = (1u << br) - 1u;
   const float rtop = 1.0f / (float)((1 << br) - 1);
-  const uint32_t lt = (1u << lane) - 1u;
+  // lane = (token q of a 4-token group, chunk quad 4*ql .. 4*ql+3): per-token
+  // work (flag word, coded offset, scale, run position) is shared by 4 chunks,
+  // and the quad's codes are one run read as a 64-bit window
+  const int tq = lane >> 3, ql = lane & 7;
+  const uint32_t below = (1u << (4 * ql)) - 1u;  // chunks before the quad
   OutT* __restrict__ out = reinterpret_cast<OutT*>(p.out);
   bool bad = false;
   int k = 0;
@@ -665,46 +695,109 @@ __global__ void __launch_bounds__(256) decode_flag_tma_kernel(DecParams p) {
     const uint32_t* fls = reinterpret_cast<const uint32_t*>(s + g.fl_off);
     const uint32_t* tos = reinterpret_cast<const uint32_t*>(s + g.to_off);
     const uint16_t* scs = reinterpret_cast<const uint16_t*>(s + g.sc_off);
-    const uint32_t bi0 = base_w[stage][0], br0 = base_w[stage][1];
+    const uint2* pays = reinterpret_cast<const uint2*>(s + g.pay_off);
+    // 32-bit arithmetic relative to the tile: coded positions (token offsets
+    // are u32), bit offsets from the tile's first code, payload rows mod 2^32
+    const uint32_t c0 = tos[0];
+    const uint32_t d0i = base_w[stage][0], d0r = base_w[stage][1];  // c0's bit in the staged words
+    const uint64_t pbase = pay_base[stage];
+    const uint32_t pbase32 = (uint32_t)pbase;
+    const uint32_t pn = pay_n[stage];
     const int ntok = (int)min((int64_t)kFlTok, p.nt - tile * kFlTok);
-    for (int tt = warp; tt < ntok; tt += 8) {
-      const int64_t tok = tok_base + tile * kFlTok + tt;
-      const uint32_t fw = fls[tt];
-      const bool fl = (fw >> lane) & 1u;
-      const uint64_t pos = (uint64_t)tos[tt] + __popc(~fw & lt);
-      float v[4];
-      if (!fl) {
-        const uint32_t ib = (uint32_t)(pos * (uint64_t)w - (uint64_t)bi0 * 32u);
-        uint32_t idx = __funnelshift_r(iw[ib >> 5], iw[(ib >> 5) + 1], ib & 31) & imask;
-        const uint32_t rbit = (uint32_t)(pos * (uint64_t)br - (uint64_t)br0 * 32u);
-        const uint32_t q = __funnelshift_r(rw[rbit >> 5], rw[(rbit >> 5) + 1], rbit & 31) & rmask;
-        bad |= idx >= (uint32_t)ncw;
-        idx = idx < (uint32_t)ncw ? idx : 0u;
-        const float rad = (float)q * (__half2float(__ushort_as_half(scs[tt])) * rtop);
-        if constexpr (k16) {
-          const uint2 cw = reinterpret_cast<const uint2*>(tab)[idx];
-          const float2 c01 = __half22float2(*reinterpret_cast<const __half2*>(&cw.x));
-          const float2 c23 = __half22float2(*reinterpret_cast<const __half2*>(&cw.y));
-          v[0] = rad * c01.x; v[1] = rad * c01.y; v[2] = rad * c23.x; v[3] = rad * c23.y;
-        } else {
-          const float4 cw = tab[idx];
-          v[0] = rad * cw.x; v[1] = rad * cw.y; v[2] = rad * cw.z; v[3] = rad * cw.w;
+    const uint32_t tok32 = (uint32_t)(tok_base + tile * kFlTok);  // mod 2^32
+    OutT* __restrict__ otile = out + (row * p.nt + tile * kFlTok) * 128 + 16 * ql;
+#pragma unroll 2
+    for (int t4 = 4 * warp; t4 < kFlTok; t4 += 32) {
+      const int tt = t4 + tq;
+      if (tt < ntok) {
+        const uint32_t fw = fls[tt];
+        const uint32_t f4 = (fw >> (4 * ql)) & 15u;
+        const uint32_t tofs = tos[tt];
+        const uint32_t rel0 = tofs - c0 + __popc(~fw & below);  // first coded position of the quad - c0
+        const float sg = __half2float(__ushort_as_half(scs[tt])) * rtop;
+        const uint32_t ib = rel0 * (uint32_t)w + d0i;
+        const uint32_t* ip = iw + (ib >> 5);
+        const uint32_t ilo = __funnelshift_r(ip[0], ip[1], ib & 31);
+        const uint32_t ihi = __funnelshift_r(ip[1], ip[2], ib & 31);
+        const uint64_t iwin = ((uint64_t)ihi << 32) | ilo;  // >= 4 codes of <= 16 bits
+        const uint32_t qb = rel0 * (uint32_t)br + d0r;
+        const uint32_t qwin = __funnelshift_r(rw[qb >> 5], rw[(qb >> 5) + 1], qb & 31);  // 4 codes <= 8 bits
+        float rad[4];
+        uint32_t idx[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const uint32_t j = (uint32_t)c - __popc(f4 & ((1u << c) - 1u));  // code slot after skips
+          uint32_t ix = (uint32_t)(iwin >> (j * (uint32_t)w)) & imask;
+          bad |= ix >= (uint32_t)ncw;
+          idx[c] = ix < (uint32_t)ncw ? ix : 0u;
+          rad[c] = (float)((qwin >> (j * (uint32_t)br)) & rmask) * sg;
         }
-      } else {
-        const uint64_t prow = (uint64_t)tok * 32 + lane - pos;
-        const ushort4 hv = __ldg(reinterpret_cast<const ushort4*>(p.payloads) + prow);
-        v[0] = __half2float(__ushort_as_half(hv.x));
-        v[1] = __half2float(__ushort_as_half(hv.y));
-        v[2] = __half2float(__ushort_as_half(hv.z));
-        v[3] = __half2float(__ushort_as_half(hv.w));
-      }
-      OutT* o = out + (row * p.nt + tile * kFlTok + tt) * 128 + 4 * lane;
-      if constexpr (sizeof(OutT) == 4) {
-        *reinterpret_cast<float4*>(o) = make_float4(v[0], v[1], v[2], v[3]);
-      } else {
-        OutT t4[4] = {Out<OutT>::cvt(v[0]), Out<OutT>::cvt(v[1]), Out<OutT>::cvt(v[2]),
-                      Out<OutT>::cvt(v[3])};
-        *reinterpret_cast<uint2*>(o) = *reinterpret_cast<const uint2*>(t4);
+        OutT* o = otile + tt * 128;
+        if constexpr (std::is_same<OutT, __half>::value) {
+          uint2 ov[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const uint2 cw = reinterpret_cast<const uint2*>(tab)[idx[c]];
+            const __half2 rr = __float2half2_rn(rad[c]);
+            const __half2 x01 = __hmul2(rr, *reinterpret_cast<const __half2*>(&cw.x));
+            const __half2 x23 = __hmul2(rr, *reinterpret_cast<const __half2*>(&cw.y));
+            ov[c] = make_uint2(*reinterpret_cast<const uint32_t*>(&x01), *reinterpret_cast<const uint32_t*>(&x23));
+          }
+          if (f4) {  // outlier chunks: their fp16 payload rows verbatim
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              if ((f4 >> c) & 1u) {
+                const uint32_t rel = (tok32 + (uint32_t)tt) * 32u - tofs +
+                                     __popc(fw & ((1u << (4 * ql + c)) - 1u)) - pbase32;
+                ov[c] = rel < pn ? pays[rel]
+                                 : __ldg(reinterpret_cast<const uint2*>(p.payloads) + (pbase + rel));
+              }
+            }
+          }
+          reinterpret_cast<uint4*>(o)[0] = make_uint4(ov[0].x, ov[0].y, ov[1].x, ov[1].y);
+          reinterpret_cast<uint4*>(o)[1] = make_uint4(ov[2].x, ov[2].y, ov[3].x, ov[3].y);
+        } else {
+          float v[16];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            float4 cw;
+            if constexpr (k16) {
+              const uint2 h = reinterpret_cast<const uint2*>(tab)[idx[c]];
+              const float2 c01 = __half22float2(*reinterpret_cast<const __half2*>(&h.x));
+              const float2 c23 = __half22float2(*reinterpret_cast<const __half2*>(&h.y));
+              cw = make_float4(c01.x, c01.y, c23.x, c23.y);
+            } else {
+              cw = tab[idx[c]];
+            }
+            v[4 * c] = rad[c] * cw.x; v[4 * c + 1] = rad[c] * cw.y;
+            v[4 * c + 2] = rad[c] * cw.z; v[4 * c + 3] = rad[c] * cw.w;
+          }
+          if (f4) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              if ((f4 >> c) & 1u) {
+                const uint32_t rel = (tok32 + (uint32_t)tt) * 32u - tofs +
+                                     __popc(fw & ((1u << (4 * ql + c)) - 1u)) - pbase32;
+                const uint2 hv = rel < pn ? pays[rel]
+                                          : __ldg(reinterpret_cast<const uint2*>(p.payloads) + (pbase + rel));
+                const float2 a01 = __half22float2(*reinterpret_cast<const __half2*>(&hv.x));
+                const float2 a23 = __half22float2(*reinterpret_cast<const __half2*>(&hv.y));
+                v[4 * c] = a01.x; v[4 * c + 1] = a01.y; v[4 * c + 2] = a23.x; v[4 * c + 3] = a23.y;
+              }
+            }
+          }
+          if constexpr (sizeof(OutT) == 4) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              reinterpret_cast<float4*>(o)[c] = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+          } else {
+            OutT t16[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) t16[i] = Out<OutT>::cvt(v[i]);
+            reinterpret_cast<uint4*>(o)[0] = reinterpret_cast<const uint4*>(t16)[0];
+            reinterpret_cast<uint4*>(o)[1] = reinterpret_cast<const uint4*>(t16)[1];
+          }
+        }
       }
     }
     __syncwarp();
@@ -903,17 +996,25 @@ int launch_decode(DecParams& p, const hqmq_decode_args* a, cudaStream_t st) {
   p.table = a->joint_f32;
   p.aligned4 = (p.D % 4 == 0) && (reinterpret_cast<uintptr_t>(a->out) % (4 * sizeof(OutT)) == 0);
   auto al16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
-  if (p.D == 128 && p.flagw && p.tokoff && p.payloads && use_smem && p.aligned4 &&
+  if (p.D == 128 && p.flagw && p.tokoff && p.payloads && use_smem && p.aligned4 && p.w <= 16 &&
       p.T % 8 == 0 && p.t0 % 8 == 0 && p.nt % 8 == 0 && al16(p.idxw) && al16(p.radw) &&
       al16(p.scales) && al16(p.flagw) && al16(p.tokoff)) {
     const FlagGeom g = fl_geom(p.w, p.br);
     const size_t fsmem = fd_table_bytes<OutT>(kGroupOrder * p.S) + (size_t)kFlStages * g.stage_bytes;
     cudaFuncSetAttribute(decode_flag_tma_kernel<OutT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          200 * 1024);
-    const int64_t bx =
-        one_wave_ctas_per_row(decode_flag_tma_kernel<OutT>, fsmem, rows, ceil_div(p.nt, kFlTok));
-    decode_flag_tma_kernel<OutT><<<dim3((unsigned)bx, (unsigned)rows), 256, fsmem, st>>>(p);
-    return check();
+    void (*kern)(DecParams) = decode_flag_tma_kernel<OutT>;
+    switch (p.w * 16 + p.br) {
+      case 9 * 16 + 4: kern = decode_flag_tma_kernel<OutT, 9, 4>; break;    // C1: S = 16
+      case 11 * 16 + 4: kern = decode_flag_tma_kernel<OutT, 11, 4>; break;  // S = 64
+      case 11 * 16 + 6: kern = decode_flag_tma_kernel<OutT, 11, 6>; break;  // C3: S = 64, b_r 6
+      case 13 * 16 + 4: kern = decode_flag_tma_kernel<OutT, 13, 4>; break;  // S = 256
+      default: break;
+    }
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    const int64_t bx = one_wave_ctas_per_row(kern, fsmem, rows, ceil_div(p.nt, kFlTok));
+    const cudaError_t e = launch_pdl(kern, dim3((unsigned)bx, (unsigned)rows), dim3(256), fsmem, st, p);
+    return e == cudaSuccess ? check() : record_cuda_error(e);
   }
   if (p.D == 128 && p.flagw && p.tokoff && p.payloads && use_smem && p.aligned4) {
     const int64_t nwt = ceil_div(p.nt, 32);  // 8 warps x 4 tokens per CTA step

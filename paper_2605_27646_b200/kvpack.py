@@ -227,8 +227,9 @@ def from_bytes(blob: bytes, device="cuda") -> QuantizedTensor:
     pay_raw = section(4)
     if len(pay_raw) != 8 * n_flag:
         raise CorruptData("payload section has the wrong length")
-    pay = dsection(4, 8 * max(1, n_flag))[: 8 * max(1, n_flag)].view(torch.float16).reshape(
-        max(1, n_flag), CHUNK_DIM)
+    # two spare rows: the Med3x decode stages payload rows in 16-byte units
+    pay = dsection(4, 8 * (n_flag + 2))[: 8 * (n_flag + 2)].view(torch.float16).reshape(
+        n_flag + 2, CHUNK_DIM)
     L = nat.lib()
     tok = None
     if outlier:
