@@ -1127,6 +1127,8 @@ __global__ void __launch_bounds__(kTcThreads, kMinB) encode_tc_kernel(EncParams 
 __global__ void token_coded_norms_kernel(const double* __restrict__ norms,
                                          const RadixGroup* groups, int64_t H, int64_t T,
                                          int64_t n_tok, int per_head, uint32_t* cnt) {
+  pdl_wait();
+  pdl_trigger();
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n_tok;
        t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t row = t / T;
@@ -1221,6 +1223,8 @@ __global__ void __launch_bounds__(kHistThreads) radix_hist_kernel(RadixParams p)
   __shared__ bool is_last;
   for (int i = threadIdx.x; i < kBins; i += kHistThreads) hs[i] = 0u;
   __syncthreads();
+  pdl_wait();  // (PDL) the previous pass's prefix / the input
+  pdl_trigger();
   const int lo = digit_lo(p.pass), width = digit_width(p.pass);
   const uint32_t dmask = (1u << width) - 1u;
   const int hi_shift = lo + width;
@@ -1325,6 +1329,8 @@ constexpr int kTailThreads = 1024;
 __global__ void __launch_bounds__(kTailThreads) radix_tail_kernel(RadixParams p) {
   __shared__ uint32_t hs[kBins];
   __shared__ unsigned long long s_pref, s_rank;
+  pdl_wait();
+  pdl_trigger();
   const int g = blockIdx.x;
   const unsigned int n = p.cand_n[g];
   const double* __restrict__ cg = p.cand + (unsigned long long)g * p.n_per_group;
@@ -1375,10 +1381,14 @@ __global__ void __launch_bounds__(kTailThreads) radix_tail_kernel(RadixParams p)
 
 // Frozen thresholds (incremental Med3x caches): groups[g].threshold = fixed[g].
 __global__ void set_thresholds_kernel(RadixGroup* groups, const double* fixed, int G) {
+  pdl_wait();
+  pdl_trigger();
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g < G) groups[g].threshold = fixed[g];
 }
 __global__ void copy_thresholds_kernel(const RadixGroup* groups, double* out, int G) {
+  pdl_wait();
+  pdl_trigger();
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
   if (g < G) out[g] = groups[g].threshold;
 }
@@ -1416,6 +1426,8 @@ __global__ void tile_count_kernel(const double* __restrict__ norms, const RadixG
 
 __global__ void finalize_counts_kernel(const uint32_t* counts, const uint32_t* prefix,
                                        int64_t n_tiles, int64_t n_chunks, int64_t* counters) {
+  pdl_wait();
+  pdl_trigger();
   if (threadIdx.x == 0 && blockIdx.x == 0) {
     const int64_t coded = n_tiles ? (int64_t)prefix[n_tiles - 1] + counts[n_tiles - 1] : 0;
     counters[0] = coded;
