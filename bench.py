@@ -113,6 +113,12 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            # the fork / first query happen BEFORE the caller starts its timer:
+            # wait (<= 3 s) for the first sample, then drop it (idle clocks)
+            t_end = time.time() + 3.0
+            while not self.lines and time.time() < t_end:
+                time.sleep(0.01)
+            self.lines.clear()
         except OSError:
             self.proc = None
         return self
@@ -359,6 +365,10 @@ def run_ours(args, wl, world, rank, local):
     torch.cuda.synchronize()
     launches["n"] = 0
     cur = torch.cuda.current_stream(dev)
+    import gc
+
+    gc.collect()
+    gc.disable()  # no collector pause inside the timed region
     with ClockSampler(local) as clk:
         if flush_l2 or graph is not None:
             # per-step event pairs on the launching stream, flush in between
@@ -400,6 +410,7 @@ def run_ours(args, wl, world, rank, local):
             stop.record(cur)
             torch.cuda.synchronize()
             elapsed_ms = start.elapsed_time(stop)
+    gc.enable()
     rank_stats = None
     if world > 1:
         t = torch.tensor([elapsed_ms, enc_ms, dec_ms], device=dev)

@@ -446,8 +446,11 @@ constexpr int kMConsumers = 8;
 constexpr int kMThreads = kMConsumers * 32;
 
 struct RingGeom {
-  uint32_t ki, kr, ks, vi, vr, vs, kf, ka, vf, va, bytes;
+  uint32_t ki, kr, ks, vi, vr, vs, kf, ka, vf, va, kp, vp, bytes;
 };
+// outlier payload rows a Med3x stage holds per tensor (the tile's rows are one
+// contiguous range of the payload section; beyond this, global loads)
+constexpr int kPayRows = 256;
 
 // One ring stage: K and V index / radius words and fp16 scales of a 128-key
 // tile; with Med3x (kFlags) also each key's flag word and its aux word (the
@@ -467,12 +470,14 @@ __host__ __device__ inline RingGeom ring_geom(int w, int br, bool flags = false)
   g.vi = o; o += up(kMT * w * 4 + slack);
   g.vr = o; o += up(kMT * br * 4 + slack);
   g.vs = o; o += up(kMT * 2);
-  g.kf = g.ka = g.vf = g.va = 0;
+  g.kf = g.ka = g.vf = g.va = g.kp = g.vp = 0;
   if (flags) {
     g.kf = o; o += kMT * 4;
     g.ka = o; o += kMT * 4;
     g.vf = o; o += kMT * 4;
     g.va = o; o += kMT * 4;
+    g.kp = o; o += (kPayRows + 2) * 8;
+    g.vp = o; o += (kPayRows + 2) * 8;
   }
   g.bytes = o;
   return g;
@@ -506,6 +511,10 @@ __global__ void __launch_bounds__(kMThreads, 2) attention_mma_kernel(AttParams p
   __shared__ __align__(8) uint64_t full[kMStages];
   __shared__ __align__(8) uint64_t tab_bar;
   __shared__ unsigned int released[kMStages];
+  // Med3x, contiguous layout: first staged payload row and staged row count
+  // per stage and tensor (count 0: global loads)
+  __shared__ unsigned long long pay_base[kFlags ? kMStages : 1][2];
+  __shared__ uint32_t pay_n[kFlags ? kMStages : 1][2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int ncw = kGroupOrder * p.S;
   constexpr int w = W, br = BR;
@@ -562,21 +571,33 @@ __global__ void __launch_bounds__(kMThreads, 2) attention_mma_kernel(AttParams p
     if constexpr (kFlags && !kPaged) {
       // compact streams: the tile's codes are [c0, c1) of the coded order
       const uint32_t fb = ntok * 4;  // ntok % 8 == 0 (T_kv % 8 == 0): 16-byte multiple
-      uint32_t ib[2], rbb[2];
-      uint64_t iw0[2], rw0[2];
+      uint32_t ib[2], rbb[2], pb[2];
+      uint64_t iw0[2], rw0[2], pa0[2];
       const AttView* vw[2] = {&p.k, &p.v};
 #pragma unroll
       for (int r = 0; r < 2; ++r) {
         const uint64_t c0 = __ldg(vw[r]->tokoff + t);
-        const uint64_t c1 = (uint64_t)__ldg(vw[r]->tokoff + t + ntok - 1) + 32u -
-                            (uint64_t)__popc(__ldg(vw[r]->flagw + t + ntok - 1));
+        const uint64_t cl = __ldg(vw[r]->tokoff + t + ntok - 1);
+        const uint32_t fl_last = __ldg(vw[r]->flagw + t + ntok - 1);
+        const uint64_t c1 = cl + 32u - (uint64_t)__popc(fl_last);
         iw0[r] = range_lo(c0, w);
         rw0[r] = range_lo(c0, br);
         ib[r] = (uint32_t)((((c1 * w + 31) >> 5) - iw0[r] + 3) & ~3ull) * 4u;
         rbb[r] = (uint32_t)((((c1 * br + 31) >> 5) - rw0[r] + 3) & ~3ull) * 4u;
+        // the tile's payload rows [t*32 - c0, (t+ntok-1)*32 - cl + flagged(last))
+        const uint64_t p0 = (uint64_t)t * 32u - c0;
+        const uint64_t p1 = (uint64_t)(t + ntok - 1) * 32u - cl + (uint64_t)__popc(fl_last);
+        pa0[r] = p0 & ~1ull;
+        const uint64_t pa1 = (p1 + 1) & ~1ull;
+        const bool st = p1 > p0 && pa1 - pa0[r] <= (uint64_t)kPayRows + 2;
+        pb[r] = st ? (uint32_t)(pa1 - pa0[r]) * 8u : 0u;
+        pay_base[stage][r] = pa0[r];
+        pay_n[stage][r] = st ? (uint32_t)(pa1 - pa0[r]) : 0u;
       }
       fence_proxy_async();
-      mbar_arrive_expect_tx(&full[stage], ib[0] + rbb[0] + ib[1] + rbb[1] + 2 * (sb + 2 * fb));
+      mbar_arrive_expect_tx(&full[stage], ib[0] + rbb[0] + ib[1] + rbb[1] + 2 * (sb + 2 * fb) + pb[0] + pb[1]);
+      if (pb[0]) bulk_g2s(s + gm.kp, p.k.payloads + pa0[0] * 4, pb[0], &full[stage]);
+      if (pb[1]) bulk_g2s(s + gm.vp, p.v.payloads + pa0[1] * 4, pb[1], &full[stage]);
       bulk_g2s(s + gm.ki, p.k.idxw + iw0[0], ib[0], &full[stage]);
       bulk_g2s(s + gm.kr, p.k.radw + rw0[0], rbb[0], &full[stage]);
       bulk_g2s(s + gm.ks, p.k.scales + t, sb, &full[stage]);
@@ -608,8 +629,9 @@ __global__ void __launch_bounds__(kMThreads, 2) attention_mma_kernel(AttParams p
   };
   // release a stage; the last of the 8 warps refills it with tile k + NS
   auto release = [&](int64_t k, int stage) {
+    __syncwarp();  // every lane's reads of the stage precede lane 0's release
     if (lane == 0) {
-      if (atomicAdd(&released[stage], 1u) == kMConsumers - 1) {
+      if (stage_release(&released[stage]) == kMConsumers - 1) {
         released[stage] = 0u;
         if (k + NS < ntile) issue(k + NS, stage);
       }
@@ -737,6 +759,15 @@ __global__ void __launch_bounds__(kMThreads, 2) attention_mma_kernel(AttParams p
       if constexpr (kPaged) return (uint64_t)ax[key] + below;
       return (uint64_t)(gtok0 + key) * 32u - (uint64_t)ax[key] + below;
     };
+    // a payload row of tensor r (0 = K, 1 = V): from the stage when staged
+    auto payload = [&](int r, uint64_t prow) -> ushort4 {
+      if constexpr (!kPaged) {
+        const uint64_t rel = prow - pay_base[stage][r];
+        if (rel < pay_n[stage][r])
+          return reinterpret_cast<const ushort4*>(s + (r ? gm.vp : gm.kp))[rel];
+      }
+      return __ldg(reinterpret_cast<const ushort4*>(r ? p.v.payloads : p.k.payloads) + prow);
+    };
     if (t0 < kend) {
       // ---- S = Q K^T: lane decodes chunks 8*t4 .. 8*t4+7 of key kw0 + 8*nt + g4
       float sc[2][4];
@@ -827,8 +858,7 @@ __global__ void __launch_bounds__(kMThreads, 2) attention_mma_kernel(AttParams p
           while (rem) {
             const int c = __ffs(rem) - 1;
             rem &= rem - 1u;
-            const ushort4 hv =
-                __ldg(reinterpret_cast<const ushort4*>(p.k.payloads) + pay_row(kax, kk, fk, c));
+            const ushort4 hv = payload(0, pay_row(kax, kk, fk, c));
             const float4 qv = *reinterpret_cast<const float4*>(qs + g4 * 128 + 4 * c);
             corr += qv.x * __half2float(__ushort_as_half(hv.x)) +
                     qv.y * __half2float(__ushort_as_half(hv.y)) +
@@ -992,8 +1022,7 @@ __global__ void __launch_bounds__(kMThreads, 2) attention_mma_kernel(AttParams p
             while (bits) {
               const int j = __ffs(bits) - 1;
               bits &= bits - 1u;
-              const ushort4 hv = __ldg(reinterpret_cast<const ushort4*>(p.v.payloads) +
-                                       pay_row(vax, kw0 + kk, fv, 4 * g4 + j));
+              const ushort4 hv = payload(1, pay_row(vax, kw0 + kk, fv, 4 * g4 + j));
               const float x[4] = {__half2float(__ushort_as_half(hv.x)),
                                   __half2float(__ushort_as_half(hv.y)),
                                   __half2float(__ushort_as_half(hv.z)),

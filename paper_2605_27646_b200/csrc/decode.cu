@@ -41,6 +41,18 @@ struct Out<__nv_bfloat16> {
   static __device__ __forceinline__ __nv_bfloat16 cvt(float v) { return __float2bfloat16_rn(v); }
 };
 
+// r * codeword (fp16 table entry) rounded ONCE to fp16: the product in fp32
+// (packed), then one RN conversion -- the fp16 output is fp16 of the fp32
+// decode, not a double rounding through an fp16 radius
+__device__ __forceinline__ uint2 mul_round_f16(float r, uint2 cw) {
+  const float2 c01 = __half22float2(*reinterpret_cast<const __half2*>(&cw.x));
+  const float2 c23 = __half22float2(*reinterpret_cast<const __half2*>(&cw.y));
+  const float2 rr = make_float2(r, r);
+  const float2 p01 = __fmul2_rn(rr, c01), p23 = __fmul2_rn(rr, c23);
+  const __half2 h01 = __floats2half2_rn(p01.x, p01.y), h23 = __floats2half2_rn(p23.x, p23.y);
+  return make_uint2(*reinterpret_cast<const uint32_t*>(&h01), *reinterpret_cast<const uint32_t*>(&h23));
+}
+
 struct DecParams {
   int64_t B, H, T, D;
   int C, S, br, w;
@@ -224,9 +236,7 @@ __device__ __forceinline__ void decode_token_fast(const DecParams& p, const uint
     const __half2 c23 = *reinterpret_cast<const __half2*>(&cw.y);
     uint2 ov;
     if constexpr (std::is_same<OutT, __half>::value) {
-      const __half2 r2 = __float2half2_rn(rad);
-      const __half2 o01 = __hmul2(r2, c01), o23 = __hmul2(r2, c23);
-      ov = make_uint2(*reinterpret_cast<const uint32_t*>(&o01), *reinterpret_cast<const uint32_t*>(&o23));
+      ov = mul_round_f16(rad, cw);
     } else {
       const float2 f01 = __half22float2(c01), f23 = __half22float2(c23);
       const __nv_bfloat162 o01 = __floats2bfloat162_rn(rad * f01.x, rad * f01.y);
@@ -281,13 +291,8 @@ __device__ __forceinline__ void decode_token2_fast(const uint32_t* __restrict__ 
     const uint2 b = reinterpret_cast<const uint2*>(tab)[i1];
     uint4 ov;
     if constexpr (std::is_same<OutT, __half>::value) {
-      const __half2 ra = __float2half2_rn(r0), rb = __float2half2_rn(r1);
-      const __half2 x0 = __hmul2(ra, *reinterpret_cast<const __half2*>(&a.x));
-      const __half2 x1 = __hmul2(ra, *reinterpret_cast<const __half2*>(&a.y));
-      const __half2 x2 = __hmul2(rb, *reinterpret_cast<const __half2*>(&b.x));
-      const __half2 x3 = __hmul2(rb, *reinterpret_cast<const __half2*>(&b.y));
-      ov = make_uint4(*reinterpret_cast<const uint32_t*>(&x0), *reinterpret_cast<const uint32_t*>(&x1),
-                      *reinterpret_cast<const uint32_t*>(&x2), *reinterpret_cast<const uint32_t*>(&x3));
+      const uint2 x01 = mul_round_f16(r0, a), x23 = mul_round_f16(r1, b);
+      ov = make_uint4(x01.x, x01.y, x23.x, x23.y);
     } else {
       const float2 a01 = __half22float2(*reinterpret_cast<const __half2*>(&a.x));
       const float2 a23 = __half22float2(*reinterpret_cast<const __half2*>(&a.y));
@@ -424,10 +429,11 @@ __global__ void __launch_bounds__(256, 7) decode_fast_kernel(DecParams p) {
                                               (uint32_t)ncw, rtop, bad, row, p.t0 + tile * kFDTok + tt);
     }
     // release the stage without a block barrier: the last warp done with it
-    // issues the tile kFDStages ahead into it
+    // (acq_rel release count: every warp's reads precede the refill) issues
+    // the tile kFDStages ahead into it
     __syncwarp();
     if (lane == 0) {
-      if (atomicAdd(&released[stage], 1u) == 7u) {
+      if (stage_release(&released[stage]) == 7u) {
         released[stage] = 0u;
         const int64_t nxt = tile + (int64_t)kFDStages * gridDim.x;
         if (nxt < ntile) issue(nxt, stage);
@@ -737,11 +743,7 @@ __global__ void __launch_bounds__(256, 6) decode_flag_tma_kernel(DecParams p) {
           uint2 ov[4];
 #pragma unroll
           for (int c = 0; c < 4; ++c) {
-            const uint2 cw = reinterpret_cast<const uint2*>(tab)[idx[c]];
-            const __half2 rr = __float2half2_rn(rad[c]);
-            const __half2 x01 = __hmul2(rr, *reinterpret_cast<const __half2*>(&cw.x));
-            const __half2 x23 = __hmul2(rr, *reinterpret_cast<const __half2*>(&cw.y));
-            ov[c] = make_uint2(*reinterpret_cast<const uint32_t*>(&x01), *reinterpret_cast<const uint32_t*>(&x23));
+            ov[c] = mul_round_f16(rad[c], reinterpret_cast<const uint2*>(tab)[idx[c]]);
           }
           if (f4) {  // outlier chunks: their fp16 payload rows verbatim
 #pragma unroll
@@ -802,7 +804,7 @@ __global__ void __launch_bounds__(256, 6) decode_flag_tma_kernel(DecParams p) {
     }
     __syncwarp();
     if (lane == 0) {
-      if (atomicAdd(&released[stage], 1u) == 7u) {
+      if (stage_release(&released[stage]) == 7u) {
         released[stage] = 0u;
         const int64_t nxt = tile + (int64_t)kFlStages * gridDim.x;
         if (nxt < ntile) issue(nxt, stage);

@@ -1023,11 +1023,27 @@ __global__ void __launch_bounds__(kTcThreads, kMinB) encode_tc_kernel(EncParams 
     for (int q = 0; q < kN / 32; ++q) {
       float vals[32];
       tc_ld32(tmem + (uint32_t)(q * 32), vals);
+      // coset scores max(max|v_i|, sum|v_i| / 2) with packed fp32 pairs: one
+      // FADD2 (|w|+|y|, |x|+|z|) per secondary and one FMUL2 per two
+      float scs[8];
+#pragma unroll
+      for (int j = 0; j < 8; j += 2) {
+        float sum[2], mx[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const float* v = vals + 4 * (j + h);
+          const float2 p2 = __fadd2_rn(make_float2(fabsf(v[0]), fabsf(v[1])),
+                                       make_float2(fabsf(v[2]), fabsf(v[3])));
+          sum[h] = p2.x + p2.y;
+          mx[h] = fmax3(fabsf(v[0]), fabsf(v[1]), fabsf(v[2]));
+        }
+        const float2 half2 = __fmul2_rn(make_float2(sum[0], sum[1]), make_float2(0.5f, 0.5f));
+        scs[j] = fmax3(mx[0], fabsf(vals[4 * j + 3]), half2.x);
+        scs[j + 1] = fmax3(mx[1], fabsf(vals[4 * j + 7]), half2.y);
+      }
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const float2 wx = make_float2(vals[4 * j], vals[4 * j + 1]);
-        const float2 yz = make_float2(vals[4 * j + 2], vals[4 * j + 3]);
-        const float sc = coset_score(wx, yz);
+        const float sc = scs[j];
         const int s = blk * kBlk + q * 8 + j;
         const bool gt = sc > best;
         second = fmaxf(second, fminf(sc, best));

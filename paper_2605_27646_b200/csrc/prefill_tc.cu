@@ -122,9 +122,6 @@ __device__ __forceinline__ void fa_wait(uint64_t* bar, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 
 // Softmax inner step over 32 scores of one row (log2 domain): masked entries
 // already -inf; exponentials against m_use by ex2.approx (inputs <= 8 or

@@ -91,24 +91,25 @@ def test_frozen_threshold_errors(cuda):
         m.PagedKVCache(m.CodecConfig(16, 4), 1, 1, 128, outlier_thresholds=1.0)
 
 
-@pytest.mark.parametrize("S,br,B,HQ,HKV,TQ,T,causal", [
-    (64, 6, 2, 8, 2, 1, 2048, True),     # the C3 codec config, GQA 4
-    (64, 6, 1, 7, 1, 1, 4104, False),    # GQA 7 (Qwen), T % 128 != 0
-    (16, 4, 2, 8, 2, 2, 1032, True),     # C1 codec config, T_q = 2 (causal offsets)
-    (256, 4, 1, 8, 1, 1, 520, True),     # S = 256 (13-bit codes)
+@pytest.mark.parametrize("S,br,B,HQ,HKV,TQ,T,causal,C", [
+    (64, 6, 2, 8, 2, 1, 2048, True, 3.0),     # the C3 codec config, GQA 4
+    (64, 6, 1, 7, 1, 1, 4104, False, 3.0),    # GQA 7 (Qwen), T % 128 != 0
+    (16, 4, 2, 8, 2, 2, 1032, True, 3.0),     # C1 codec config, T_q = 2 (causal offsets)
+    (256, 4, 1, 8, 1, 1, 520, True, 3.0),     # S = 256 (13-bit codes)
+    (64, 4, 1, 8, 2, 1, 1024, True, 1.2),     # ~25% outliers: tiles past the staged payload rows
 ])
-def test_med3x_attention_tensor_core_vs_oracle(cuda, oracle, S, br, B, HQ, HKV, TQ, T, causal):
+def test_med3x_attention_tensor_core_vs_oracle(cuda, oracle, S, br, B, HQ, HKV, TQ, T, causal, C):
     m = hq()
     gen = torch.Generator(device=cuda).manual_seed(T + S)
-    cfg = m.CodecConfig(S, br, outlier_multiplier=3.0)
+    cfg = m.CodecConfig(S, br, outlier_multiplier=C)
     bank = m.CodebookBank(0, S)
     k = heavy((B, HKV, T, 128), gen, cuda)
     v = heavy((B, HKV, T, 128), gen, cuda)
     pk = m.encode_tensor(k, cfg, role="K", bank=bank, layer=4)
     pv = m.encode_tensor(v, cfg, role="V", bank=bank, layer=4)
     assert pk.n_payload > 0 and pv.n_payload > 0
-    rk = oracle.encode(np64(k), S, br, multiplier=3.0, layer=4, role="K")
-    rv = oracle.encode(np64(v), S, br, multiplier=3.0, layer=4, role="V")
+    rk = oracle.encode(np64(k), S, br, multiplier=C, layer=4, role="K")
+    rv = oracle.encode(np64(v), S, br, multiplier=C, layer=4, role="V")
     assert m.to_bytes(pk) == oracle.to_bytes(rk) and m.to_bytes(pv) == oracle.to_bytes(rv)
     q = torch.randn((B, HQ, TQ, 128), generator=gen, device=cuda)
     acfg = m.AttentionConfig(B, HQ, HKV, TQ, T, 128, causal=causal)

@@ -18,16 +18,20 @@ def hq():
 
 
 def _dense(m, cfg, bank, q, ks, vs, g, layer=0):
-    """Per-sequence reference: one-shot encode + fp64 decode + dense attention."""
+    """Per-sequence reference: one-shot encode + fp64 decode (bit-exact against
+    the oracle's decode, test_gpu_parity.py) + the ORACLE's dense fp64
+    attention (oracle.reference_attend, attention.py:80-101)."""
+    import hqmq_oracle as O
+
     outs = []
     for b, (k, v) in enumerate(zip(ks, vs)):
-        T = k.shape[1]
         pk = m.encode_tensor(k[None], cfg, role="K", bank=bank, layer=layer)
         pv = m.encode_tensor(v[None], cfg, role="V", bank=bank, layer=layer)
-        acfg = m.AttentionConfig(1, q.shape[1], k.shape[0], 1, T, 128)
-        outs.append(m.reference_attend(q[b:b + 1], m.decode_tensor(pk, bank, dtype=torch.float64),
-                                       m.decode_tensor(pv, bank, dtype=torch.float64), acfg))
-    return torch.cat(outs)
+        kd = m.decode_tensor(pk, bank, dtype=torch.float64).cpu().numpy()
+        vd = m.decode_tensor(pv, bank, dtype=torch.float64).cpu().numpy()
+        outs.append(torch.from_numpy(O.reference_attend(q[b:b + 1].double().cpu().numpy(), kd, vd,
+                                                        q.shape[1] // k.shape[0], causal=True)))
+    return torch.cat(outs).to(q.device)
 
 
 @pytest.mark.parametrize("S,br,g", [(64, 4, 4), (16, 4, 8), (256, 4, 1), (64, 6, 2)])
