@@ -179,8 +179,14 @@ __global__ void __launch_bounds__(kDecThreads) decode_kernel(DecParams p) {
 // three sections into a kFDStages-deep shared-memory ring with 1-D bulk
 // copies (cp.async.bulk, completion on an mbarrier) while all 8 warps decode
 // the previous tiles (warp = token, lane = chunk) and write coalesced rows.
-constexpr int kFDTok = 64;
-constexpr int kFDStages = 4;
+#ifndef HQMQ_FD_TOK
+#define HQMQ_FD_TOK 128
+#endif
+#ifndef HQMQ_FD_STAGES
+#define HQMQ_FD_STAGES 2
+#endif
+constexpr int kFDTok = HQMQ_FD_TOK;        // tokens per ring tile
+constexpr int kFDStages = HQMQ_FD_STAGES;  // ring depth
 
 struct FastDecodeGeom {
   uint32_t idx_off, rad_off, sc_off, stage_bytes;
