@@ -457,8 +457,8 @@ def test_attention_golden(cuda, name):
     (1, 8, 2, 200, 200, True, 3.0),     # Med3x payloads inside the tiles
 ])
 def test_attention_prefill_tensor_core(cuda, oracle, case):
-    """Tensor-core prefill path (rows > 8, d=128) vs the dense fp64 reference over
-    the decoded cache (attention.py:80-101).  Tolerance 2e-3: the fp16 operand
+    """Prefill paths (rows > 8, d=128) vs the dense fp64 reference over the
+    decoded cache (attention.py:80-101).  Tolerance 2e-3 relative to max(1, |out|): the fp16 operand
     rounding of V dominates on causal rows that see only a few keys (the paper
     reports 9.8e-4 for its fp16 prefill kernel)."""
     m = hq()
@@ -472,12 +472,14 @@ def test_attention_prefill_tensor_core(cuda, oracle, case):
     pk = m.encode_tensor(k, cfg, role="K", bank=bank)
     pv = m.encode_tensor(v, cfg, role="V", bank=bank)
     acfg = m.AttentionConfig(B, HQ, HKV, TQ, TK, 128, causal=causal)
-    out = m.fused_attend(q, pk, pv, bank, acfg).double().cpu().numpy()
     dense = oracle.reference_attend(q.double().cpu().numpy(),
                                     m.decode_tensor(pk, bank, dtype=torch.float64).cpu().numpy(),
                                     m.decode_tensor(pv, bank, dtype=torch.float64).cpu().numpy(),
                                     HQ // HKV, causal=causal)
-    assert np.max(np.abs(out - dense)) < 2e-3
+    bound = np.maximum(1.0, np.abs(dense))  # Med3x payload rows exceed 1
+    for mode in ("tcgen05", "auto"):  # the fused kernels, and fp16 decode + SDPA
+        out = m.fused_attend(q, pk, pv, bank, acfg, prefill=mode).double().cpu().numpy()
+        assert np.max(np.abs(out - dense) / bound) < 2e-3, mode
 
 
 def test_attention_decode_llama_shape(cuda, oracle):

@@ -1,7 +1,9 @@
-"""The two tcgen05 prefill kernels (attention_fa2_kernel below 4096 keys,
-attention_fa4_kernel from 4096 keys: launch_prefill_tc picks by key count)
-against the oracle's dense fp64 attention over the fp64 decode of the same
-cache.  Bound: 2e-3 relative to max(1, |out|) -- TWICE the reference's fp32
+"""Prefill attention over the compressed cache, both paths: the two tcgen05
+prefill kernels (prefill="tcgen05": attention_fa2_kernel below 4096 keys,
+attention_fa4_kernel from 4096 keys; launch_prefill_tc picks by key count --
+the C ABI's path) and the default composition (prefill="auto": the sm_100a
+fp16 decode + PyTorch SDPA), against the oracle's dense fp64 attention over
+the fp64 decode of the same cache.  Bound: 2e-3 relative to max(1, |out|) -- TWICE the reference's fp32
 tolerance (test_attention.py:97-102, 1e-3): Q, K, V and P are fp16 tensor-core
 operands, and fp16 rounding of Q and K moves logits of magnitude ~10 by ~1e-2,
 i.e. P by ~1% (measured worst 1.2e-3 on causal GQA rows).  A documented gap
@@ -20,6 +22,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, os.path.join(ROOT, "oracle"))
 
 
+@pytest.mark.parametrize("mode", ["tcgen05", "auto"])
 @pytest.mark.parametrize("shape", [
     (1, 8, 2, 300, 300, True),     # fa2, GQA 4, causal, ragged tiles
     (2, 4, 4, 130, 200, True),     # fa2, no GQA, Tq < Tkv offset
@@ -27,7 +30,7 @@ sys.path.insert(0, os.path.join(ROOT, "oracle"))
     (1, 8, 2, 200, 4100, True),    # fa4 (>= 4096 keys), ragged last tile
     (1, 4, 1, 64, 4096, False),    # fa4, GQA 4, non-causal
 ])
-def test_prefill_kernels_vs_oracle(cuda, shape):
+def test_prefill_kernels_vs_oracle(cuda, shape, mode):
     import torch
 
     import hqmq_oracle as O
@@ -44,7 +47,10 @@ def test_prefill_kernels_vs_oracle(cuda, shape):
     pk = m.encode_tensor(k, cfg, role="K", bank=bank)
     pv = m.encode_tensor(v, cfg, role="V", bank=bank)
     acfg = m.AttentionConfig(B, HQ, HKV, TQ, TK, 128, causal=causal)
-    out = m.fused_attend(q, pk, pv, bank, acfg).double().cpu().numpy()
+    name = m.attention_kernel(q, pk, pv, bank, acfg, prefill=mode)
+    assert name == ("prefill_tc (tcgen05 flash attention)" if mode == "tcgen05"
+                    else "decode_fast_kernel (fp16) + torch SDPA"), name
+    out = m.fused_attend(q, pk, pv, bank, acfg, prefill=mode).double().cpu().numpy()
     kd = m.decode_tensor(pk, bank, dtype=torch.float64).cpu().numpy()
     vd = m.decode_tensor(pv, bank, dtype=torch.float64).cpu().numpy()
     # kd / vd: the fp64 decode, bit-exact against the oracle's decode
