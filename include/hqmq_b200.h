@@ -5,8 +5,11 @@
  * (/root/reference/pkg/src/hqmq/).  Every entry point takes plain device
  * pointers and sizes (caller-allocated, e.g. by torch), is asynchronous on the
  * caller's CUDA stream (`stream` is a cudaStream_t passed as void*; NULL = the
- * legacy default stream), holds no global mutable state, and returns an
- * hqmq_status.  Data-dependent failures that the reference raises as Python
+ * legacy default stream), and returns an hqmq_status.  The only mutable
+ * library state is per thread: the last error text (hqmq_last_error) and a
+ * small cache of occupancy queries keyed by (kernel, shared memory, device)
+ * that sizes the decode grids; calls are reentrant across streams and
+ * devices (the kernel launches on the calling thread's current device).  Data-dependent failures that the reference raises as Python
  * exceptions are reported through a device-resident error word (HQMQ_DEVERR_*)
  * that the host maps to the reference's exception types after it synchronises.
  *

@@ -1139,25 +1139,99 @@ __global__ void __launch_bounds__(kTcThreads, kMinB) encode_tc_kernel(EncParams 
                  "n"(2 * kN));
 }
 
-// Per-token coded (unflagged) chunk count from the stored norms (C = 32).
-__global__ void token_coded_norms_kernel(const double* __restrict__ norms,
-                                         const RadixGroup* groups, int64_t H, int64_t T,
-                                         int64_t n_tok, int per_head, uint32_t* cnt) {
-  pdl_wait();
-  pdl_trigger();
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n_tok;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t row = t / T;
-    const double thr = groups[per_head ? (int)(row % H) : 0].threshold;
-    const double2* nr = reinterpret_cast<const double2*>(norms + t * 32);
-    uint32_t c = 0;
+// Coded-chunk count of every token and its exclusive prefix (token_offsets),
+// in ONE pass with a decoupled look-back across blocks: warp = 32 tokens
+// (one coalesced 256-byte load of a token's 32 squared norms per step, flags
+// by ballot), block = 256 tokens, block order from a ticket counter so every
+// predecessor is already running.  Status word per block: bits 62-63 = 1
+// (aggregate published) / 2 (inclusive prefix published), low bits the value.
+// The last block writes counters[0..1] (n_coded, n_payload).  Replaces the
+// per-token count kernel + cub scan + finalize of the first version.
+constexpr int kOffThreads = 256;
+__global__ void __launch_bounds__(kOffThreads) token_offsets_kernel(
+    const double* __restrict__ norms, const RadixGroup* groups, int64_t H, int64_t T, int64_t n_tok,
+    int per_head, unsigned long long* status, unsigned int* ticket, uint32_t* tokoff,
+    int64_t n_chunks, int64_t* counters) {
+  __shared__ uint32_t s_blk;
+  __shared__ uint32_t wsum[kOffThreads / 32];
+  __shared__ unsigned long long s_prefix;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_blk = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const int64_t blk = s_blk;
+  const int64_t tok0 = blk * kOffThreads + warp * 32;
+  // lane l ends up with the coded count of token tok0 + l; 8 tokens' norm rows
+  // in flight per step (coalesced 256-byte loads), flags by ballot
+  uint32_t mine = 0;
+  const double thr0 = groups[0].threshold;
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      const double2 v = nr[k];  // squared norms
-      c += (sqrt_gt(v.x, thr) ? 0u : 1u) + (sqrt_gt(v.y, thr) ? 0u : 1u);
+  for (int j0 = 0; j0 < 32; j0 += 8) {
+    double v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int64_t t = tok0 + j0 + k;
+      v[k] = t < n_tok ? __ldcs(norms + t * 32 + lane) : 0.0;
     }
-    cnt[t] = c;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int64_t t = tok0 + j0 + k;
+      const double thr = per_head ? groups[(int)((t / T) % H)].threshold : thr0;
+      const bool fl = t < n_tok && sqrt_gt(v[k], thr);
+      const uint32_t m = __ballot_sync(0xffffffffu, fl);
+      if (lane == j0 + k && t < n_tok) mine = 32u - __popc(m);  // tokens past the end count 0
+    }
   }
+  // block exclusive scan of the 256 counts
+  uint32_t incl = mine;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  uint32_t wbase = 0, total = 0;
+  for (int w = 0; w < kOffThreads / 32; ++w) {
+    if (w < warp) wbase += wsum[w];
+    total += wsum[w];
+  }
+  // decoupled look-back, warp 0: 32 predecessors' status words per step
+  if (warp == 0) {
+    const unsigned long long kAgg = 1ull << 62, kInc = 2ull << 62, kMaskV = (1ull << 62) - 1ull;
+    unsigned long long prefix = 0;
+    if (blk == 0) {
+      if (lane == 0) atomicExch(status, kInc | total);
+    } else {
+      if (lane == 0) atomicExch(status + blk, kAgg | total);
+      int64_t b = blk - 1;
+      while (true) {
+        const int64_t idx = b - lane;
+        // (before block 0: an inclusive prefix of 0)
+        const unsigned long long st = idx >= 0 ? __ldcg(status + idx) : kInc;
+        if (__any_sync(0xffffffffu, (st >> 62) == 0ull)) continue;  // a predecessor not published yet
+        const uint32_t incm = __ballot_sync(0xffffffffu, (st >> 62) == 2ull);
+        const int first = incm ? __ffs(incm) - 1 : 31;  // nearest inclusive prefix
+        unsigned long long v = lane <= first ? (st & kMaskV) : 0ull;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        prefix += v;
+        if (incm) break;
+        b -= 32;
+      }
+      if (lane == 0) atomicExch(status + blk, kInc | (prefix + total));
+    }
+    if (lane == 0) {
+      s_prefix = prefix;
+      if (blk * kOffThreads + kOffThreads >= n_tok) {  // the last block: totals
+        const int64_t coded = (int64_t)(prefix + total);
+        counters[0] = coded;
+        counters[1] = n_chunks - coded;
+      }
+    }
+  }
+  __syncthreads();
+  const int64_t t = tok0 + lane;
+  if (t < n_tok) tokoff[t] = (uint32_t)(s_prefix + wbase + incl - mine);
 }
 
 // ------------------------------------------------------ Med3x radix select
@@ -1188,6 +1262,7 @@ struct RadixParams {
   unsigned int* done;
   int G;
   int norms_only;  // pass 0 stores the squared norms and builds no histogram (fixed thresholds)
+  double* thr_out; // optional: the groups' thresholds (hqmq_encode_args.thresholds_out)
 };
 
 // Shared-memory histogram add.  (Pass 0's digits -- exponent + top mantissa
@@ -1390,8 +1465,9 @@ __global__ void __launch_bounds__(kTailThreads) radix_tail_kernel(RadixParams p)
   if (threadIdx.x == 0) {
     p.groups[g].prefix = s_pref;
     p.groups[g].rank = s_rank;
-    p.groups[g].threshold =
-        __dmul_rn(p.multiplier, __dsqrt_rn(__longlong_as_double((long long)s_pref)));
+    const double thr = __dmul_rn(p.multiplier, __dsqrt_rn(__longlong_as_double((long long)s_pref)));
+    p.groups[g].threshold = thr;
+    if (p.thr_out) p.thr_out[g] = thr;
   }
 }
 
@@ -1410,9 +1486,13 @@ __global__ void copy_thresholds_kernel(const RadixGroup* groups, double* out, in
 }
 
 __global__ void radix_init_kernel(RadixGroup* groups, unsigned int* cand_n, int G,
-                                  unsigned long long n_per_group) {
-  const int g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g < G) {
+                                  unsigned long long n_per_group, unsigned long long* status = nullptr,
+                                  int64_t n_status = 0, unsigned int* ticket = nullptr) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (status && i < n_status) status[i] = 0ull;
+  if (ticket && i == 0) *ticket = 0u;
+  const int g = (int)i;
+  if (i < G) {
     groups[g].prefix = 0ull;
     groups[g].rank = (n_per_group - 1) / 2;
     groups[g].threshold = 0.0;
@@ -1558,7 +1638,14 @@ int launch_encode(const hqmq_encode_args* a, const Layout& L, cudaStream_t st) {
     const unsigned long long n_per_group =
         (unsigned long long)(L.n_chunks / (a->per_head_pooling ? a->heads : 1));
     unsigned int* cand_n = reinterpret_cast<unsigned int*>(ws + L.off_cand_n);
-    radix_init_kernel<<<(L.G + 127) / 128, 128, 0, st>>>(groups, cand_n, L.G, n_per_group);
+    // warp path: the single-pass token-offset scan's block status words
+    // (in the tile-prefix region) and its block ticket (done[1]) start at 0
+    const int64_t n_tok_all = L.rows * a->tokens;
+    const int64_t n_status = L.warp_path ? ceil_div(n_tok_all, kOffThreads) : 0;
+    unsigned long long* status = reinterpret_cast<unsigned long long*>(ws + L.off_prefix);
+    const int64_t n_init = std::max<int64_t>(L.G, n_status);
+    radix_init_kernel<<<(unsigned)ceil_div(n_init, 128), 128, 0, st>>>(
+        groups, cand_n, L.G, n_per_group, L.warp_path ? status : nullptr, n_status, nullptr);
     RadixParams rp;
     rp.B = a->batch; rp.H = a->heads; rp.T = a->tokens; rp.D = a->head_dim; rp.C = L.C;
     rp.per_head = a->per_head_pooling; rp.aligned4 = aligned4; rp.multiplier = a->outlier_multiplier;
@@ -1572,32 +1659,30 @@ int launch_encode(const hqmq_encode_args* a, const Layout& L, cudaStream_t st) {
         1, std::min<int64_t>(ceil_div((int64_t)148 * 4, L.rows), ceil_div(row_chunks, kHistThreads * 8)));
 
     rp.norms_only = a->fixed_thresholds != nullptr;
+    rp.thr_out = a->thresholds_out;
     if (rp.norms_only) {  // frozen thresholds: the norms pass only
       rp.pass = 0;
       radix_hist_kernel<InT><<<dim3((unsigned)bx_full, (unsigned)L.rows), kHistThreads, 0, st>>>(rp);
       set_thresholds_kernel<<<(L.G + 127) / 128, 128, 0, st>>>(groups, a->fixed_thresholds, L.G);
+      if (a->thresholds_out)
+        copy_thresholds_kernel<<<(L.G + 127) / 128, 128, 0, st>>>(groups, a->thresholds_out, L.G);
     } else {
       for (int pass = 0; pass <= 2; ++pass) {
         rp.pass = pass;
         radix_hist_kernel<InT><<<dim3((unsigned)bx_full, (unsigned)L.rows), kHistThreads, 0, st>>>(rp);
       }
-      radix_tail_kernel<<<L.G, kTailThreads, 0, st>>>(rp);
+      radix_tail_kernel<<<L.G, kTailThreads, 0, st>>>(rp);  // also writes thresholds_out
     }
-    if (a->thresholds_out)
-      copy_thresholds_kernel<<<(L.G + 127) / 128, 128, 0, st>>>(groups, a->thresholds_out, L.G);
     uint32_t* counts = reinterpret_cast<uint32_t*>(ws + L.off_counts);
     size_t cub_bytes = L.cub_bytes;
     if (L.warp_path) {
-      // per-token coded counts -> exclusive scan straight into token_offsets
-      const int64_t n_tok = L.rows * a->tokens;
-      token_coded_norms_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n_tok, 256), 148 * 16), 256,
-                                 0, st>>>(rp.norms, groups, a->heads, a->tokens, n_tok,
-                                          a->per_head_pooling, counts);
-      e = cub::DeviceScan::ExclusiveSum(ws + L.off_cub, cub_bytes, counts, a->token_offsets,
-                                        (int)n_tok, st);
-      if (e != cudaSuccess) return cuda_fail(e);
-      finalize_counts_kernel<<<1, 32, 0, st>>>(counts, a->token_offsets, n_tok, L.n_chunks,
-                                               a->counters);
+      // per-token coded counts and their exclusive scan into token_offsets,
+      // one pass (decoupled look-back), totals into counters
+      (void)counts;
+      (void)cub_bytes;
+      token_offsets_kernel<<<(unsigned)n_status, kOffThreads, 0, st>>>(
+          rp.norms, groups, a->heads, a->tokens, n_tok_all, a->per_head_pooling, status, done + 1,
+          a->token_offsets, L.n_chunks, a->counters);
     } else {
       prefix = reinterpret_cast<uint32_t*>(ws + L.off_prefix);
       tile_count_kernel<<<dim3((unsigned)L.tiles_per_row, (unsigned)L.rows), 256, 0, st>>>(
