@@ -60,6 +60,10 @@ class PagedKVCache:
         self.med3x = config.outlier_multiplier is not None
         if outlier_thresholds is not None and not self.med3x:
             raise InvalidArgument("outlier_thresholds requires outlier extraction")
+        if self.med3x and config.codebook_size > 170:
+            # the Med3x paged kernel keeps four 24*S-entry fp16 tables (K and V,
+            # each with its residual) in shared memory: S <= 170 (index_bits <= 12)
+            raise InvalidArgument("paged Med3x caches support codebook_size <= 170")
         if head_dim != 128:
             raise InvalidArgument("paged caches support head_dim 128")
         if batch < 1 or kv_heads < 1 or max_tokens < 1:

@@ -89,6 +89,8 @@ def test_frozen_threshold_errors(cuda):
                         outlier_thresholds=[1.0, 2.0, 3.0])
     with pytest.raises(m.InvalidArgument):
         m.PagedKVCache(m.CodecConfig(16, 4), 1, 1, 128, outlier_thresholds=1.0)
+    with pytest.raises(m.InvalidArgument):  # four S=256 tables exceed shared memory
+        m.PagedKVCache(m.CodecConfig(256, 4, outlier_multiplier=3.0), 1, 1, 128)
 
 
 @pytest.mark.parametrize("S,br,B,HQ,HKV,TQ,T,causal,C", [
@@ -221,3 +223,23 @@ def test_paged_med3x_appends_token_local(cuda):
         assert pa.keys() == pb.keys() and len(pa) > 0
         for slot in pa:
             np.testing.assert_array_equal(pa[slot], pb[slot])
+
+
+@pytest.mark.parametrize("dtype,D,pool", [(torch.float32, 96, "batch"), (torch.bfloat16, 64, "per_head")])
+def test_frozen_threshold_general_path(cuda, oracle, dtype, D, pool):
+    """Frozen thresholds on the general encode path (not fp16 / head_dim 128:
+    the tile kernel): thresholds_out equals the oracle's C * median, and a
+    frozen-threshold encode is bit-exact against the oracle."""
+    m = hq()
+    gen = torch.Generator(device=cuda).manual_seed(D)
+    cfg = m.CodecConfig(24, 5, seed=3, outlier_multiplier=2.5, median_pooling=pool)
+    bank = m.CodebookBank(3, 24)
+    x = heavy((2, 3, 40, D), gen, cuda).to(dtype)
+    qt = m.encode_tensor(x, cfg, layer=2, role="K", bank=bank)
+    thr_ref = oracle.outlier_thresholds(oracle_norms(oracle, np64(x)), 2.5, pool)
+    np.testing.assert_array_equal(qt.outlier_thresholds.cpu().numpy(), thr_ref)
+    y = heavy((2, 3, 17, D), gen, cuda).to(dtype)
+    qy = m.encode_tensor(y, cfg, layer=2, role="K", bank=bank, outlier_thresholds=thr_ref)
+    ref = oracle.encode(np64(y), 24, 5, seed=3, multiplier=2.5, pooling=pool, layer=2, role="K",
+                        thresholds=thr_ref)
+    assert m.to_bytes(qy) == oracle.to_bytes(ref)

@@ -1,8 +1,11 @@
 """Randomised attention parity: fused_attend (decode steps, chunked / full prefill,
-causal or not, GQA groups 1-8, Med3x or not, S in {16, 64, 256}) against the dense
-fp64 attention over the decoded cache (attention.py:80-101), tolerance 2e-3 (relative
-to |out| where that exceeds 1: fp16 P and V); for
-decode steps without Med3x also the paged cache (same tolerance).
+causal or not, GQA groups 1-8, Med3x or not, S in {16, 64, 256}) against the
+ORACLE's dense fp64 attention (oracle.reference_attend, attention.py:80-101) over
+the fp64 decode of the cache (bit-exact against the oracle's decode), tolerance
+2e-3 relative to |out| where that exceeds 1 (fp16 P and V); for decode steps also
+the paged cache (same tolerance) -- with Med3x a prefill append (own median) and a
+frozen-threshold append, referenced against the contiguous encodes of the same
+two calls with the same thresholds.
 
     python tools/fuzz_attention.py --cases 100 --seed 1
 """
@@ -11,7 +14,9 @@ import os
 import sys
 import time
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path[:0] = [ROOT, os.path.join(ROOT, "oracle")]
+import hqmq_oracle as O  # noqa: E402  (checker only)
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
@@ -38,8 +43,13 @@ def one(rs, dev):
     pv = m.encode_tensor(v, cfg, role="V", bank=bank)
     acfg = m.AttentionConfig(B, HKV * g, HKV, TQ, TK, 128, causal=causal)
     out = m.fused_attend(q, pk, pv, bank, acfg)
-    dense = m.reference_attend(q, m.decode_tensor(pk, bank, dtype=torch.float64),
-                               m.decode_tensor(pv, bank, dtype=torch.float64), acfg)
+
+    def dense_of(kd, vd):
+        return torch.from_numpy(O.reference_attend(q.double().cpu().numpy(), kd.cpu().numpy(),
+                                                   vd.cpu().numpy(), g, causal=causal)).to(dev)
+
+    dense = dense_of(m.decode_tensor(pk, bank, dtype=torch.float64),
+                     m.decode_tensor(pv, bank, dtype=torch.float64))
     # fp16 P and V: a row that sees few keys returns ~v rounded to fp16, so the
     # bound is 2e-3 relative to |out| where that exceeds 1 (Med3x payload rows)
     diff = (out.double() - dense).abs()
@@ -48,15 +58,26 @@ def one(rs, dev):
     desc = f"S={S} C={C} B={B} Hkv={HKV} g={g} Tq={TQ} Tkv={TK} causal={causal}: err {err:.2e} (scaled {rel:.2e})"
     if not rel < 2e-3:
         return False, desc
-    if decode and C is None and g <= 8:
+    if decode and g <= 8 and (C is None or (TK >= 2 and S <= 170)):
         cache = m.PagedKVCache(cfg, B, HKV, TK, bank=bank, device=dev,
                                page_order_seed=int(rs.integers(0, 100)))
-        cut = int(rs.integers(0, TK + 1))
+        cut = int(rs.integers(1 if C else 0, TK + (0 if C else 1)))
         if cut:
             cache.append(k[:, :, :cut], v[:, :, :cut])
         if cut < TK:
             cache.append(k[:, :, cut:], v[:, :, cut:])
         paged = cache.attend(q)
+        if C is not None:  # the reference: the same two calls, the second frozen
+            parts = []
+            for role, x in (("K", k), ("V", v)):
+                a = m.encode_tensor(x[:, :, :cut], cfg, role=role, bank=bank)
+                segs = [m.decode_tensor(a, bank, dtype=torch.float64)]
+                if cut < TK:
+                    b2 = m.encode_tensor(x[:, :, cut:], cfg, role=role, bank=bank,
+                                         outlier_thresholds=a.outlier_thresholds)
+                    segs.append(m.decode_tensor(b2, bank, dtype=torch.float64))
+                parts.append(torch.cat(segs, dim=2))
+            dense = dense_of(*parts)
         perr = ((paged.double() - dense).abs() / dense.abs().clamp_min(1.0)).max().item()
         d = (paged - out).abs().max().item()
         # the contiguous call may take another kernel (fp32 CUDA-core when
