@@ -561,7 +561,9 @@ def decode_token_range(packed: QuantizedTensor, bank: CodebookBank, start: int, 
     dc = packed._dc
     if dc is None or dc[0] is not bank:
         tabs = bank.device_tables(packed.layer, packed.head_base, s.heads, packed.role, dev)
-        err = torch.zeros(1, dtype=torch.int32, device=dev)
+        # decode index errors OR into the tensor's own error word (meta[3], zeroed by
+        # the encode): no allocation or fill per tensor
+        err = packed._meta.view(torch.int32)[6:7]
         args = packed._decode_args(0, 0, code, None, err, tabs["joint_f32"], tabs["joint_f64"],
                                    tabs["joint_f16"])
         dc = packed._dc = (bank, args, tabs, err)
