@@ -832,6 +832,103 @@ __global__ void __launch_bounds__(kWThreads, kMinB) encode_warp_kernel(EncParams
   }
 }
 
+// ------------------------------------------------ prep, no extraction
+// The prep pass of the model shapes without Med3x (fp16 / bf16, head_dim 128):
+// every token owns exactly BR whole radius words (32 chunks x BR bits), so a
+// token's radius codes are OR-reduced across the warp into those words with
+// REDUX (one per word; lanes 0..BR-1 store them) -- no shared-memory staging,
+// no edge words.  Warp = 4 tokens per step (lane = chunk), the next step's
+// input prefetched; per token: exact fp64 squared norms, sigma = sqrt_rn of
+// the warp max (the 4 tokens' square roots in lanes 0..3 at once), fp16 scale,
+// quanta from fp32 with an exact fp64 replay near a rounding boundary.
+template <typename InT, int BR>
+__global__ void __launch_bounds__(256, 4) encode_prep_kernel(EncParams p) {
+  constexpr int kT = 4;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  pdl_wait();  // (PDL) the input may come from the previous kernel
+  pdl_trigger();
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) {
+    p.counters[0] = p.B * p.H * p.T * 32;  // n_coded: every chunk (no extraction)
+    p.counters[1] = 0;
+  }
+  const int64_t row = blockIdx.y;
+  const double top = (double)((1 << BR) - 1);
+  const float ftop = (float)top;
+  const float qm = 4.0e-6f * (ftop + 1.0f);
+  const int64_t ntiles = ceil_div(p.T, kT);
+  const int64_t stride = (int64_t)gridDim.x * 8;
+  const InT* __restrict__ data = reinterpret_cast<const InT*>(p.data);
+  auto load_tile = [&](int64_t wt, uint2 (&raw)[kT]) {
+#pragma unroll
+    for (int j = 0; j < kT; ++j) {
+      const int64_t t = wt * kT + j;
+      raw[j] = make_uint2(0u, 0u);
+      if (wt < ntiles && t < p.T)
+        raw[j] = __ldg(reinterpret_cast<const uint2*>(data + (row * p.T + t) * 128) + lane);
+    }
+  };
+  int64_t wt = (int64_t)blockIdx.x * 8 + warp;
+  uint2 raw[kT];
+  load_tile(wt, raw);
+  for (; wt < ntiles; wt += stride) {
+    uint2 nxt[kT];
+    load_tile(wt + stride, nxt);
+    const int64_t t0 = wt * kT;
+    const int ntok = (int)min((int64_t)kT, p.T - t0);
+    const int64_t tok0 = row * p.T + t0;
+    double sq[kT];
+    double sig_l = 0.0;  // lane j (< kT) collects token j's max s
+#pragma unroll
+    for (int j = 0; j < kT; ++j) {
+      const InT* v = reinterpret_cast<const InT*>(&raw[j]);
+      double x[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) x[i] = In<InT>::d(v[i]);
+      double q2 = __dmul_rn(x[0], x[0]);
+      q2 = __dadd_rn(q2, __dmul_rn(x[1], x[1]));
+      q2 = __dadd_rn(q2, __dmul_rn(x[2], x[2]));
+      sq[j] = __dadd_rn(q2, __dmul_rn(x[3], x[3]));
+      const double m = warp_max_nonneg_f64(sq[j]);
+      sig_l = lane == j ? m : sig_l;
+    }
+    sig_l = __dsqrt_rn(sig_l);
+#pragma unroll
+    for (int j = 0; j < kT; ++j) {
+      if (j >= ntok) break;  // warp-uniform
+      double sg = __shfl_sync(0xffffffffu, sig_l, j);
+      if (!(sg > 0.0)) sg = 1.0;
+      const __half hs = __double2half(sg);
+      const double sw = (double)__half2float(hs);
+      if (lane == j) {
+        p.scales[tok0 + j] = __half_as_ushort(hs);
+        if (!(sw > 0.0)) atomicOr(p.err, HQMQ_DEVERR_SIGMA_NONPOSITIVE);
+      }
+      uint32_t q = 0;
+      if (sq[j] > 0.0) {
+        const float s32 = (float)sq[j];
+        const float vq = (s32 * rsqrtf(s32)) * __fdividef(ftop, (float)sw) + 0.5f;
+        const float fq = floorf(vq), fr = vq - fq;
+        if (s32 > 1e-30f && fr >= qm && fr <= 1.0f - qm) q = (uint32_t)fminf(fmaxf(fq, 0.f), ftop);
+        else q = exact_quantum(__dsqrt_rn(sq[j]), sw, top);
+      }
+      // the token's BR radius words: word k holds bits [32k, 32k+32) of the
+      // 32 x BR-bit run; lane l's code sits at bit BR*l
+      const uint32_t bit = (uint32_t)(BR * lane);
+      uint32_t my = 0;
+#pragma unroll
+      for (int k = 0; k < BR; ++k) {
+        const int d = (int)bit - 32 * k;  // code offset relative to word k
+        const uint32_t c = d >= 0 ? (d < 32 ? q << d : 0u) : (d > -BR ? q >> (-d) : 0u);
+        const uint32_t word = __reduce_or_sync(0xffffffffu, c);
+        if (lane == k) my = word;
+      }
+      if (lane < BR) p.radw[(tok0 + j) * BR + lane] = my;
+    }
+#pragma unroll
+    for (int j = 0; j < kT; ++j) raw[j] = nxt[j];
+  }
+}
+
 // ------------------------------------------- tcgen05 search (tensor cores)
 // The S-loop's rotations v_s = u (x) conj(q_s) for all secondaries are one
 // GEMM, V[chunk][4s+c] = sum_i u_i R_s[i][c], with contraction 4.  On sm_100a
@@ -1620,8 +1717,14 @@ int launch_encode(const hqmq_encode_args* a, const Layout& L, cudaStream_t st) {
     cudaMemsetAsync(a->radius_words, 0, a->radius_capacity_words * 4, st);
   if (!L.warp_path && a->flag_words && a->flag_capacity_words)
     cudaMemsetAsync(a->flag_words, 0, a->flag_capacity_words * 4, st);
-  cudaMemsetAsync(a->counters, 0, 3 * sizeof(int64_t), st);
-  if (a->error_word) cudaMemsetAsync(a->error_word, 0, sizeof(uint32_t), st);
+  // counters and the error word: one memset when they are contiguous (the
+  // Python host's int64[4] meta block)
+  if (a->error_word == reinterpret_cast<uint32_t*>(a->counters + 3)) {
+    cudaMemsetAsync(a->counters, 0, 4 * sizeof(int64_t), st);
+  } else {
+    cudaMemsetAsync(a->counters, 0, 3 * sizeof(int64_t), st);
+    if (a->error_word) cudaMemsetAsync(a->error_word, 0, sizeof(uint32_t), st);
+  }
   if (L.n_chunks == 0) {
     set_counts_kernel<<<1, 32, 0, st>>>(0, a->counters);
     e = cudaGetLastError();
@@ -1694,9 +1797,9 @@ int launch_encode(const hqmq_encode_args* a, const Layout& L, cudaStream_t st) {
       finalize_counts_kernel<<<1, 32, 0, st>>>(counts, prefix, L.n_tiles, L.n_chunks,
                                                a->counters);
     }
-  } else {
+  } else if (!(L.warp_path && (a->radius_bits == 4 || a->radius_bits == 6))) {
     set_counts_kernel<<<1, 32, 0, st>>>(L.n_chunks, a->counters);
-  }
+  }  // (else the no-extraction prep kernel writes n_coded = n_chunks)
   EncParams p;
   p.B = a->batch; p.H = a->heads; p.T = a->tokens; p.D = a->head_dim;
   p.C = L.C; p.S = a->codebook_size; p.br = a->radius_bits; p.w = a->index_bits;
@@ -1723,9 +1826,22 @@ int launch_encode(const hqmq_encode_args* a, const Layout& L, cudaStream_t st) {
         const int64_t bx = std::max<int64_t>(1, std::min<int64_t>(want, ceil_div(ntiles, kWWarps)));
         launch_pdl(kern, dim3((unsigned)bx, (unsigned)L.rows), dim3(kWThreads), smem, st, p);
       };
+      // the prep pass: the REDUX-packing kernel without extraction (b_r 4 / 6),
+      // the general warp kernel otherwise
+      auto prep = [&]() {
+        if (!ext && (a->radius_bits == 4 || a->radius_bits == 6)) {
+          auto pk = a->radius_bits == 4 ? encode_prep_kernel<InT, 4> : encode_prep_kernel<InT, 6>;
+          const int64_t ntiles = ceil_div(a->tokens, 4);
+          const int64_t want = ceil_div((int64_t)148 * 4, L.rows);
+          const int64_t bx = std::max<int64_t>(1, std::min<int64_t>(want, ceil_div(ntiles, 8)));
+          launch_pdl(pk, dim3((unsigned)bx, (unsigned)L.rows), dim3(256), 0, st, p);
+        } else {
+          launch(encode_warp_kernel<InT, 4, 4, 1>, 4, 4);
+        }
+      };
       switch (a->search_path) {
         case HQMQ_SEARCH_CUDA_CORE:  // prep pass, then the FFMA2 search pass
-          launch(encode_warp_kernel<InT, 4, 4, 1>, 4, 4);
+          prep();
           launch(encode_warp_kernel<InT, 4, 2, 2>, 4, 2);
           break;
         default: {  // split: prep pass, then the tensor-core search pass
@@ -1736,14 +1852,14 @@ int launch_encode(const hqmq_encode_args* a, const Layout& L, cudaStream_t st) {
           const bool tc16 = !tc32 && a->codebook_size % 16 == 0 &&
                             (a->codebook_size >= 48 || a->search_path == HQMQ_SEARCH_TENSOR_CORE);
           if (!tc32 && !tc16) {
-            launch(encode_warp_kernel<InT, 4, 4, 1>, 4, 4);
+            prep();
             launch(encode_warp_kernel<InT, 4, 2, 2>, 4, 2);
             break;
           }
           // the prep stays a pass of its own: fusing it into the tensor-core
           // kernel (run under the first MMA of each tile) measured 1.7% slower
           // at S = 64 and 2.7% at S = 256
-          launch(encode_warp_kernel<InT, 4, 4, 1>, 4, 4);
+          prep();
           auto tc = [&](auto kern) {
             const size_t tsmem = 2 * 4096 + (size_t)a->codebook_size * 4 * 32 +
                                  (size_t)a->codebook_size * 64;
