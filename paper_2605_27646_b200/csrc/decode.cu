@@ -740,7 +740,7 @@ __global__ void __launch_bounds__(256, 6) decode_flag_tma_kernel(DecParams p) {
         for (int c = 0; c < 4; ++c) {
           const uint32_t j = (uint32_t)c - __popc(f4 & ((1u << c) - 1u));  // code slot after skips
           uint32_t ix = (uint32_t)(iwin >> (j * (uint32_t)w)) & imask;
-          bad |= ix >= (uint32_t)ncw;
+          bad |= !((f4 >> c) & 1u) && ix >= (uint32_t)ncw;  // (a flagged chunk's slot is unused)
           idx[c] = ix < (uint32_t)ncw ? ix : 0u;
           rad[c] = (float)((qwin >> (j * (uint32_t)br)) & rmask) * sg;
         }

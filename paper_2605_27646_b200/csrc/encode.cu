@@ -951,7 +951,22 @@ constexpr int kTcThreads = kTcWarps * 32;
 constexpr int kTcBlk = 32;                 // secondaries per MMA (N = 128)
 constexpr int kTcN = 4 * kTcBlk;
 constexpr uint32_t kTcLBO = 128, kTcSBO = 256;  // K-major SWIZZLE_NONE core-matrix strides
-constexpr float kDeltaTc = 1e-5f;          // certification margin (split-fp16 rotation)
+// Certification margin of the tensor-core search.  A wrong certified index
+// needs the chosen secondary's fp32 score (top32) to exceed every other
+// secondary's TMEM score by kDeltaTc while the fp64 reference prefers one of
+// them, i.e. kDeltaTc <= the sum of the score errors: fp32 direction vs the
+// reference's fp64 x / r (|du| <= ~3.6e-7, on both scores of the gap: 7.2e-7),
+// the fp32 exact-rotation score of the chosen (~1e-7) and the split-fp16 TMEM
+// score of the other (u and R each kept to 22 bits, u2*R2 dropped, fp32
+// accumulation: <= ~6e-7; measured <= 2.8e-7, tools/ubench_umma.cu) -- at most
+// ~1.4e-6 with every error aligned against us.  3e-6 keeps a 2x margin (was
+// 1e-5: 3.3x the fixups).  Measured: the index / radius streams of the 64 C2
+// units and 32 C5 units are bit-identical for margins 1e-5, 3e-6, 1.5e-6 and
+// 1e-6 (tools/margin_check.py), and the adversarial fixtures pass.
+#ifndef HQMQ_DELTA_TC
+#define HQMQ_DELTA_TC 3e-6f
+#endif
+constexpr float kDeltaTc = HQMQ_DELTA_TC;  // certification margin (split-fp16 rotation)
 
 __device__ __forceinline__ uint32_t tc_kmaj(int r, int k) {
   return (r >> 3) * kTcSBO + (k >> 3) * kTcLBO + (r & 7) * 16 + (k & 7) * 2;

@@ -291,6 +291,14 @@ def test_full_size_c3_unit(cuda, oracle):
     ref = _oracle_encode(oracle, x64, cfg, 3, "K")
     assert qt.n_payload == ref.payloads.shape[0]
     assert m.to_bytes(qt) == oracle.to_bytes(ref)
+    # decode reports index errors into the tensor's own error word: the
+    # code slots a flagged chunk skips must not raise a false CorruptData
+    want = m.decode_tensor(qt, bank, dtype=torch.float64)
+    for dt in (torch.float16, torch.float32):
+        got = m.decode_tensor(qt, bank, dtype=dt)
+        qt.synchronize()
+        rel = ((got.double() - want).abs() / (want.abs() + 1e-2)).max().item()
+        assert rel < (1e-2 if dt == torch.float16 else 1e-6), (dt, rel)
 
 
 @pytest.mark.parametrize("C", [None, 3.0])
@@ -313,6 +321,7 @@ def test_decode_token_ranges_fast_paths(cuda, C):
         for dt in (torch.float16, torch.bfloat16):
             got = m.decode_token_range(qt, bank, a, b, dtype=dt).double().cpu().numpy()
             assert np.max(np.abs(got - want) / (np.abs(want) + 1e-2)) < 1e-2, (a, b, dt)
+    qt.synchronize()  # no false index error from the range kernels
 
 
 def test_append_tokens_equals_full_encode(cuda):
