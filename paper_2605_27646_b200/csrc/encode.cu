@@ -56,9 +56,6 @@ __device__ __forceinline__ bool sqrt_gt(double s, double thr) {
 
 constexpr int kDigitBits = 13;
 constexpr int kBins = 1 << kDigitBits;  // 8192
-constexpr int kPasses = 5;              // lo bits: 50, 37, 24, 11, 0
-__host__ __device__ constexpr int digit_lo(int pass) { return pass < 4 ? 50 - 13 * pass : 0; }
-__host__ __device__ constexpr int digit_width(int pass) { return pass < 4 ? 13 : 11; }
 constexpr int kHistThreads = 256;
 
 struct RadixGroup {
@@ -66,6 +63,11 @@ struct RadixGroup {
   unsigned long long rank;
   double threshold;
   unsigned long long n;
+  // sampled-bracket median (median_sample_kernel / median_pass_kernel): the
+  // key range [a, b] holding the rank-th key, the elements below it counted
+  // by the current pass, histogram shift, mode (kModeHist / Compact / Done)
+  unsigned long long a, b, below;
+  int sh, mode;
 };
 
 struct EncParams {
@@ -622,7 +624,7 @@ __global__ void __launch_bounds__(kWThreads, kMinB) encode_warp_kernel(EncParams
         const double m = warp_max_nonneg_f64(fl ? 0.0 : sq[j]);
         sig_l = (lane % kWT) == j ? m : sig_l;
       }
-      sig_l = __dsqrt_rn(sig_l);
+      sig_l = __dsqrt_rn(lane < kWT ? sig_l : 1.0);  // (lanes >= kWT: off the slow path)
   #pragma unroll
       for (int j = 0; j < kWT; ++j) {
         const bool valid = j < ntok;
@@ -891,7 +893,7 @@ __global__ void __launch_bounds__(256, 4) encode_prep_kernel(EncParams p) {
       const double m = warp_max_nonneg_f64(sq[j]);
       sig_l = lane == j ? m : sig_l;
     }
-    sig_l = __dsqrt_rn(sig_l);
+    sig_l = __dsqrt_rn(lane < kT ? sig_l : 1.0);  // (lanes >= kT: off the slow path)
 #pragma unroll
     for (int j = 0; j < kT; ++j) {
       if (j >= ntok) break;  // warp-uniform
@@ -1251,49 +1253,20 @@ __global__ void __launch_bounds__(kTcThreads, kMinB) encode_tc_kernel(EncParams 
                  "n"(2 * kN));
 }
 
-// Coded-chunk count of every token and its exclusive prefix (token_offsets),
-// in ONE pass with a decoupled look-back across blocks: warp = 32 tokens
-// (one coalesced 256-byte load of a token's 32 squared norms per step, flags
-// by ballot), block = 256 tokens, block order from a ticket counter so every
-// predecessor is already running.  Status word per block: bits 62-63 = 1
-// (aggregate published) / 2 (inclusive prefix published), low bits the value.
-// The last block writes counters[0..1] (n_coded, n_payload).  Replaces the
-// per-token count kernel + cub scan + finalize of the first version.
 constexpr int kOffThreads = 256;
-__global__ void __launch_bounds__(kOffThreads) token_offsets_kernel(
-    const double* __restrict__ norms, const RadixGroup* groups, int64_t H, int64_t T, int64_t n_tok,
-    int per_head, unsigned long long* status, unsigned int* ticket, uint32_t* tokoff,
-    int64_t n_chunks, int64_t* counters) {
-  __shared__ uint32_t s_blk;
+// Exclusive scan of one count per thread (thread = token, block = kOffThreads
+// consecutive tokens taken in ticket order) chained across blocks by a
+// decoupled look-back; returns the thread's exclusive offset.  Status word per
+// block: bits 62-63 = 1 (aggregate published) / 2 (inclusive prefix
+// published), low bits the value.  The last block writes counters[0..1]
+// (n_coded, n_payload).
+__device__ __forceinline__ uint32_t scan_lookback(uint32_t mine, int64_t blk, int64_t n_tok,
+                                                  unsigned long long* status, int64_t n_chunks,
+                                                  int64_t* counters) {
   __shared__ uint32_t wsum[kOffThreads / 32];
   __shared__ unsigned long long s_prefix;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) s_blk = atomicAdd(ticket, 1u);
-  __syncthreads();
-  const int64_t blk = s_blk;
-  const int64_t tok0 = blk * kOffThreads + warp * 32;
-  // lane l ends up with the coded count of token tok0 + l; 8 tokens' norm rows
-  // in flight per step (coalesced 256-byte loads), flags by ballot
-  uint32_t mine = 0;
-  const double thr0 = groups[0].threshold;
-#pragma unroll
-  for (int j0 = 0; j0 < 32; j0 += 8) {
-    double v[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int64_t t = tok0 + j0 + k;
-      v[k] = t < n_tok ? __ldcs(norms + t * 32 + lane) : 0.0;
-    }
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const int64_t t = tok0 + j0 + k;
-      const double thr = per_head ? groups[(int)((t / T) % H)].threshold : thr0;
-      const bool fl = t < n_tok && sqrt_gt(v[k], thr);
-      const uint32_t m = __ballot_sync(0xffffffffu, fl);
-      if (lane == j0 + k && t < n_tok) mine = 32u - __popc(m);  // tokens past the end count 0
-    }
-  }
-  // block exclusive scan of the 256 counts
+  // block exclusive scan of the kOffThreads counts
   uint32_t incl = mine;
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
@@ -1342,27 +1315,64 @@ __global__ void __launch_bounds__(kOffThreads) token_offsets_kernel(
     }
   }
   __syncthreads();
-  const int64_t t = tok0 + lane;
-  if (t < n_tok) tokoff[t] = (uint32_t)(s_prefix + wbase + incl - mine);
+  return (uint32_t)(s_prefix + wbase + incl - mine);
 }
 
-// ------------------------------------------------------ Med3x radix select
+// Coded-chunk count of every token and its exclusive prefix (token_offsets),
+// in ONE pass: warp = 32 tokens (one coalesced 256-byte load of a token's 32
+// squared norms per step, flags by ballot), block = 256 tokens, then
+// scan_lookback.  Replaces the per-token count kernel + cub scan + finalize of
+// the first version; used where the fused prep below does not apply.
+__global__ void __launch_bounds__(kOffThreads) token_offsets_kernel(
+    const double* __restrict__ norms, const RadixGroup* groups, int64_t H, int64_t T, int64_t n_tok,
+    int per_head, unsigned long long* status, unsigned int* ticket, uint32_t* tokoff,
+    int64_t n_chunks, int64_t* counters) {
+  __shared__ uint32_t s_blk;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x == 0) s_blk = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const int64_t blk = s_blk;
+  const int64_t tok0 = blk * kOffThreads + warp * 32;
+  // lane l ends up with the coded count of token tok0 + l; 8 tokens' norm rows
+  // in flight per step (coalesced 256-byte loads), flags by ballot
+  uint32_t mine = 0;
+  const double thr0 = groups[0].threshold;
+#pragma unroll
+  for (int j0 = 0; j0 < 32; j0 += 8) {
+    double v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int64_t t = tok0 + j0 + k;
+      v[k] = t < n_tok ? __ldcs(norms + t * 32 + lane) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int64_t t = tok0 + j0 + k;
+      const double thr = per_head ? groups[(int)((t / T) % H)].threshold : thr0;
+      const bool fl = t < n_tok && sqrt_gt(v[k], thr);
+      const uint32_t m = __ballot_sync(0xffffffffu, fl);
+      if (lane == j0 + k && t < n_tok) mine = 32u - __popc(m);  // tokens past the end count 0
+    }
+  }
+  const uint32_t off = scan_lookback(mine, blk, n_tok, status, n_chunks, counters);
+  const int64_t t = tok0 + lane;
+  if (t < n_tok) tokoff[t] = off;
+}
+
+
+// ------------------------------------------------------ Med3x median
 // Exact lower median (rank (n-1)//2, outliers.py:50-55) of the fp64 chunk
 // norms of every pooling group.  The select runs on the squared norms s (the
 // reference's r = sqrt_rn(s) is monotone in s, so median(r) =
-// sqrt_rn(median(s)) and no per-chunk sqrt is needed): non-negative doubles
-// order like their uint64 bit patterns, so 5 histogram passes over
-// 13/13/13/13/11-bit digits of bits [62:0] pin the element.  Passes 0-2 stream
-// the whole call (pass 0 computes and stores s from the input); pass 2 also
-// compacts the elements still matching the 26-bit prefix into per-group
-// candidate lists, so passes 3-4 touch only those.  Each pass's last CTA
-// selects the digit; the threshold is C * sqrt_rn(median s).
+// sqrt_rn(median(s)) and no per-chunk sqrt is needed); non-negative doubles
+// order like their uint64 bit patterns (the keys).  The threshold is
+// C * sqrt_rn(median s).  Kernels: median_sample_kernel / median_pass_kernel
+// below.
 struct RadixParams {
   int64_t B, H, T, D;
   int C;
   int per_head;
   int aligned4;
-  int pass;
   double multiplier;
   const void* data;
   double* norms;
@@ -1373,145 +1383,424 @@ struct RadixParams {
   uint32_t* hist;  // [G][kBins]
   unsigned int* done;
   int G;
-  int norms_only;  // pass 0 stores the squared norms and builds no histogram (fixed thresholds)
   double* thr_out; // optional: the groups' thresholds (hqmq_encode_args.thresholds_out)
 };
 
-// Shared-memory histogram add.  (Pass 0's digits -- exponent + top mantissa
-// bits -- concentrate in a few bins, but aggregating equal bins across the
-// warp with __match_any_sync first measured 2-4% slower than plain atomics.)
-__device__ __forceinline__ void hist_add_sparse(uint32_t* hs, uint32_t bin, bool active) {
-  if (active) atomicAdd(hs + bin, 1u);
+// The 4 elements of one chunk as one vector load (head_dim % 4 == 0 with an
+// aligned base: chunk i of a row starts at element 4i -- no token / chunk split).
+template <typename InT> struct ChunkVec;
+template <> struct ChunkVec<__half> { typedef uint2 T; };
+template <> struct ChunkVec<__nv_bfloat16> { typedef uint2 T; };
+template <> struct ChunkVec<float> { typedef uint4 T; };
+struct alignas(16) Dbl4 { double v[4]; };
+template <> struct ChunkVec<double> { typedef Dbl4 T; };
+
+template <typename InT>
+__device__ __forceinline__ double chunk_vec_sq(const typename ChunkVec<InT>::T& raw) {
+  const InT* v = reinterpret_cast<const InT*>(&raw);
+  double x[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) x[k] = In<InT>::d(v[k]);
+  double sq = __dmul_rn(x[0], x[0]);
+  sq = __dadd_rn(sq, __dmul_rn(x[1], x[1]));
+  sq = __dadd_rn(sq, __dmul_rn(x[2], x[2]));
+  return __dadd_rn(sq, __dmul_rn(x[3], x[3]));
 }
 
-// Last block: pick, for every group, the bin holding rank k; narrow the prefix.
-__device__ void radix_select_last(RadixParams& p) {
-  const int lo = digit_lo(p.pass), width = digit_width(p.pass);
-  const int nb = 1 << width;
-  const int per = nb / kHistThreads;
-  typedef cub::BlockScan<uint32_t, kHistThreads> BS;
-  __shared__ typename BS::TempStorage scan_tmp;
-  for (int g = 0; g < p.G; ++g) {
-    uint32_t* hg = p.hist + (int64_t)g * kBins;
-    uint32_t sum = 0;
-    for (int i = 0; i < per; ++i) sum += __ldcg(hg + threadIdx.x * per + i);
-    const unsigned long long k = p.groups[g].rank;  // read before the scan's barriers
-    uint32_t excl;
-    BS(scan_tmp).ExclusiveSum(sum, excl);
-    if (excl <= k && k < (unsigned long long)excl + sum) {
-      unsigned long long acc = excl;
-      int bin = threadIdx.x * per;
-      for (;; ++bin) {
-        const uint32_t c = __ldcg(hg + bin);
-        if (acc + c > k) break;
-        acc += c;
-      }
-      p.groups[g].prefix |= ((unsigned long long)bin) << lo;
-      p.groups[g].rank = k - acc;
-      if (p.pass == kPasses - 1) {
-        const double med = __dsqrt_rn(__longlong_as_double((long long)p.groups[g].prefix));
-        p.groups[g].threshold = __dmul_rn(p.multiplier, med);
-      }
-    }
-    __syncthreads();
-    for (int i = threadIdx.x; i < kBins; i += kHistThreads) hg[i] = 0u;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) *p.done = 0u;
+// ------------------------------------------ Med3x median: sampled bracket
+// The exact lower median of every pooling group (rank k = (n-1)//2 of the
+// squared norms s; keys = their bit patterns, which order like the values) by
+// narrowing a key range [a, b] that holds rank k:
+//   median_sample_kernel: a strided sample of 512 keys per group (norms
+//     computed from the input), sorted in shared memory; [a, b] = the sample
+//     keys at ranks m/2 -+ 57 (5 sigma of the sample rank of the median;
+//     about 22% of the group's elements fall inside).  A group of <= 512
+//     chunks is its own sample: exact at once.
+//   median_pass_kernel (x3): one pass over the group's elements (the first
+//     computes and stores the norms from the input): elements below a are
+//     counted (ballots, no atomics), elements inside [a, b] go either to an
+//     8192-bin shared histogram of (key - a) >> sh, or -- once the range holds
+//     <= 1024 of them -- to a candidate list.  The last CTA narrows [a, b] to
+//     the bin holding rank k - below, or selects the exact key among the
+//     candidates.  A bracket that misses (rank k below a or above b) narrows
+//     to the side it missed; whatever is unresolved after the third pass is
+//     finished by that pass's last CTA alone (exact, slow, never seen on
+//     model-like data).
+// Only the ~22% of elements inside the bracket touch shared atomics (the fixed
+// 13-bit radix digits of the first version put every element of the first
+// pass into a handful of contended bins).
+constexpr int kSample = 512;
+constexpr int kSampleHalf = 57;
+constexpr int kSampleThreads = 256;
+constexpr int kCandMax = 1024;
+enum : int { kModeHist = 0, kModeCompact = 1, kModeDone = 2 };
+
+__device__ __forceinline__ int range_shift(unsigned long long w) {
+  const int bits = w ? 64 - __clzll((long long)w) : 0;
+  return bits > kDigitBits ? bits - kDigitBits : 0;
 }
 
 template <typename InT>
-__global__ void __launch_bounds__(kHistThreads) radix_hist_kernel(RadixParams p) {
-  __shared__ uint32_t hs[kBins];
-  __shared__ bool is_last;
-  for (int i = threadIdx.x; i < kBins; i += kHistThreads) hs[i] = 0u;
-  __syncthreads();
-  pdl_wait();  // (PDL) the previous pass's prefix / the input
-  pdl_trigger();
-  const int lo = digit_lo(p.pass), width = digit_width(p.pass);
-  const uint32_t dmask = (1u << width) - 1u;
-  const int hi_shift = lo + width;
-  const int lane = threadIdx.x & 31;
-  if (p.pass <= 2) {
-    // full pass: grid (bx, rows); the block strides over its row, kRB elements
-    // per thread per step with all loads issued before use (memory-level
-    // parallelism: the pass is a pure stream over 8 B/chunk)
-    constexpr int kRB = 8;
-    const int64_t row = blockIdx.y;
-    const int g = p.per_head ? (int)(row % p.H) : 0;
-    const int64_t L = p.T * p.C;
-    const unsigned long long pref = p.groups[g].prefix;
-    const InT* __restrict__ data = reinterpret_cast<const InT*>(p.data);
-    double* __restrict__ nrow = p.norms + row * L;
-    for (int64_t i0 = (int64_t)blockIdx.x * kHistThreads * kRB; i0 < L;
-         i0 += (int64_t)gridDim.x * kHistThreads * kRB) {
-      double rr[kRB];
-      if (p.pass == 0) {
-        InT v[kRB][4];
+__device__ __forceinline__ double chunk_sq(const InT* __restrict__ data, int64_t row, int64_t i,
+                                           const RadixParams& p) {
+  const int64_t t = i / p.C;
+  const int c = (int)(i - t * p.C);
+  InT v[4];
+  load_chunk(data + (row * p.T + t) * p.D, c, (int)p.D, p.aligned4 != 0, v);
+  double x[4];
 #pragma unroll
-        for (int j = 0; j < kRB; ++j) {
-          const int64_t i = i0 + j * kHistThreads + threadIdx.x;
-          if (i < L) {
-            const int64_t t = i / p.C;
-            const int c = (int)(i - t * p.C);
-            load_chunk(data + (row * p.T + t) * p.D, c, (int)p.D, p.aligned4 != 0, v[j]);
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < kRB; ++j) {
-          const int64_t i = i0 + j * kHistThreads + threadIdx.x;
-          rr[j] = 0.0;
-          if (i < L) {
-            double x[4];
-#pragma unroll
-            for (int k = 0; k < 4; ++k) x[k] = In<InT>::d(v[j][k]);
-            // the select runs on s = r^2: rank statistics commute with the
-            // monotone sqrt_rn, so median(r) = sqrt_rn(median(s)) exactly
-            double sq = __dmul_rn(x[0], x[0]);
-            sq = __dadd_rn(sq, __dmul_rn(x[1], x[1]));
-            sq = __dadd_rn(sq, __dmul_rn(x[2], x[2]));
-            rr[j] = __dadd_rn(sq, __dmul_rn(x[3], x[3]));
-            nrow[i] = rr[j];
-          }
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < kRB; ++j) {
-          const int64_t i = i0 + j * kHistThreads + threadIdx.x;
-          rr[j] = i < L ? __ldcs(nrow + i) : 0.0;
-        }
-      }
-#pragma unroll
-      if (p.norms_only) continue;
-      for (int j = 0; j < kRB; ++j) {
-        const int64_t i = i0 + j * kHistThreads + threadIdx.x;
-        const unsigned long long key = (unsigned long long)__double_as_longlong(rr[j]);
-        const bool active = i < L && (key >> hi_shift) == (pref >> hi_shift);
-        const uint32_t bin = (uint32_t)(key >> lo) & dmask;
-        if (p.pass == 2) {
-          // compact the survivors of the 26-bit prefix for passes 3-4
-          const unsigned m = __ballot_sync(0xffffffffu, active);
-          if (m) {
-            const int leader = __ffs(m) - 1;
-            unsigned int base = 0;
-            if (lane == leader) base = atomicAdd(p.cand_n + g, (unsigned)__popc(m));
-            base = __shfl_sync(0xffffffffu, base, leader);
-            if (active)
-              p.cand[(unsigned long long)g * p.n_per_group + base +
-                     __popc(m & ((1u << lane) - 1u))] = rr[j];
-          }
-        } else {
-          hist_add_sparse(hs, bin, active);
+  for (int k = 0; k < 4; ++k) x[k] = In<InT>::d(v[k]);
+  double sq = __dmul_rn(x[0], x[0]);
+  sq = __dadd_rn(sq, __dmul_rn(x[1], x[1]));
+  sq = __dadd_rn(sq, __dmul_rn(x[2], x[2]));
+  return __dadd_rn(sq, __dmul_rn(x[3], x[3]));
+}
+
+__device__ __forceinline__ void median_done(RadixParams& p, int g, unsigned long long key) {
+  RadixGroup& G = p.groups[g];
+  G.prefix = key;
+  G.mode = kModeDone;
+  const double thr = __dmul_rn(p.multiplier, __dsqrt_rn(__longlong_as_double((long long)key)));
+  G.threshold = thr;
+  if (p.thr_out) p.thr_out[g] = thr;
+}
+
+template <typename InT>
+__global__ void __launch_bounds__(kSampleThreads) median_sample_kernel(RadixParams p, unsigned long long* status,
+                                                             int64_t n_status) {
+  __shared__ unsigned long long sk[kSample];
+  const int g = blockIdx.x, tid = threadIdx.x;
+  // (the token-offset scan's status words and this group's histogram start at 0)
+  for (int64_t i = (int64_t)g * kSampleThreads + tid; i < n_status; i += (int64_t)gridDim.x * kSampleThreads)
+    status[i] = 0ull;
+  for (int i = tid; i < kBins; i += kSampleThreads) p.hist[(int64_t)g * kBins + i] = 0u;
+  const InT* __restrict__ data = reinterpret_cast<const InT*>(p.data);
+  const int64_t L = p.T * p.C;
+  const unsigned long long n = p.n_per_group;
+  const int m = (int)(n < (unsigned long long)kSample ? n : (unsigned long long)kSample);
+  for (int i = tid; i < kSample; i += kSampleThreads) {
+    unsigned long long key = ~0ull;  // padding sorts last
+    if (i < m) {
+      const unsigned long long e = (unsigned long long)i * n / (unsigned long long)m;
+      const int64_t b = (int64_t)(e / (unsigned long long)L), kk = (int64_t)e - b * L;
+      const int64_t row = p.per_head ? b * p.H + g : b;
+      key = (unsigned long long)__double_as_longlong(chunk_sq(data, row, kk, p));
+    }
+    sk[i] = key;
+  }
+  // bitonic sort, ascending
+  for (int size = 2; size <= kSample; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      __syncthreads();
+      for (int i = tid; i < kSample / 2; i += kSampleThreads) {
+        const int lo = 2 * i - (i & (stride - 1)), hi = lo + stride;
+        const unsigned long long x = sk[lo], y = sk[hi];
+        if ((x > y) == ((lo & size) == 0)) {
+          sk[lo] = y;
+          sk[hi] = x;
         }
       }
     }
   }
-  if (p.pass == 2 || p.norms_only) return;  // compaction only / norms only
   __syncthreads();
-  const int g = p.per_head ? (int)(blockIdx.y % p.H) : 0;
+  if (tid == 0) {
+    RadixGroup& G = p.groups[g];
+    const unsigned long long k = (n - 1) / 2;
+    G.rank = k;
+    G.n = n;
+    G.below = 0ull;
+    G.prefix = 0ull;
+    G.threshold = 0.0;
+    p.cand_n[g] = 0u;
+    if ((unsigned long long)m == n) {
+      median_done(p, g, sk[k]);
+    } else {
+      const int lo = max(0, m / 2 - kSampleHalf), hi = min(m - 1, m / 2 + kSampleHalf);
+      G.a = sk[lo];
+      G.b = sk[hi];
+      G.sh = range_shift(G.b - G.a);
+      G.mode = kModeHist;
+    }
+  }
+}
+
+// One narrowing step of group g from its counts (hist[g], G.below, the
+// candidate list), run by one CTA (all threads).
+__device__ void median_step(RadixParams& p, int g, unsigned long long* scratch) {
+  __shared__ unsigned long long s_a, s_b, s_res;
+  __shared__ int s_found;
+  __shared__ uint32_t s_cnt;
+  RadixGroup& G = p.groups[g];
+  const int mode = G.mode;
+  if (mode == kModeDone) return;
+  const long long r = (long long)G.rank - (long long)G.below;  // rank inside [a, b]
+  const unsigned long long a = G.a, b = G.b;
+  const int nt = blockDim.x, tid = threadIdx.x;
   uint32_t* hg = p.hist + (int64_t)g * kBins;
-  for (int i = threadIdx.x; i < kBins; i += kHistThreads)
-    if (hs[i]) atomicAdd(hg + i, hs[i]);
+  if (tid == 0) s_found = 0;
+  __syncthreads();
+  if (mode == kModeHist) {
+    // bins are scanned in thread order: thread t owns bins [t*kPer, (t+1)*kPer),
+    // held in registers (one round of independent loads, no serial re-reads)
+    constexpr int kPer = kBins / kHistThreads;
+    uint32_t hv[kPer];
+    uint32_t sum = 0;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+      hv[i] = __ldcg(hg + tid * kPer + i);
+      sum += hv[i];
+    }
+    typedef cub::BlockScan<uint32_t, kHistThreads> BS;
+    __shared__ typename BS::TempStorage scan_tmp;
+    uint32_t excl, total;
+    BS(scan_tmp).ExclusiveSum(sum, excl, total);
+    if (tid == 0) {
+      // a bracket that missed narrows to the side it missed
+      if (r < 0) { s_a = 0ull; s_b = a - 1ull; s_cnt = 0xffffffffu; s_found = 1; }
+      else if (r >= (long long)total) {
+        s_a = b + 1ull; s_b = 0x7fffffffffffffffull; s_cnt = 0xffffffffu; s_found = 1;
+      }
+    }
+    __syncthreads();
+    if (!s_found && (long long)excl <= r && r < (long long)excl + (long long)sum) {
+      long long acc = excl;
+      int bin = tid * kPer;
+      uint32_t cnt = 0;
+#pragma unroll
+      for (int i = 0; i < kPer; ++i) {
+        if (acc >= 0 && acc + (long long)hv[i] > r) {
+          bin = tid * kPer + i;
+          cnt = hv[i];
+          acc = -1;  // found
+        } else if (acc >= 0) {
+          acc += hv[i];
+        }
+      }
+      s_cnt = cnt;
+      const unsigned long long na = a + ((unsigned long long)bin << G.sh);
+      const unsigned long long span = (1ull << G.sh) - 1ull;
+      s_a = na;
+      s_b = (b - na < span) ? b : na + span;
+     
+      s_found = 1;
+    }
+    __syncthreads();
+    for (int i = tid; i < kBins; i += nt) hg[i] = 0u;
+    if (tid == 0) {
+      if (s_a == s_b) {
+        median_done(p, g, s_a);
+      } else {
+        G.a = s_a;
+        G.b = s_b;
+        G.sh = range_shift(s_b - s_a);
+        G.mode = s_cnt <= (uint32_t)kCandMax ? kModeCompact : kModeHist;
+      }
+      G.below = 0ull;
+      p.cand_n[g] = 0u;
+    }
+  } else {
+    // exact select among the <= kCandMax candidates (all inside [a, b]):
+    // a 256-bin shared histogram of (key - a) >> sh2 picks the bin holding
+    // rank r, then the bin's few keys are ranked by counting
+    unsigned long long* sc = scratch;              // [kCandMax] (the caller's histogram space)
+    unsigned long long* sbin = scratch + kCandMax;  // [kCandMax]
+    __shared__ uint32_t h2[256];
+    __shared__ uint32_t s_nb, s_bin;
+    __shared__ long long s_rr;
+    const unsigned int n_all = p.cand_n[g];
+    const unsigned int n = min(n_all, (unsigned int)kCandMax);
+    const double* cg = p.cand + (unsigned long long)g * p.n_per_group;
+    const unsigned long long w = b - a;
+    const int sh2 = (w ? 64 - __clzll((long long)w) : 0) > 8 ? (64 - __clzll((long long)w)) - 8 : 0;
+    for (int i = tid; i < 256; i += nt) h2[i] = 0u;
+    if (tid == 0) { s_res = ~0ull; s_nb = 0u; s_bin = 0xffffffffu; s_rr = 0; }
+    __syncthreads();
+    for (unsigned int i = tid; i < n; i += nt) {
+      const unsigned long long key = (unsigned long long)__double_as_longlong(__ldcg(cg + i));
+      sc[i] = key;
+      if (key >= a && key <= b) atomicAdd(h2 + (uint32_t)((key - a) >> sh2), 1u);
+    }
+    __syncthreads();
+    {
+      typedef cub::BlockScan<uint32_t, kHistThreads> BS2;
+      __shared__ typename BS2::TempStorage scan2;
+      const uint32_t c = tid < 256 ? h2[tid] : 0u;
+      uint32_t excl;
+      BS2(scan2).ExclusiveSum(c, excl);
+      if (tid < 256 && (long long)excl <= r && r < (long long)excl + (long long)c) {
+        s_bin = (uint32_t)tid;
+        s_rr = r - (long long)excl;
+      }
+    }
+    __syncthreads();
+    for (unsigned int i = tid; i < n; i += nt) {
+      const unsigned long long key = sc[i];
+      if (s_bin != 0xffffffffu && key >= a && key <= b && (uint32_t)((key - a) >> sh2) == s_bin)
+        sbin[atomicAdd(&s_nb, 1u)] = key;
+    }
+    __syncthreads();
+    for (unsigned int i = tid; i < s_nb; i += nt) {
+      const unsigned long long ki = sbin[i];
+      unsigned int lt = 0, le = 0;
+      for (unsigned int j = 0; j < s_nb; ++j) {
+        lt += sbin[j] < ki;
+        le += sbin[j] <= ki;
+      }
+      if ((long long)lt <= s_rr && s_rr < (long long)le) s_res = ki;  // (equal keys write the same)
+    }
+    __syncthreads();
+    if (tid == 0) {
+      if (s_res != ~0ull && n_all <= (unsigned int)kCandMax) {
+        median_done(p, g, s_res);
+      } else {  // (not reachable from a consistent count) histogram the range again
+        G.sh = range_shift(b - a);
+        G.mode = kModeHist;
+      }
+      G.below = 0ull;
+      p.cand_n[g] = 0u;
+    }
+  }
+  __syncthreads();
+}
+
+// Count / histogram / compact one element (pass body shared by the grid pass
+// and the single-CTA finish).
+__device__ __forceinline__ void median_visit(RadixParams& p, int g, int mode, unsigned long long a,
+                                             unsigned long long b, int sh, uint32_t* hs,
+                                             bool valid, double s, unsigned int& below) {
+  const unsigned long long key = (unsigned long long)__double_as_longlong(s);
+  below += (valid && key < a) ? 1u : 0u;
+  const bool in = valid && key >= a && key <= b;
+  if (mode == kModeHist) {
+    if (in) atomicAdd(hs + ((key - a) >> sh), 1u);
+  } else {
+    const unsigned m = __ballot_sync(0xffffffffu, in);
+    if (m) {
+      const int lane = threadIdx.x & 31, leader = __ffs(m) - 1;
+      unsigned int base = 0;
+      if (lane == leader) base = atomicAdd(p.cand_n + g, (unsigned)__popc(m));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      const unsigned int at = base + __popc(m & ((1u << lane) - 1u));
+      if (in && at < (unsigned int)kCandMax) p.cand[(unsigned long long)g * p.n_per_group + at] = s;
+    }
+  }
+}
+
+__device__ __forceinline__ unsigned long long block_sum_u64(unsigned long long v) {
+  __shared__ unsigned long long ws[32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if (lane == 0) ws[warp] = v;
+  __syncthreads();
+  unsigned long long t = 0;
+  for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += ws[w];
+  return t;
+}
+
+// Unresolved after the last pass: this CTA alone repeats passes over group g
+// (hist into the global histogram, compaction into the candidate list).
+__device__ void median_finish(RadixParams& p, int g, unsigned long long* scratch) {
+  const int64_t L = p.T * p.C;
+  const int64_t nrows = p.per_head ? p.B : p.B * p.H;
+  for (int it = 0; it < 16 && p.groups[g].mode != kModeDone; ++it) {
+    __syncthreads();
+    const RadixGroup G = p.groups[g];
+    unsigned int below = 0;
+    uint32_t* hg = p.hist + (int64_t)g * kBins;
+    for (int64_t rr = 0; rr < nrows; ++rr) {
+      const int64_t row = p.per_head ? rr * p.H + g : rr;
+      const double* nrow = p.norms + row * L;
+      for (int64_t i0 = 0; i0 < L; i0 += blockDim.x) {
+        const int64_t i = i0 + threadIdx.x;
+        const bool valid = i < L;
+        median_visit(p, g, G.mode, G.a, G.b, G.sh, hg, valid, valid ? __ldcg(nrow + i) : 0.0, below);
+      }
+    }
+    const unsigned long long tb = block_sum_u64(below);
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) p.groups[g].below = tb;
+    __syncthreads();
+    median_step(p, g, scratch);
+  }
+}
+
+template <typename InT, bool kInput>
+__global__ void __launch_bounds__(kHistThreads) median_pass_kernel(RadixParams p, int last) {
+  __shared__ __align__(16) uint32_t hs[kBins];
+  static_assert(kBins * 4 >= 2 * kCandMax * 8, "median_step scratch");
+  __shared__ bool is_last;
+  if (!kInput && p.done[2]) return;  // every group resolved
+  const int64_t row = blockIdx.y;
+  const int g = p.per_head ? (int)(row % p.H) : 0;
+  const int mode = p.groups[g].mode;
+  const unsigned long long a = p.groups[g].a, b = p.groups[g].b;
+  const int sh = p.groups[g].sh;
+  const bool active = mode != kModeDone;
+  if (active && mode == kModeHist)
+    for (int i = threadIdx.x; i < kBins; i += kHistThreads) hs[i] = 0u;
+  __syncthreads();
+  constexpr int kRB = kInput ? 8 : 16;  // (norm-only passes: more loads in flight)
+  const int64_t L = p.T * p.C;
+  const bool flat = p.D == 4 * p.C && p.aligned4;
+  const InT* __restrict__ data = reinterpret_cast<const InT*>(p.data);
+  double* __restrict__ nrow = p.norms + row * L;
+  unsigned int below = 0;
+  for (int64_t i0 = (int64_t)blockIdx.x * kHistThreads * kRB; i0 < L;
+       i0 += (int64_t)gridDim.x * kHistThreads * kRB) {
+    double rr[kRB];
+    if (kInput && flat) {
+      typedef typename ChunkVec<InT>::T V;
+      const V* __restrict__ rowv = reinterpret_cast<const V*>(data + row * p.T * p.D);
+      V raw[kRB];
+#pragma unroll
+      for (int j = 0; j < kRB; ++j) {
+        const int64_t i = i0 + j * kHistThreads + threadIdx.x;
+        if (i < L) raw[j] = rowv[i];
+      }
+#pragma unroll
+      for (int j = 0; j < kRB; ++j) {
+        const int64_t i = i0 + j * kHistThreads + threadIdx.x;
+        rr[j] = 0.0;
+        if (i < L) {
+          rr[j] = chunk_vec_sq<InT>(raw[j]);
+          nrow[i] = rr[j];
+        }
+      }
+    } else if constexpr (kInput) {  // head_dim % 4 != 0 (zero-padded last chunk)
+#pragma unroll
+      for (int j = 0; j < kRB; ++j) {
+        const int64_t i = i0 + j * kHistThreads + threadIdx.x;
+        rr[j] = 0.0;
+        if (i < L) {
+          rr[j] = chunk_sq(data, row, i, p);
+          nrow[i] = rr[j];
+        }
+      }
+    } else {
+      if (!active) break;
+#pragma unroll
+      for (int j = 0; j < kRB; ++j) {
+        const int64_t i = i0 + j * kHistThreads + threadIdx.x;
+        rr[j] = i < L ? __ldcg(nrow + i) : 0.0;
+      }
+    }
+    if (!active) continue;
+#pragma unroll
+    for (int j = 0; j < kRB; ++j)
+      median_visit(p, g, mode, a, b, sh, hs, i0 + j * kHistThreads + threadIdx.x < L, rr[j], below);
+  }
+  const unsigned long long tb = block_sum_u64(below);
+  if (active) {
+    if (threadIdx.x == 0 && tb) atomicAdd(&p.groups[g].below, tb);
+    if (mode == kModeHist) {
+      uint32_t* hg = p.hist + (int64_t)g * kBins;
+      for (int i = threadIdx.x; i < kBins; i += kHistThreads)
+        if (hs[i]) atomicAdd(hg + i, hs[i]);
+    }
+  }
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -1519,67 +1808,18 @@ __global__ void __launch_bounds__(kHistThreads) radix_hist_kernel(RadixParams p)
     is_last = atomicAdd(p.done, 1u) == total - 1;
   }
   __syncthreads();
-  if (is_last) {
-    __threadfence();
-    radix_select_last(p);
-  }
-}
-
-// Digits 2..4 of every group's select over its compacted candidates (the
-// elements matching the 26-bit prefix of passes 0-1), one CTA per group with
-// shared-memory histograms; sets the group's threshold C * median.
-constexpr int kTailThreads = 1024;
-__global__ void __launch_bounds__(kTailThreads) radix_tail_kernel(RadixParams p) {
-  __shared__ uint32_t hs[kBins];
-  __shared__ unsigned long long s_pref, s_rank;
-  pdl_wait();
-  pdl_trigger();
-  const int g = blockIdx.x;
-  const unsigned int n = p.cand_n[g];
-  const double* __restrict__ cg = p.cand + (unsigned long long)g * p.n_per_group;
+  if (!is_last) return;
+  __threadfence();
+  __syncthreads();
+  unsigned long long* scratch = reinterpret_cast<unsigned long long*>(hs);  // (16 KB of it)
+  for (int gg = 0; gg < p.G; ++gg) median_step(p, gg, scratch);
+  if (last)
+    for (int gg = 0; gg < p.G; ++gg) median_finish(p, gg, scratch);
   if (threadIdx.x == 0) {
-    s_pref = p.groups[g].prefix;
-    s_rank = p.groups[g].rank;
-  }
-  for (int pass = 2; pass < kPasses; ++pass) {
-    const int lo = digit_lo(pass), width = digit_width(pass);
-    const uint32_t dmask = (1u << width) - 1u;
-    const int hi_shift = lo + width;
-    for (int i = threadIdx.x; i < kBins; i += kTailThreads) hs[i] = 0u;
-    __syncthreads();
-    const unsigned long long pref = s_pref;
-    for (unsigned int i = threadIdx.x; i < n; i += kTailThreads) {
-      const unsigned long long key = (unsigned long long)__double_as_longlong(cg[i]);
-      if ((key >> hi_shift) == (pref >> hi_shift)) atomicAdd(hs + ((uint32_t)(key >> lo) & dmask), 1u);
-    }
-    __syncthreads();
-    const int per = kBins / kTailThreads;  // 8 bins per thread
-    uint32_t sum = 0;
-    for (int i = 0; i < per; ++i) sum += hs[threadIdx.x * per + i];
-    typedef cub::BlockScan<uint32_t, kTailThreads> BS;
-    __shared__ typename BS::TempStorage scan_tmp;
-    uint32_t excl;
-    BS(scan_tmp).ExclusiveSum(sum, excl);
-    const unsigned long long k = s_rank;
-    __syncthreads();
-    if (excl <= k && k < (unsigned long long)excl + sum) {
-      unsigned long long acc = excl;
-      int bin = threadIdx.x * per;
-      for (;; ++bin) {
-        if (acc + hs[bin] > k) break;
-        acc += hs[bin];
-      }
-      s_pref = pref | (((unsigned long long)bin) << lo);
-      s_rank = k - acc;
-    }
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    p.groups[g].prefix = s_pref;
-    p.groups[g].rank = s_rank;
-    const double thr = __dmul_rn(p.multiplier, __dsqrt_rn(__longlong_as_double((long long)s_pref)));
-    p.groups[g].threshold = thr;
-    if (p.thr_out) p.thr_out[g] = thr;
+    int all = 1;
+    for (int gg = 0; gg < p.G; ++gg) all &= p.groups[gg].mode == kModeDone;
+    p.done[2] = (unsigned int)all;
+    p.done[0] = 0u;
   }
 }
 
@@ -1588,7 +1828,10 @@ __global__ void set_thresholds_kernel(RadixGroup* groups, const double* fixed, i
   pdl_wait();
   pdl_trigger();
   const int g = blockIdx.x * blockDim.x + threadIdx.x;
-  if (g < G) groups[g].threshold = fixed[g];
+  if (g < G) {
+    groups[g].threshold = fixed[g];
+    groups[g].mode = kModeDone;  // (the norms pass then stores the norms only)
+  }
 }
 __global__ void copy_thresholds_kernel(const RadixGroup* groups, double* out, int G) {
   pdl_wait();
@@ -1747,23 +1990,27 @@ int launch_encode(const hqmq_encode_args* a, const Layout& L, cudaStream_t st) {
   }
   RadixGroup* groups = nullptr;
   uint32_t* prefix = nullptr;
+  const int64_t n_tok_all = L.rows * a->tokens;
+  const int64_t n_status = L.warp_path ? ceil_div(n_tok_all, kOffThreads) : 0;
+  unsigned long long* status = reinterpret_cast<unsigned long long*>(ws + L.off_prefix);
+  unsigned int* ticket = nullptr;
   if (ext) {
     groups = reinterpret_cast<RadixGroup*>(ws + L.off_groups);
     uint32_t* hist = reinterpret_cast<uint32_t*>(ws + L.off_hist);
     unsigned int* done = reinterpret_cast<unsigned int*>(ws + L.off_done);
-    cudaMemsetAsync(hist, 0, (size_t)L.G * kBins * 4, st);
+    const bool frozen = a->fixed_thresholds != nullptr;
     cudaMemsetAsync(done, 0, 16, st);
     const unsigned long long n_per_group =
         (unsigned long long)(L.n_chunks / (a->per_head_pooling ? a->heads : 1));
     unsigned int* cand_n = reinterpret_cast<unsigned int*>(ws + L.off_cand_n);
     // warp path: the single-pass token-offset scan's block status words
     // (in the tile-prefix region) and its block ticket (done[1]) start at 0
-    const int64_t n_tok_all = L.rows * a->tokens;
-    const int64_t n_status = L.warp_path ? ceil_div(n_tok_all, kOffThreads) : 0;
-    unsigned long long* status = reinterpret_cast<unsigned long long*>(ws + L.off_prefix);
-    const int64_t n_init = std::max<int64_t>(L.G, n_status);
-    radix_init_kernel<<<(unsigned)ceil_div(n_init, 128), 128, 0, st>>>(
-        groups, cand_n, L.G, n_per_group, L.warp_path ? status : nullptr, n_status, nullptr);
+    ticket = done + 1;
+    if (frozen) {  // (the median path's sample kernel initialises groups and status itself)
+      const int64_t n_init = std::max<int64_t>(L.G, n_status);
+      radix_init_kernel<<<(unsigned)ceil_div(n_init, 128), 128, 0, st>>>(
+          groups, cand_n, L.G, n_per_group, L.warp_path ? status : nullptr, n_status, nullptr);
+    }
     RadixParams rp;
     rp.B = a->batch; rp.H = a->heads; rp.T = a->tokens; rp.D = a->head_dim; rp.C = L.C;
     rp.per_head = a->per_head_pooling; rp.aligned4 = aligned4; rp.multiplier = a->outlier_multiplier;
@@ -1776,20 +2023,19 @@ int launch_encode(const hqmq_encode_args* a, const Layout& L, cudaStream_t st) {
     const int64_t bx_full = std::max<int64_t>(
         1, std::min<int64_t>(ceil_div((int64_t)148 * 4, L.rows), ceil_div(row_chunks, kHistThreads * 8)));
 
-    rp.norms_only = a->fixed_thresholds != nullptr;
     rp.thr_out = a->thresholds_out;
-    if (rp.norms_only) {  // frozen thresholds: the norms pass only
-      rp.pass = 0;
-      radix_hist_kernel<InT><<<dim3((unsigned)bx_full, (unsigned)L.rows), kHistThreads, 0, st>>>(rp);
+    if (frozen) {  // frozen thresholds: the norms pass only
       set_thresholds_kernel<<<(L.G + 127) / 128, 128, 0, st>>>(groups, a->fixed_thresholds, L.G);
+      median_pass_kernel<InT, true><<<dim3((unsigned)bx_full, (unsigned)L.rows), kHistThreads, 0, st>>>(rp, 0);
       if (a->thresholds_out)
         copy_thresholds_kernel<<<(L.G + 127) / 128, 128, 0, st>>>(groups, a->thresholds_out, L.G);
-    } else {
-      for (int pass = 0; pass <= 2; ++pass) {
-        rp.pass = pass;
-        radix_hist_kernel<InT><<<dim3((unsigned)bx_full, (unsigned)L.rows), kHistThreads, 0, st>>>(rp);
-      }
-      radix_tail_kernel<<<L.G, kTailThreads, 0, st>>>(rp);  // also writes thresholds_out
+    } else {  // exact median: sampled bracket + 3 narrowing passes (the first stores the norms)
+      median_sample_kernel<InT><<<L.G, kSampleThreads, 0, st>>>(rp, L.warp_path ? status : nullptr,
+                                                                  L.warp_path ? n_status : 0);
+      const dim3 grid((unsigned)bx_full, (unsigned)L.rows);
+      median_pass_kernel<InT, true><<<grid, kHistThreads, 0, st>>>(rp, 0);
+      median_pass_kernel<InT, false><<<grid, kHistThreads, 0, st>>>(rp, 0);
+      median_pass_kernel<InT, false><<<grid, kHistThreads, 0, st>>>(rp, 1);
     }
     uint32_t* counts = reinterpret_cast<uint32_t*>(ws + L.off_counts);
     size_t cub_bytes = L.cub_bytes;

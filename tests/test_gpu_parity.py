@@ -301,6 +301,56 @@ def test_full_size_c3_unit(cuda, oracle):
         assert rel < (1e-2 if dt == torch.float16 else 1e-6), (dt, rel)
 
 
+def _median_sample_positions(n, m=8192):
+    """Chunk indices (within a pooling group) of the encode's strided median
+    sample (encode.cu median_sample_kernel: e_i = i * n // m)."""
+    m = min(m, n)
+    return (np.arange(m, dtype=np.uint64) * np.uint64(n)) // np.uint64(m)
+
+
+@pytest.mark.parametrize("case", ["sample_high", "sample_low", "per_head_high", "ties", "two_values"])
+def test_median_bracket_adversarial(cuda, oracle, case):
+    """The sampled-bracket Med3x median (encode.cu median_sample_kernel /
+    median_pass_kernel) on inputs built against it: the chunks the strided
+    sample reads scaled x40 (the bracket misses low: the narrowing passes and
+    the last pass's single-CTA finish take over) or x1/40 (misses high),
+    per-head pooling, all norms equal, two distinct norms -- exact against the
+    oracle (outliers.py:50-55 lower median, strict r > C*median)."""
+    m = hq()
+    B, H, T, D = 1, 2, 512, 128  # 32768 chunks per call: the sample is a quarter
+    C = D // 4
+    L = T * C
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal((B, H, T, D))
+    pooling = "per_head" if case == "per_head_high" else "batch"
+    if case in ("sample_high", "sample_low", "per_head_high"):
+        scale = 1.0 / 40.0 if case == "sample_low" else 40.0
+        if pooling == "batch":
+            for e in _median_sample_positions(B * H * L):
+                row, k = divmod(int(e), L)
+                t, c = divmod(k, C)
+                x[row // H, row % H, t, 4 * c:4 * c + 4] *= scale
+        else:
+            for g in range(H):
+                for e in _median_sample_positions(B * L):
+                    b, k = divmod(int(e), L)
+                    t, c = divmod(k, C)
+                    x[b, g, t, 4 * c:4 * c + 4] *= scale
+    elif case == "ties":
+        x[:] = np.tile(rng.standard_normal(4), D // 4)
+    else:  # two_values: every other token zero
+        x[:] = np.tile(rng.standard_normal(4), D // 4)
+        x[:, :, ::2] = 0.0
+    xt = torch.from_numpy(x.astype(np.float16)).to(cuda)
+    x64 = xt.double().cpu().numpy()
+    cfg = m.CodecConfig(codebook_size=64, radius_bits=6, outlier_multiplier=3.0, median_pooling=pooling)
+    bank = m.CodebookBank(0, 64)
+    qt = m.encode_tensor(xt, cfg, layer=5, role="K", bank=bank)
+    ref = _oracle_encode(oracle, x64, cfg, 5, "K")
+    assert qt.n_payload == ref.payloads.shape[0], (qt.n_payload, ref.payloads.shape[0])
+    assert m.to_bytes(qt) == oracle.to_bytes(ref)
+
+
 @pytest.mark.parametrize("C", [None, 3.0])
 def test_decode_token_ranges_fast_paths(cuda, C):
     """Token-range decode through the TMA fast paths (head_dim 128, 8-aligned
