@@ -1432,12 +1432,14 @@ __device__ __forceinline__ double chunk_vec_sq(const typename ChunkVec<InT>::T& 
 constexpr int kSample = 512;
 constexpr int kSampleHalf = 57;
 constexpr int kSampleThreads = 256;
-constexpr int kCandMax = 1024;
+constexpr int kCandMax = 4096;   // compaction threshold (candidates per group)
+constexpr int kBinMax = 1024;    // keys of one select bin held in shared memory
+constexpr int kFirstBits = 10;   // the first pass's histogram: 1024 bins (fewer global merges)
 enum : int { kModeHist = 0, kModeCompact = 1, kModeDone = 2 };
 
-__device__ __forceinline__ int range_shift(unsigned long long w) {
+__device__ __forceinline__ int range_shift(unsigned long long w, int bins_log2 = kDigitBits) {
   const int bits = w ? 64 - __clzll((long long)w) : 0;
-  return bits > kDigitBits ? bits - kDigitBits : 0;
+  return bits > bins_log2 ? bits - bins_log2 : 0;
 }
 
 template <typename InT>
@@ -1518,7 +1520,7 @@ __global__ void __launch_bounds__(kSampleThreads) median_sample_kernel(RadixPara
       const int lo = max(0, m / 2 - kSampleHalf), hi = min(m - 1, m / 2 + kSampleHalf);
       G.a = sk[lo];
       G.b = sk[hi];
-      G.sh = range_shift(G.b - G.a);
+      G.sh = range_shift(G.b - G.a, kFirstBits);
       G.mode = kModeHist;
     }
   }
@@ -1599,25 +1601,23 @@ __device__ void median_step(RadixParams& p, int g, unsigned long long* scratch) 
       p.cand_n[g] = 0u;
     }
   } else {
-    // exact select among the <= kCandMax candidates (all inside [a, b]):
-    // a 256-bin shared histogram of (key - a) >> sh2 picks the bin holding
-    // rank r, then the bin's few keys are ranked by counting
-    unsigned long long* sc = scratch;              // [kCandMax] (the caller's histogram space)
-    unsigned long long* sbin = scratch + kCandMax;  // [kCandMax]
+    // exact select among the <= kCandMax candidates (all inside [a, b]),
+    // streamed from the list twice: a 256-bin shared histogram of
+    // (key - a) >> sh2 picks the bin holding rank r, then that bin's keys
+    // (<= kBinMax, else the range narrows to the bin) are ranked by counting
+    unsigned long long* sbin = scratch;  // [kBinMax] (the caller's histogram space)
     __shared__ uint32_t h2[256];
     __shared__ uint32_t s_nb, s_bin;
     __shared__ long long s_rr;
     const unsigned int n_all = p.cand_n[g];
     const unsigned int n = min(n_all, (unsigned int)kCandMax);
     const double* cg = p.cand + (unsigned long long)g * p.n_per_group;
-    const unsigned long long w = b - a;
-    const int sh2 = (w ? 64 - __clzll((long long)w) : 0) > 8 ? (64 - __clzll((long long)w)) - 8 : 0;
+    const int sh2 = range_shift(b - a, 8);
     for (int i = tid; i < 256; i += nt) h2[i] = 0u;
     if (tid == 0) { s_res = ~0ull; s_nb = 0u; s_bin = 0xffffffffu; s_rr = 0; }
     __syncthreads();
     for (unsigned int i = tid; i < n; i += nt) {
       const unsigned long long key = (unsigned long long)__double_as_longlong(__ldcg(cg + i));
-      sc[i] = key;
       if (key >= a && key <= b) atomicAdd(h2 + (uint32_t)((key - a) >> sh2), 1u);
     }
     __syncthreads();
@@ -1633,27 +1633,35 @@ __device__ void median_step(RadixParams& p, int g, unsigned long long* scratch) 
       }
     }
     __syncthreads();
-    for (unsigned int i = tid; i < n; i += nt) {
-      const unsigned long long key = sc[i];
-      if (s_bin != 0xffffffffu && key >= a && key <= b && (uint32_t)((key - a) >> sh2) == s_bin)
-        sbin[atomicAdd(&s_nb, 1u)] = key;
-    }
-    __syncthreads();
-    for (unsigned int i = tid; i < s_nb; i += nt) {
-      const unsigned long long ki = sbin[i];
-      unsigned int lt = 0, le = 0;
-      for (unsigned int j = 0; j < s_nb; ++j) {
-        lt += sbin[j] < ki;
-        le += sbin[j] <= ki;
+    if (s_bin != 0xffffffffu && h2[s_bin] <= (uint32_t)kBinMax) {
+      for (unsigned int i = tid; i < n; i += nt) {
+        const unsigned long long key = (unsigned long long)__double_as_longlong(__ldcg(cg + i));
+        if (key >= a && key <= b && (uint32_t)((key - a) >> sh2) == s_bin) sbin[atomicAdd(&s_nb, 1u)] = key;
       }
-      if ((long long)lt <= s_rr && s_rr < (long long)le) s_res = ki;  // (equal keys write the same)
+      __syncthreads();
+      for (unsigned int i = tid; i < s_nb; i += nt) {
+        const unsigned long long ki = sbin[i];
+        unsigned int lt = 0, le = 0;
+        for (unsigned int j = 0; j < s_nb; ++j) {
+          lt += sbin[j] < ki;
+          le += sbin[j] <= ki;
+        }
+        if ((long long)lt <= s_rr && s_rr < (long long)le) s_res = ki;  // (equal keys write the same)
+      }
+    } else if (s_bin != 0xffffffffu && tid == 0 && n_all <= (unsigned int)kCandMax) {
+      // a crowded bin: narrow the range to it and histogram again
+      const unsigned long long na = a + ((unsigned long long)s_bin << sh2);
+      const unsigned long long span = (1ull << sh2) - 1ull;
+      G.a = na;
+      G.b = (b - na < span) ? b : na + span;
+      s_res = ~0ull - 1ull;  // (marker: narrowed)
     }
     __syncthreads();
     if (tid == 0) {
-      if (s_res != ~0ull && n_all <= (unsigned int)kCandMax) {
+      if (s_res < ~0ull - 1ull && n_all <= (unsigned int)kCandMax) {
         median_done(p, g, s_res);
-      } else {  // (not reachable from a consistent count) histogram the range again
-        G.sh = range_shift(b - a);
+      } else {  // a narrowed crowded bin, or (not reachable from a consistent count) the range again
+        G.sh = range_shift(G.b - G.a);
         G.mode = kModeHist;
       }
       G.below = 0ull;
@@ -1730,7 +1738,7 @@ __device__ void median_finish(RadixParams& p, int g, unsigned long long* scratch
 template <typename InT, bool kInput>
 __global__ void __launch_bounds__(kHistThreads) median_pass_kernel(RadixParams p, int last) {
   __shared__ __align__(16) uint32_t hs[kBins];
-  static_assert(kBins * 4 >= 2 * kCandMax * 8, "median_step scratch");
+  static_assert(kBins * 4 >= kBinMax * 8, "median_step scratch");
   __shared__ bool is_last;
   if (!kInput && p.done[2]) return;  // every group resolved
   const int64_t row = blockIdx.y;
