@@ -751,26 +751,23 @@ __global__ void __launch_bounds__(256, 6) decode_flag_tma_kernel(DecParams p) {
           for (int c = 0; c < 4; ++c) {
             ov[c] = mul_round_f16(rad[c], reinterpret_cast<const uint2*>(tab)[idx[c]]);
           }
-          if (f4) {  // outlier chunks: their fp16 payload rows verbatim
-            // payload row of chunk c = rows before the quad + flagged chunks
-            // before c within it (c - slot of c)
-            const uint32_t prow0 = (tok32 + (uint32_t)tt) * 32u - tofs + __popc(fw & below) - pbase32;
-            if (pn != 0) {  // staged tile: predicated shared loads, no per-chunk branches
+          // payload row of chunk c = rows before the quad + flagged chunks
+          // before c within it (c - slot of c)
+          const uint32_t prow0 = (tok32 + (uint32_t)tt) * 32u - tofs + __popc(fw & below) - pbase32;
+          if (pn != 0) {  // staged tile: predicated shared loads, no branches
 #pragma unroll
-              for (int c = 0; c < 4; ++c) {
+            for (int c = 0; c < 4; ++c) {
+              const uint32_t j = (uint32_t)c - __popc(f4 & ((1u << c) - 1u));
+              const uint32_t rel = min(prow0 + (uint32_t)c - j, pn - 1u);
+              if ((f4 >> c) & 1u) ov[c] = pays[rel];
+            }
+          } else if (f4) {  // unstaged tile: the outlier rows from global
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              if ((f4 >> c) & 1u) {
                 const uint32_t j = (uint32_t)c - __popc(f4 & ((1u << c) - 1u));
-                const uint32_t rel = min(prow0 + (uint32_t)c - j, pn - 1u);
-                const uint2 pv = pays[rel];
-                ov[c] = ((f4 >> c) & 1u) ? pv : ov[c];
-              }
-            } else {
-#pragma unroll
-              for (int c = 0; c < 4; ++c) {
-                if ((f4 >> c) & 1u) {
-                  const uint32_t j = (uint32_t)c - __popc(f4 & ((1u << c) - 1u));
-                  ov[c] = __ldg(reinterpret_cast<const uint2*>(p.payloads) +
-                                (pbase + (uint32_t)(prow0 + (uint32_t)c - j)));
-                }
+                ov[c] = __ldg(reinterpret_cast<const uint2*>(p.payloads) +
+                              (pbase + (uint32_t)(prow0 + (uint32_t)c - j)));
               }
             }
           }
