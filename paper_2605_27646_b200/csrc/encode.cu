@@ -1416,14 +1416,15 @@ __device__ __forceinline__ double chunk_vec_sq(const typename ChunkVec<InT>::T& 
 //     keys at ranks m/2 -+ 57 (5 sigma of the sample rank of the median;
 //     about 22% of the group's elements fall inside).  A group of <= 512
 //     chunks is its own sample: exact at once.
-//   median_pass_kernel (x3): one pass over the group's elements (the first
+//   median_pass_kernel (x2, x3 for groups over ~8M chunks): one pass over
+//     the group's elements (the first
 //     computes and stores the norms from the input): elements below a are
 //     counted (ballots, no atomics), elements inside [a, b] go either to an
 //     8192-bin shared histogram of (key - a) >> sh, or -- once the range holds
 //     <= 1024 of them -- to a candidate list.  The last CTA narrows [a, b] to
 //     the bin holding rank k - below, or selects the exact key among the
 //     candidates.  A bracket that misses (rank k below a or above b) narrows
-//     to the side it missed; whatever is unresolved after the third pass is
+//     to the side it missed; whatever is unresolved after the last pass is
 //     finished by that pass's last CTA alone (exact, slow, never seen on
 //     model-like data).
 // Only the ~22% of elements inside the bracket touch shared atomics (the fixed
@@ -1583,8 +1584,7 @@ __device__ void median_step(RadixParams& p, int g, unsigned long long* scratch) 
       const unsigned long long span = (1ull << G.sh) - 1ull;
       s_a = na;
       s_b = (b - na < span) ? b : na + span;
-     
-      s_found = 1;
+      // (s_found is read by the other threads in this phase: not written here)
     }
     __syncthreads();
     for (int i = tid; i < kBins; i += nt) hg[i] = 0u;
@@ -2040,10 +2040,16 @@ int launch_encode(const hqmq_encode_args* a, const Layout& L, cudaStream_t st) {
     } else {  // exact median: sampled bracket + 3 narrowing passes (the first stores the norms)
       median_sample_kernel<InT><<<L.G, kSampleThreads, 0, st>>>(rp, L.warp_path ? status : nullptr,
                                                                   L.warp_path ? n_status : 0);
+      // Pass 1 narrows the bracket (<= ~25% of the group) to one of 1024 bins;
+      // while such a bin stays within the compaction threshold (twice the mean
+      // as headroom) pass 2 resolves and is the last pass; larger groups get a
+      // third.  Anything unresolved by the last pass is finished by its last CTA.
+      const bool two_pass =
+          n_per_group <= (unsigned long long)(kCandMax / 2) * (1ull << kFirstBits) * 4ull;
       const dim3 grid((unsigned)bx_full, (unsigned)L.rows);
       median_pass_kernel<InT, true><<<grid, kHistThreads, 0, st>>>(rp, 0);
-      median_pass_kernel<InT, false><<<grid, kHistThreads, 0, st>>>(rp, 0);
-      median_pass_kernel<InT, false><<<grid, kHistThreads, 0, st>>>(rp, 1);
+      median_pass_kernel<InT, false><<<grid, kHistThreads, 0, st>>>(rp, two_pass ? 1 : 0);
+      if (!two_pass) median_pass_kernel<InT, false><<<grid, kHistThreads, 0, st>>>(rp, 1);
     }
     uint32_t* counts = reinterpret_cast<uint32_t*>(ws + L.off_counts);
     size_t cub_bytes = L.cub_bytes;

@@ -12,8 +12,8 @@ therefore needs no collective on the data path:
 * ``ShardPlan.weak``: every rank owns a full cache of its own (replicas).
 
 Splitting a unit by KV head is exchange-free only with per-head median
-pooling; with "batch" pooling the exact median would need one histogram
-all-reduce per radix pass.  ``head_split`` exposes the per-head variant
+pooling; with "batch" pooling the exact median would need the bracket
+counts and histograms all-reduced per narrowing pass.  ``head_split`` exposes the per-head variant
 (head_base offsets keep the codebook keys of the unsplit call,
 codec.py:133-135).
 
