@@ -204,6 +204,40 @@ int hqmq_expand_tokens(const hqmq_decode_args* args, uint32_t* index_slots,
                        uint32_t* radius_slots, uint32_t* payload_offsets,
                        uint32_t payload_base, void* stream);
 
+/* The paged cache's append scatter (no reference
+ * counterpart -- the reference keeps one dense tensor per call,
+ * codec.py:124-147): the token-aligned sections of a freshly encoded
+ * (n_seq, kv_heads, n_new, head_dim) call go to their page slots.  Source
+ * token row r = (i*kv_heads + h)*n_new + t lands in slot
+ * block_table[(seq_ids[i]*kv_heads + h)*max_pages + p]*page_tokens + o,
+ * (p, o) = divmod(seq_start[i] + t, page_tokens): index_bits index words,
+ * radius_bits radius words, the fp16 scale and -- for Med3x caches
+ * (flag_pages != NULL) -- the flag word and payload-row offset of the token
+ * (src_index / src_radius in the fixed per-token slot layout of
+ * hqmq_expand_tokens).  A page id outside [0, num_pages) sets
+ * HQMQ_DEVERR_INDEX_RANGE in *error_word (if given) and skips the token. */
+typedef struct {
+  int32_t n_seq, kv_heads, n_new, max_pages;
+  int32_t page_tokens, index_bits, radius_bits, _pad;
+  int64_t num_pages;
+  const int32_t* seq_ids;     /* [n_seq], device */
+  const int32_t* seq_start;   /* [n_seq], device: tokens already cached */
+  const int32_t* block_table; /* [batch*kv_heads*max_pages], device */
+  const uint32_t* src_index;  /* [n_rows][index_bits] */
+  const uint32_t* src_radius; /* [n_rows][radius_bits] */
+  const uint16_t* src_scales; /* [n_rows] */
+  const uint32_t* src_flags;  /* [n_rows] or NULL */
+  const uint32_t* src_payoff; /* [n_rows] or NULL */
+  uint32_t* index_pages;      /* [num_pages][page_tokens*index_bits] */
+  uint32_t* radius_pages;     /* [num_pages][page_tokens*radius_bits] */
+  uint16_t* scale_pages;      /* [num_pages][page_tokens] */
+  uint32_t* flag_pages;       /* [num_pages][page_tokens] or NULL */
+  uint32_t* payoff_pages;     /* [num_pages][page_tokens] or NULL */
+  uint32_t* error_word;       /* optional */
+} hqmq_paged_append_args;
+
+int hqmq_paged_append(const hqmq_paged_append_args* args, void* stream);
+
 /* Pack dense arrays (indices int32, quanta uint8, flags uint8 or NULL) into
  * the section streams (the inverse of hqmq_unpack; kvpack.py:134-146).
  * index/radius/flag word buffers must be zero-filled by the caller. */

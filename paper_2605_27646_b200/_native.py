@@ -107,6 +107,19 @@ class PagedAttentionArgs(ctypes.Structure):
     ]
 
 
+class PagedAppendArgs(ctypes.Structure):
+    _fields_ = [
+        ("n_seq", c_i32), ("kv_heads", c_i32), ("n_new", c_i32), ("max_pages", c_i32),
+        ("page_tokens", c_i32), ("index_bits", c_i32), ("radius_bits", c_i32), ("_pad", c_i32),
+        ("num_pages", c_i64),
+        ("seq_ids", c_vp), ("seq_start", c_vp), ("block_table", c_vp),
+        ("src_index", c_vp), ("src_radius", c_vp), ("src_scales", c_vp),
+        ("src_flags", c_vp), ("src_payoff", c_vp),
+        ("index_pages", c_vp), ("radius_pages", c_vp), ("scale_pages", c_vp),
+        ("flag_pages", c_vp), ("payoff_pages", c_vp), ("error_word", c_vp),
+    ]
+
+
 # Every symbol include/hqmq_b200.h declares, with its ctypes signature.
 SIGNATURES = {
     "hqmq_version": ([], ctypes.c_char_p),
@@ -120,6 +133,7 @@ SIGNATURES = {
     "hqmq_unpack": ([ctypes.POINTER(DecodeArgs), c_vp, c_vp, c_vp, c_vp], c_i32),
     "hqmq_expand_tokens": ([ctypes.POINTER(DecodeArgs), c_vp, c_vp, c_vp, ctypes.c_uint32, c_vp],
                            c_i32),
+    "hqmq_paged_append": ([ctypes.POINTER(PagedAppendArgs), c_vp], c_i32),
     "hqmq_pack": ([c_i64, c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                    ctypes.c_size_t, c_vp], c_i32),
     "hqmq_pack_workspace_bytes": ([c_i64], ctypes.c_size_t),

@@ -1153,6 +1153,37 @@ int decode_fp16_tiles(const hqmq_decode_args* a, int tile_log2, int mn, int64_t 
 }
 }  // namespace hqmq
 
+namespace hqmq {
+// Paged append scatter (hqmq_paged_append): warp = one source token row.
+__global__ void __launch_bounds__(256) paged_append_kernel(hqmq_paged_append_args a, int64_t n_rows) {
+  const int lane = threadIdx.x & 31;
+  const int64_t stride = (int64_t)gridDim.x * 8;
+  for (int64_t r = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5); r < n_rows; r += stride) {
+    const int64_t t = r % a.n_new, ih = r / a.n_new;
+    const int h = (int)(ih % a.kv_heads), i = (int)(ih / a.kv_heads);
+    const int64_t pos = (int64_t)__ldg(a.seq_start + i) + t;
+    const int64_t pi = pos / a.page_tokens, o = pos - pi * a.page_tokens;
+    const int64_t page = pi < a.max_pages
+        ? (int64_t)__ldg(a.block_table + ((int64_t)__ldg(a.seq_ids + i) * a.kv_heads + h) * a.max_pages + pi)
+        : -1;
+    if (page < 0 || page >= a.num_pages) {
+      if (lane == 0 && a.error_word) atomicOr(a.error_word, HQMQ_DEVERR_INDEX_RANGE);
+      continue;
+    }
+    const int64_t slot = page * a.page_tokens + o;
+    if (lane < a.index_bits)
+      a.index_pages[slot * a.index_bits + lane] = __ldg(a.src_index + r * a.index_bits + lane);
+    if (lane < a.radius_bits)
+      a.radius_pages[slot * a.radius_bits + lane] = __ldg(a.src_radius + r * a.radius_bits + lane);
+    if (lane == 0) a.scale_pages[slot] = __ldg(a.src_scales + r);
+    if (a.flag_pages) {
+      if (lane == 1) a.flag_pages[slot] = __ldg(a.src_flags + r);
+      if (lane == 2) a.payoff_pages[slot] = __ldg(a.src_payoff + r);
+    }
+  }
+}
+}  // namespace hqmq
+
 extern "C" {
 
 int hqmq_decode(const hqmq_decode_args* a, void* stream) {
@@ -1175,6 +1206,24 @@ int hqmq_decode(const hqmq_decode_args* a, void* stream) {
     }
     default: return HQMQ_ERR_INVALID_ARGUMENT;
   }
+}
+
+int hqmq_paged_append(const hqmq_paged_append_args* a, void* stream) {
+  using namespace hqmq;
+  if (!a || a->n_seq < 0 || a->kv_heads < 1 || a->n_new < 0 || a->max_pages < 1 ||
+      a->page_tokens < 1 || a->index_bits < 1 || a->index_bits > 32 || a->radius_bits < 1 ||
+      a->radius_bits > 32 || a->num_pages < 1 || !a->seq_ids || !a->seq_start || !a->block_table ||
+      !a->src_index || !a->src_radius || !a->src_scales || !a->index_pages || !a->radius_pages ||
+      !a->scale_pages)
+    return HQMQ_ERR_INVALID_ARGUMENT;
+  if ((a->flag_pages != nullptr) != (a->payoff_pages != nullptr) ||
+      (a->flag_pages && (!a->src_flags || !a->src_payoff)))
+    return HQMQ_ERR_INVALID_ARGUMENT;
+  const int64_t n_rows = (int64_t)a->n_seq * a->kv_heads * a->n_new;
+  if (n_rows == 0) return HQMQ_OK;
+  const int64_t blocks = std::min<int64_t>(ceil_div(n_rows, 8), 148 * 8);
+  paged_append_kernel<<<(unsigned)blocks, 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(*a, n_rows);
+  return check();
 }
 
 int hqmq_expand_tokens(const hqmq_decode_args* a, uint32_t* index_slots, uint32_t* radius_slots,

@@ -11,8 +11,10 @@ appending is:
 
   1. encode_tensor of the new tokens (the sm_100a encode, bit-identical to the
      reference on those tokens: without extraction the codec is token-local);
-  2. a row scatter of each new token's code words into its page slot
-     (device index_copy); pages are taken from a free list as rows grow.
+  2. one scatter kernel per role (hqmq_paged_append) moving each new token's
+     code words, scale (and Med3x flag word / payload offset) into its page
+     slot, the slot computed on the device from the block table; pages are
+     taken from a free list as rows grow.
 
 attend() runs the decode-attention kernel with a block table
 (hqmq_attention_decode_paged).
@@ -44,7 +46,7 @@ import math
 from . import _native as nat
 from .codebook import CodebookBank
 from .codec import CodecConfig, _bank_for, _torch, check_out, encode_tensor
-from .errors import InvalidArgument
+from .errors import CorruptData, InvalidArgument
 
 PAGE_TOKENS = 128
 
@@ -111,6 +113,10 @@ class PagedKVCache:
         self._table_host = [[[-1] * self.max_pages for _ in range(kv_heads)] for _ in range(batch)]
         self.lengths = [0] * batch
         self.kv_lens = torch.zeros(batch, dtype=torch.int32, device=dev)
+        # device error word of the append scatter (HQMQ_DEVERR_INDEX_RANGE on a
+        # page id outside the pool: not reachable through this class's own
+        # page bookkeeping; read by check_errors())
+        self._err = torch.zeros(1, dtype=torch.int32, device=dev)
         self._free = list(range(self.num_pages - 1, -1, -1))
         if page_order_seed is not None:  # a fragmented pool: pages handed out in random order
             import random
@@ -153,33 +159,47 @@ class PagedKVCache:
                     self._page(b, h, i)
         self.block_table.copy_(torch.tensor(self._table_host, dtype=torch.int32))
         dev = self.device
-        sel = torch.tensor(seqs, dtype=torch.int64, device=dev)
-        t = torch.tensor([self.lengths[b] for b in seqs], dtype=torch.int64, device=dev)[:, None, None] \
-            + torch.arange(n_new, device=dev)[None, None, :]
-        heads = torch.arange(self.kv_heads, device=dev)[None, :, None]
-        page = self.block_table[sel[:, None, None], heads, t // PAGE_TOKENS].to(torch.int64)
-        slots = (page * PAGE_TOKENS + t % PAGE_TOKENS).reshape(-1)
-        n_tok = slots.numel()
+        # (seq ids, cached lengths) of the appended sequences; the scatter into
+        # the page slots is one kernel per role (hqmq_paged_append)
+        seq_info = torch.tensor([seqs, [self.lengths[b] for b in seqs]], dtype=torch.int32,
+                                device=dev)
+        n_tok = len(seqs) * self.kv_heads * n_new
         w, br = self.config.index_bits, self.config.radius_bits
         for role, x in (("K", k), ("V", v)):
             qt = encode_tensor(x, self.config, layer=self.layer, role=role, bank=self.bank,
                                head_base=self.head_base, device=self.device,
                                outlier_thresholds=self.thresholds[role] if self.med3x else None)
             pool = self.pages[role]
+            a = nat.PagedAppendArgs()
+            a.n_seq, a.kv_heads, a.n_new, a.max_pages = len(seqs), self.kv_heads, n_new, \
+                self.max_pages
+            a.page_tokens, a.index_bits, a.radius_bits = PAGE_TOKENS, w, br
+            a.num_pages = self.num_pages
+            a.seq_ids, a.seq_start = seq_info[0].data_ptr(), seq_info[1].data_ptr()
+            a.block_table = self.block_table.data_ptr()
             if self.med3x:
                 if self.thresholds[role] is None:  # the prefill freezes its thresholds
                     self.thresholds[role] = qt.outlier_thresholds.clone()
                 iw, rw, payoff = self._expand(role, qt, n_tok)
-                pool["flags"].view(-1).index_copy_(0, slots, qt.flag_words[:n_tok])
-                pool["payoff"].view(-1).index_copy_(0, slots, payoff)
+                a.src_flags, a.src_payoff = qt.flag_words.data_ptr(), payoff.data_ptr()
+                a.flag_pages, a.payoff_pages = pool["flags"].data_ptr(), pool["payoff"].data_ptr()
             else:
-                iw, rw = qt.index_words[: n_tok * w], qt.radius_words[: n_tok * br]
-            pool["index"].view(-1, w).index_copy_(0, slots, iw.view(n_tok, w))
-            pool["radius"].view(-1, br).index_copy_(0, slots, rw.view(n_tok, br))
-            pool["scales"].view(-1).index_copy_(0, slots, qt.scales.reshape(-1))
+                iw, rw = qt.index_words, qt.radius_words
+            a.src_index, a.src_radius = iw.data_ptr(), rw.data_ptr()
+            a.src_scales = qt.scales.data_ptr()
+            a.index_pages, a.radius_pages = pool["index"].data_ptr(), pool["radius"].data_ptr()
+            a.scale_pages = pool["scales"].data_ptr()
+            a.error_word = self._err.data_ptr()
+            nat.launch(dev, "hqmq_paged_append", nat.lib().hqmq_paged_append, ctypes.byref(a))
         for b in seqs:
             self.lengths[b] += n_new
         self.kv_lens.copy_(torch.tensor(self.lengths, dtype=torch.int32))
+
+    def check_errors(self) -> None:
+        """Raise CorruptData if an append met a page id outside the pool
+        (synchronises with the device)."""
+        if int(self._err.item()):
+            raise CorruptData("paged append: page id outside the page pool")
 
     def _expand(self, role, qt, n_tok):
         """Med3x: the encoder's compact sections -> fixed per-token slots and

@@ -87,6 +87,69 @@ def test_paged_codes_match_one_shot_encode(cuda):
             assert torch.equal(pool["scales"].view(-1)[pid], ref.scales.reshape(-1)[row])
 
 
+def test_paged_append_subsets_fragmented_pool(cuda):
+    """hqmq_paged_append: appends for sequence subsets in any order into a
+    shuffled page pool land in the right slots -- page contents equal each
+    sequence's one-shot encode rows (token-local codec without extraction)."""
+    m = hq()
+    cfg = m.CodecConfig(64, 4)
+    bank = m.CodebookBank(0, 64)
+    gen = torch.Generator(device=cuda).manual_seed(9)
+    B, H = 3, 2
+    cache = m.PagedKVCache(cfg, B, H, max_tokens=384, bank=bank, page_order_seed=3)
+    per_seq = {b: [] for b in range(B)}
+    for seqs, n in (([2, 0], 70), ([1], 130), ([0, 1, 2], 61), ([2], 1)):
+        x = torch.randn((len(seqs), H, n, 128), generator=gen, device=cuda).half()
+        cache.append(x, x, seqs=seqs)
+        for i, b in enumerate(seqs):
+            per_seq[b].append(x[i:i + 1])
+    cache.check_errors()
+    w, br = cfg.index_bits, cfg.radius_bits
+    pool = cache.pages["V"]
+    for b in range(B):
+        xs = torch.cat(per_seq[b], dim=2)
+        ref = m.encode_tensor(xs, cfg, role="V", bank=bank)
+        T = xs.shape[2]
+        assert cache.lengths[b] == T
+        for h in range(H):
+            for t in range(T):
+                pid = int(cache.block_table[b, h, t // 128]) * 128 + t % 128
+                row = h * T + t
+                assert torch.equal(pool["index"].view(-1, w)[pid], ref.index_words[row * w:(row + 1) * w])
+                assert torch.equal(pool["radius"].view(-1, br)[pid],
+                                   ref.radius_words[row * br:(row + 1) * br])
+                assert torch.equal(pool["scales"].view(-1)[pid], ref.scales.reshape(-1)[row])
+
+
+def test_paged_append_bad_page_reported(cuda):
+    """A block-table entry outside the pool is skipped and reported through the
+    cache's device error word (check_errors -> CorruptData)."""
+    import ctypes
+
+    m = hq()
+    from paper_2605_27646_b200 import _native as nat
+
+    cache = m.PagedKVCache(m.CodecConfig(16, 4), 1, 1, 256, num_pages=2)
+    x = torch.randn((1, 1, 4, 128), device=cuda).half()
+    qt = m.encode_tensor(x, cache.config, bank=cache.bank)
+    table = torch.full((1, 1, 2), -1, dtype=torch.int32, device=cuda)
+    info = torch.zeros((2, 1), dtype=torch.int32, device=cuda)
+    pool = cache.pages["K"]
+    a = nat.PagedAppendArgs()
+    a.n_seq, a.kv_heads, a.n_new, a.max_pages = 1, 1, 4, 2
+    a.page_tokens, a.index_bits, a.radius_bits, a.num_pages = 128, cache.config.index_bits, 4, 2
+    a.seq_ids, a.seq_start, a.block_table = info[0].data_ptr(), info[1].data_ptr(), table.data_ptr()
+    a.src_index, a.src_radius = qt.index_words.data_ptr(), qt.radius_words.data_ptr()
+    a.src_scales = qt.scales.data_ptr()
+    a.index_pages, a.radius_pages = pool["index"].data_ptr(), pool["radius"].data_ptr()
+    a.scale_pages = pool["scales"].data_ptr()
+    a.error_word = cache._err.data_ptr()
+    nat.launch(cuda, "hqmq_paged_append", nat.lib().hqmq_paged_append, ctypes.byref(a))
+    with pytest.raises(m.CorruptData):
+        cache.check_errors()
+    assert int(pool["index"].abs().sum()) == 0  # nothing written
+
+
 def test_paged_errors(cuda):
     m = hq()
     cache = m.PagedKVCache(m.CodecConfig(16, 4), 1, 1, 128, num_pages=1)

@@ -102,6 +102,25 @@ def test_paged_struct_layouts_with_compiler(tmp_path):
                    A.num_splits.offset, A.workspace_bytes.offset]
 
 
+def test_paged_append_struct_layout_with_compiler(tmp_path):
+    """hqmq_paged_append_args as the C compiler lays it out."""
+    from paper_2605_27646_b200 import _native
+
+    src = tmp_path / "probe_append.c"
+    src.write_text(
+        '#include <stdio.h>\n#include <stddef.h>\n#include "hqmq_b200.h"\n'
+        "int main(){printf(\"%zu %zu %zu %zu\\n\", sizeof(hqmq_paged_append_args),"
+        " offsetof(hqmq_paged_append_args, num_pages), offsetof(hqmq_paged_append_args, src_index),"
+        " offsetof(hqmq_paged_append_args, error_word));return 0;}\n")
+    exe = tmp_path / "probe_append"
+    import subprocess
+
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    out = [int(v) for v in subprocess.check_output([str(exe)]).split()]
+    A = _native.PagedAppendArgs
+    assert out == [ctypes.sizeof(A), A.num_pages.offset, A.src_index.offset, A.error_word.offset]
+
+
 def test_no_cpu_fallback_without_device():
     torch = pytest.importorskip("torch")
     if torch.cuda.is_available():
