@@ -1747,8 +1747,11 @@ __global__ void __launch_bounds__(kHistThreads) median_pass_kernel(RadixParams p
   const unsigned long long a = p.groups[g].a, b = p.groups[g].b;
   const int sh = p.groups[g].sh;
   const bool active = mode != kModeDone;
+  // bins in use: (b - a) >> sh + 1 (<= 1024 in the first pass, <= 8192 after)
+  const unsigned long long span_bins = ((b - a) >> sh) + 1ull;
+  const int nbins = span_bins < (unsigned long long)kBins ? (int)span_bins : kBins;
   if (active && mode == kModeHist)
-    for (int i = threadIdx.x; i < kBins; i += kHistThreads) hs[i] = 0u;
+    for (int i = threadIdx.x; i < nbins; i += kHistThreads) hs[i] = 0u;
   __syncthreads();
   constexpr int kRB = kInput ? 8 : 16;  // (norm-only passes: more loads in flight)
   const int64_t L = p.T * p.C;
@@ -1805,7 +1808,7 @@ __global__ void __launch_bounds__(kHistThreads) median_pass_kernel(RadixParams p
     if (threadIdx.x == 0 && tb) atomicAdd(&p.groups[g].below, tb);
     if (mode == kModeHist) {
       uint32_t* hg = p.hist + (int64_t)g * kBins;
-      for (int i = threadIdx.x; i < kBins; i += kHistThreads)
+      for (int i = threadIdx.x; i < nbins; i += kHistThreads)
         if (hs[i]) atomicAdd(hg + i, hs[i]);
     }
   }
@@ -2028,6 +2031,8 @@ int launch_encode(const hqmq_encode_args* a, const Layout& L, cudaStream_t st) {
     rp.n_per_group = n_per_group;
     rp.groups = groups; rp.hist = hist; rp.done = done; rp.G = L.G;
     const int64_t row_chunks = a->tokens * L.C;
+    // median passes: up to 4 CTAs per SM (>= 8 chunks per thread; 32 measured
+    // the same on C1's 1M-chunk calls, which are launch / latency bound)
     const int64_t bx_full = std::max<int64_t>(
         1, std::min<int64_t>(ceil_div((int64_t)148 * 4, L.rows), ceil_div(row_chunks, kHistThreads * 8)));
 
