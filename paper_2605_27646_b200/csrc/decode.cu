@@ -562,8 +562,11 @@ __global__ void __launch_bounds__(256) decode_flag_kernel(DecParams p) {
 // flag words, token offsets and scales; warps then decode like the fast path
 // (warp = token, lane = chunk, coded position = token offset + ballot popc),
 // flagged lanes reading their fp16 payload row from global.
+#ifndef HQMQ_FL_STAGES
+#define HQMQ_FL_STAGES 4
+#endif
 constexpr int kFlTok = 64;
-constexpr int kFlStages = 4;
+constexpr int kFlStages = HQMQ_FL_STAGES;  // (sweep: tools/gpu_r4e.sh)
 
 struct FlagGeom {
   uint32_t idx_off, rad_off, fl_off, to_off, sc_off, pay_off, stage_bytes;
