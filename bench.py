@@ -94,18 +94,67 @@ def self_launch(argv, n):
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled DURING the timed region: NVML from
+    a polling thread (10 ms period; each call is a few microseconds), or
+    nvidia-smi at its 200 ms period when pynvml is unavailable."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    PERIOD_S = 0.010
 
     def __init__(self, index: int):
         self.index = index
         self.proc = None
         self.lines = []
+        self.samples = []  # (sm_mhz, max_mhz, reason bitmask) from NVML
+        self.nvml = None
+        self.source = None
+
+    def _nvml_handle(self):
+        import pynvml
+        import torch
+
+        pynvml.nvmlInit()
+        props = torch.cuda.get_device_properties(self.index)
+        uuid = getattr(props, "uuid", None)
+        if uuid is not None:
+            try:
+                u = str(uuid)
+                return pynvml, pynvml.nvmlDeviceGetHandleByUUID(u if u.startswith("GPU-") else "GPU-" + u)
+            except Exception:
+                pass
+        try:
+            bus = f"{props.pci_domain_id:08x}:{props.pci_bus_id:02x}:{props.pci_device_id:02x}.0"
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
+
+    def _poll(self):
+        nv, h = self.nvml
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self.stop.is_set():
+            try:
+                self.samples.append((nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM), mx,
+                                     nv.nvmlDeviceGetCurrentClocksEventReasons(h)))
+            except Exception:
+                pass
+            self.stop.wait(self.PERIOD_S)
 
     def __enter__(self):
+        try:
+            self.nvml = self._nvml_handle()
+            self.stop = threading.Event()
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            t_end = time.time() + 3.0  # first (idle) sample before the caller's timer
+            while not self.samples and time.time() < t_end:
+                time.sleep(0.001)
+            self.samples.clear()
+            self.source = f"nvml, {int(self.PERIOD_S * 1000)} ms period"
+            return self
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
@@ -119,6 +168,7 @@ class ClockSampler:
             while not self.lines and time.time() < t_end:
                 time.sleep(0.01)
             self.lines.clear()
+            self.source = "nvidia-smi, 200 ms period"
         except OSError:
             self.proc = None
         return self
@@ -129,6 +179,13 @@ class ClockSampler:
 
     def __exit__(self, *exc):
         self.late = False
+        if self.nvml is not None:
+            if not self.samples:  # region shorter than one period: one sample right after
+                time.sleep(self.PERIOD_S)
+                self.late = bool(self.samples)
+            self.stop.set()
+            self.thread.join(timeout=2)
+            return
         if self.proc and not self.lines:
             # timed region shorter than nvidia-smi's start-up + 200 ms period
             # (e.g. C1): take the first sample right after it, and say so
@@ -146,6 +203,16 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        if self.nvml is not None:
+            nv = self.nvml[0]
+            bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                    nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+            for clk, m, r in self.samples:
+                sm.append(float(clk))
+                mx.append(float(m))
+                for nm, bit in zip(names, bits):
+                    if r & bit:
+                        reasons.add(nm)
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 7:
@@ -161,7 +228,7 @@ class ClockSampler:
         if not sm:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
         out = {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
-               "samples": len(sm)}
+               "samples": len(sm), "source": self.source}
         if getattr(self, "late", False):
             out["note"] = "timed region shorter than the sampling period: sampled just after it"
         return out
