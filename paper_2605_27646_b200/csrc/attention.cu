@@ -74,7 +74,7 @@ __global__ void __launch_bounds__(kAttThreads) attention_split_kernel(AttParams 
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t bh = blockIdx.y;  // b * Hkv + hkv
-  const int64_t b = bh / p.Hkv, hkv = bh % p.Hkv;
+  const int64_t b = (uint32_t)bh / (uint32_t)p.Hkv, hkv = (uint32_t)bh % (uint32_t)p.Hkv;  // (32-bit)
   const int split = blockIdx.x;
   const int row0 = blockIdx.z * kRows;
   const int C = p.C, D = (int)p.D, ncw = kGroupOrder * p.S;
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(kAttThreads) attention_split_kernel(AttParams 
 __global__ void combine_kernel(AttParams p) {
   const int64_t bh = blockIdx.x;
   const int r = blockIdx.y;
-  const int64_t b = bh / p.Hkv, hkv = bh % p.Hkv;
+  const int64_t b = (uint32_t)bh / (uint32_t)p.Hkv, hkv = (uint32_t)bh % (uint32_t)p.Hkv;  // (32-bit)
   const int64_t base = (bh * p.nrows + r) * p.splits;
   float M = -INFINITY;
   for (int s = 0; s < p.splits; ++s) M = fmaxf(M, p.part_ml[2 * (base + s)]);
@@ -284,7 +284,7 @@ __global__ void __launch_bounds__(kAttThreads) attention_f64_kernel(AttParams p,
   double* p_s = v_s + kKT * 4 * kMaxC;        // [kRows][kKT]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t bh = blockIdx.y;
-  const int64_t b = bh / p.Hkv, hkv = bh % p.Hkv;
+  const int64_t b = (uint32_t)bh / (uint32_t)p.Hkv, hkv = (uint32_t)bh % (uint32_t)p.Hkv;  // (32-bit)
   const int split = blockIdx.x;
   const int row0 = blockIdx.z * kRows;
   const int C = p.C, D = (int)p.D, ncw = kGroupOrder * p.S;
@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(kAttThreads) attention_f64_kernel(AttParams p,
 __global__ void combine_f64_kernel(AttParams p, AttParams64 p64) {
   const int64_t bh = blockIdx.x;
   const int r = blockIdx.y;
-  const int64_t b = bh / p.Hkv, hkv = bh % p.Hkv;
+  const int64_t b = (uint32_t)bh / (uint32_t)p.Hkv, hkv = (uint32_t)bh % (uint32_t)p.Hkv;  // (32-bit)
   const int64_t base = (bh * p.nrows + r) * p.splits;
   double M = -INFINITY;
   for (int s = 0; s < p.splits; ++s) M = fmax(M, p64.part_ml[2 * (base + s)]);
@@ -540,7 +540,7 @@ __global__ void __launch_bounds__(kMThreads, 2) attention_mma_kernel(AttParams p
   }
 
   const int64_t bh = blockIdx.y;
-  const int64_t b = bh / p.Hkv, hkv = bh % p.Hkv;
+  const int64_t b = (uint32_t)bh / (uint32_t)p.Hkv, hkv = (uint32_t)bh % (uint32_t)p.Hkv;  // (32-bit)
   const int64_t kbeg = (int64_t)blockIdx.x * p.keys_per_split;
   const int64_t tkv = kPaged ? (int64_t)__ldg(p.kv_lens + b) : p.Tkv;  // this sequence's keys
   const int64_t kend = min(tkv, kbeg + p.keys_per_split);

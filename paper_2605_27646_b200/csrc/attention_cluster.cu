@@ -73,8 +73,12 @@ struct CParams {
   AttParams p;
   int nsplit;               // key splits per row
   int64_t kps;              // keys per split (multiple of 128)
-  int64_t items;            // Hkv * B * nsplit, hkv-major
+  int64_t items;            // Hkv * B * nsplit, hkv-major (< 2^31)
   int ncw;
+  float q_scale;            // softmax scale * log2(e) * 2^9 / top, from the host
+  // (the kernel's loop is kept free of subroutine calls -- 64-bit integer and
+  // IEEE fp32 division -- so ptxas keeps the global-memory descriptor in
+  // uniform registers instead of re-materialising it before every load)
 };
 
 // ---------------------------------------------------------------- PTX bits
@@ -206,10 +210,13 @@ struct Item {
 __device__ __forceinline__ Item item_at(const CParams& c, int64_t i) {
   const AttParams& p = c.p;
   Item it;
-  it.hkv = i / (p.B * c.nsplit);
-  const int64_t r = i - it.hkv * p.B * c.nsplit;
-  it.b = r / c.nsplit;
-  it.split = (int)(r - it.b * c.nsplit);
+  const uint32_t per_h = (uint32_t)p.B * (uint32_t)c.nsplit;  // 32-bit: items < 2^31
+  const uint32_t hk = (uint32_t)i / per_h;
+  const uint32_t r = (uint32_t)i - hk * per_h;
+  const uint32_t bq = r / (uint32_t)c.nsplit;
+  it.hkv = hk;
+  it.b = bq;
+  it.split = (int)(r - bq * (uint32_t)c.nsplit);
   it.bh = it.b * p.Hkv + it.hkv;
   const int64_t tkv = p.kv_lens ? (int64_t)__ldg(p.kv_lens + it.b) : p.Tkv;
   it.kbeg = (int64_t)it.split * c.kps;
@@ -344,7 +351,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCThreads, 1)
 
   const int nclus = gridDim.x / 2;
   const int64_t clus = blockIdx.x / 2;
-  const int64_t i0 = clus * c.items / nclus, i1 = (clus + 1) * c.items / nclus;
+  const int64_t i0 = (int64_t)((uint64_t)clus * (uint64_t)c.items / (uint32_t)nclus);
+  const int64_t i1 = (int64_t)((uint64_t)(clus + 1) * (uint64_t)c.items / (uint32_t)nclus);
 
   if (lane == 0) {
     mbar_init(mbox, 1);
@@ -384,7 +392,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCThreads, 1)
       uint32_t qb[8][2];
       {
         // softmax scale * log2(e) * 2^9 / top (the decoded products are q c 2^-9)
-        const float qs = p.scale_log2 * kProdScale / (float)((1 << BR) - 1);
+        const float qs = c.q_scale;
         const bool rv = g4 < p.nrows;
         const int gi = rv ? g4 / (int)p.Tq : 0, qi = rv ? g4 - gi * (int)p.Tq : 0;
         const float4* qrow = reinterpret_cast<const float4*>(
@@ -707,7 +715,9 @@ int launch_pair_attention(AttParams p, int64_t max_tkv, cudaStream_t st) {
   CParams c;
   pair_plan(p.B * p.Hkv, max_tkv, c.nsplit, c.kps);
   c.items = p.Hkv * p.B * c.nsplit;
+  if (c.items >= (1ll << 31)) return HQMQ_ERR_UNSUPPORTED;
   c.ncw = kGroupOrder * p.S;
+  c.q_scale = p.scale_log2 * kProdScale / (float)((1 << p.br) - 1);
   const int64_t parts = p.B * p.Hkv * p.nrows * c.nsplit * kCW;
   p.part_ml = p.part_o + parts * 128;
   c.p = p;

@@ -109,7 +109,7 @@ template <typename OutT, bool kSmem>
 __global__ void __launch_bounds__(kDecThreads) decode_kernel(DecParams p) {
   extern __shared__ float4 tab_s[];
   const int64_t row = blockIdx.y;
-  const int h = (int)(row % p.H);
+  const int h = (int)((uint32_t)row % (uint32_t)p.H);  // (32-bit: no division subroutine)
   const int ncw = kGroupOrder * p.S;
   const float4* __restrict__ gtab = reinterpret_cast<const float4*>(p.table) + (int64_t)h * ncw;
   if (kSmem) {
@@ -330,7 +330,7 @@ __global__ void __launch_bounds__(256, 7) decode_fast_kernel(DecParams p) {
   __shared__ __align__(8) uint64_t tab_bar;
   __shared__ unsigned int released[kFDStages];
   const int64_t row = blockIdx.y;
-  const int h = (int)(row % p.H);
+  const int h = (int)((uint32_t)row % (uint32_t)p.H);  // (32-bit: no division subroutine)
   const int ncw = kGroupOrder * p.S;
   const int w = W ? W : p.w, br = BR ? BR : p.br;
   const FastDecodeGeom g = fd_geom(w, br);
@@ -460,7 +460,7 @@ __global__ void __launch_bounds__(256) decode_flag_kernel(DecParams p) {
   __shared__ __align__(8) uint64_t tab_bar;
   constexpr int kU = 4;
   const int64_t row = blockIdx.y;
-  const int h = (int)(row % p.H);
+  const int h = (int)((uint32_t)row % (uint32_t)p.H);  // (32-bit: no division subroutine)
   const int ncw = kGroupOrder * p.S;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   constexpr bool k16 = sizeof(OutT) == 2;
@@ -606,7 +606,7 @@ __global__ void __launch_bounds__(256, 6) decode_flag_tma_kernel(DecParams p) {
   __shared__ unsigned long long pay_base[kFlStages];
   __shared__ uint32_t pay_n[kFlStages];
   const int64_t row = blockIdx.y;
-  const int h = (int)(row % p.H);
+  const int h = (int)((uint32_t)row % (uint32_t)p.H);  // (32-bit: no division subroutine)
   const int ncw = kGroupOrder * p.S;
   const int w = W ? W : p.w, br = BR ? BR : p.br;  // compile-time for the model configs
   const FlagGeom g = fl_geom(w, br);
@@ -835,7 +835,7 @@ __global__ void __launch_bounds__(256, 6) decode_flag_tma_kernel(DecParams p) {
 // Bit-exact fp64 decode: ((q * sigma_w) / top) * codeword (codec.py:315-320).
 __global__ void __launch_bounds__(kDecThreads) decode_f64_kernel(DecParams p) {
   const int64_t row = blockIdx.y;
-  const int h = (int)(row % p.H);
+  const int h = (int)((uint32_t)row % (uint32_t)p.H);  // (32-bit: no division subroutine)
   const int ncw = kGroupOrder * p.S;
   const double* __restrict__ tab = reinterpret_cast<const double*>(p.table) + (int64_t)h * ncw * 4;
   const double top = (double)((1 << p.br) - 1);
