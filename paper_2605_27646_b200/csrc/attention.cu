@@ -1089,7 +1089,9 @@ __global__ void __launch_bounds__(kMThreads, 2) attention_mma_kernel(AttParams p
     const int gi = r / (int)p.Tq, qi = r - gi * (int)p.Tq;
     const int64_t hq = hkv * p.g + gi;
     if (p.splits == 1) {
-      p.out[((b * p.Hq + hq) * p.Tq + qi) * 128 + d] = O / L;
+      // (fast divide: an IEEE '/' here is a subroutine call, which makes ptxas keep
+      // the global-memory descriptor out of the uniform registers kernel-wide)
+      p.out[((b * p.Hq + hq) * p.Tq + qi) * 128 + d] = __fdividef(O, L);
     } else {
       const int64_t idx = (bh * p.nrows + r) * p.splits + blockIdx.x;
       p.part_o[idx * 128 + d] = O;
