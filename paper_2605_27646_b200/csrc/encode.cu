@@ -1348,7 +1348,9 @@ __global__ void __launch_bounds__(kOffThreads) token_offsets_kernel(
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
       const int64_t t = tok0 + j0 + k;
-      const double thr = per_head ? groups[(int)((t / T) % H)].threshold : thr0;
+      // (32-bit index arithmetic: n_tok < 2^31; a 64-bit division would be a
+      // subroutine call inside the unrolled loop)
+      const double thr = per_head ? groups[((uint32_t)t / (uint32_t)T) % (uint32_t)H].threshold : thr0;
       const bool fl = t < n_tok && sqrt_gt(v[k], thr);
       const uint32_t m = __ballot_sync(0xffffffffu, fl);
       if (lane == j0 + k && t < n_tok) mine = 32u - __popc(m);  // tokens past the end count 0
