@@ -433,16 +433,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCThreads, 1)
       R nx;
       if (warp < it.nblk) kload(nx, warp);
       for (int j = warp; j < it.nblk; j += kCW) {
-        const R cu = nx;
-        if (j + kCW < it.nblk) kload(nx, j + kCW);
+        // everything this block needs is taken out of the load buffer first,
+        // then the next block is loaded into the same registers (no copies)
         if (kPfDist > 0 && lane == 0 && j + kPfDist * kCW < it.nblk)
           prefetch_block<W, BR, kPaged>(p, own, it, (j + kPfDist * kCW) * kBK, true);
         typename R::Run ia, ib;
-        ia.align(cu.ia, sh_i);
-        ib.align(cu.ib, sh_i);
+        ia.align(nx.ia, sh_i);
+        ib.align(nx.ib, sh_i);
+        const float2 sk = __half22float2(__halves2half2(nx.ska, nx.skb));
+        float2 sv = __half22float2(__halves2half2(nx.sva, nx.svb));
+        uint32_t rq[4];  // radius words: b_r 4 -> (ra0, ra1, rb0, rb1); else (ra, rb, ra2, rb2)
+        if constexpr (BR == 4) {
+          rq[0] = nx.ra[0];
+          rq[1] = rq[0] >> 4;
+          rq[2] = nx.rb[0];
+          rq[3] = rq[2] >> 4;
+        } else {
+          rq[0] = __funnelshift_r(nx.ra[0], nx.ra[1], sh_r);
+          rq[1] = __funnelshift_r(nx.rb[0], nx.rb[1], sh_r);
+          rq[2] = nx.ra[1] >> sh_r;
+          rq[3] = nx.rb[1] >> sh_r;
+        }
+        if (j + kCW < it.nblk) kload(nx, j + kCW);
         float sc[4] = {0.f, 0.f, 0.f, 0.f};
         if constexpr (BR == 4) {
-          const uint32_t ra0 = cu.ra[0], ra1 = ra0 >> 4, rb0 = cu.rb[0], rb1 = rb0 >> 4;
+          const uint32_t ra0 = rq[0], ra1 = rq[1], rb0 = rq[2], rb1 = rq[3];
 #pragma unroll
           for (int ks = 0; ks < 8; ++ks) {
             const uint2 ca = lds64(ia.addr(ks, tab_lane));
@@ -462,9 +477,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCThreads, 1)
                   hmul2_raw(qb_, cb.y), qb[ks][0], qb[ks][1]);
           }
         } else {
-          const uint32_t ra = __funnelshift_r(cu.ra[0], cu.ra[1], sh_r);
-          const uint32_t rb = __funnelshift_r(cu.rb[0], cu.rb[1], sh_r);
-          const uint32_t ra2 = cu.ra[1] >> sh_r, rb2 = cu.rb[1] >> sh_r;
+          const uint32_t ra = rq[0], rb = rq[1], ra2 = rq[2], rb2 = rq[3];
           constexpr uint32_t kRM = (1u << BR) - 1u;
 #pragma unroll
           for (int ks = 0; ks < 8; ++ks) {
@@ -486,8 +499,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCThreads, 1)
           }
         }
         // sc = S^T[key a][r0], [a][r1], [b][r0], [b][r1]; per-key sigma_k
-        const float2 sk = __half22float2(__halves2half2(cu.ska, cu.skb));
-        float2 sv = __half22float2(__halves2half2(cu.sva, cu.svb));
         float s00 = sc[0] * sk.x, s01 = sc[1] * sk.x, s10 = sc[2] * sk.y, s11 = sc[3] * sk.y;
         const int kt0 = j * kBK;
         if (kt0 + kBK > vis_min) {  // some key of this block is masked (warp-uniform)
@@ -567,17 +578,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCThreads, 1)
       R nx;
       if (warp < it.nblk) vload(nx, warp);
       for (int j = warp; j < it.nblk; j += kCW) {
-        const R cu = nx;
-        if (j + kCW < it.nblk) vload(nx, j + kCW);
         if (kPfDist > 0 && lane == 0 && j + kPfDist * kCW < it.nblk)
           prefetch_block<W, BR, kPaged>(p, own, it, (j + kPfDist * kCW) * kBK, false);
         typename R::Run ic[4];
         uint32_t rr[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          ic[e].align(cu.iw[e], sh_i);
-          rr[e] = __funnelshift_r(cu.rw[e][0], cu.rw[e][1], sh_r);  // 4 codes of this lane
+          ic[e].align(nx.iw[e], sh_i);
+          rr[e] = __funnelshift_r(nx.rw[e][0], nx.rw[e][1], sh_r);  // 4 codes of this lane
         }
+        if (j + kCW < it.nblk) vload(nx, j + kCW);  // (into the registers just consumed)
         mbar_wait(mbox, u & 1u);  // the K twin's message has landed (complete-tx)
         // P^T B fragment of row g4, keys 2t4, 2t4+1, 2t4+8, 2t4+9 (positions
         // 4 t4 .. 4 t4 + 3 hold keys 2t4, 2t4+8, 2t4+1, 2t4+9); rescale
