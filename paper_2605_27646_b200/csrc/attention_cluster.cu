@@ -236,6 +236,24 @@ __device__ __forceinline__ int64_t token_of(const AttParams& p, const Item& it, 
     return it.bh * p.Tkv + key;
 }
 
+// the page id of item-relative block jb (paged caches), loaded a block ahead
+// of its code words so that the table read is off the code loads' critical path
+template <bool kPaged>
+__device__ __forceinline__ int32_t block_page(const AttParams& p, const Item& it, int jb) {
+  if constexpr (kPaged)
+    return __ldg(p.block_table + it.bh * p.max_pages + (it.kbeg + (int64_t)jb * kBK) / 128);
+  else
+    return 0;
+}
+template <bool kPaged>
+__device__ __forceinline__ int64_t block_token_pg(const AttParams& p, const Item& it, int jb, int32_t pg) {
+  const int64_t key = it.kbeg + (int64_t)jb * kBK;
+  if constexpr (kPaged)
+    return (int64_t)pg * 128 + (key & 127);
+  else
+    return it.bh * p.Tkv + key;
+}
+
 // prefetch the 16-key block at item-relative key k0 of one role into L2
 template <int W, int BR, bool kPaged>
 __device__ __forceinline__ void prefetch_block(const AttParams& p, const AttView& v, const Item& it,
@@ -423,15 +441,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCThreads, 1)
       // p = 2^-inf = 0 without special cases
       float m0 = -1e30f, m1 = -1e30f, l0 = 0.f, l1 = 0.f;  // l: this lane's partial sums
       const KOffs ko_full = k_offs<W, BR>(g4, g4 + 8, t4);
-      auto kload = [&](R& r, int jb) {
+      auto kload = [&](R& r, int jb, int32_t pg) {
         const int k0 = jb * kBK, klast = it.kend_rel - 1 - k0;
+        int64_t tok;
+        if constexpr (kPaged) tok = block_token_pg<true>(p, it, jb, pg);
+        else tok = block_token<false>(p, it, k0);
         if (klast >= kBK - 1)
-          k_load<W, BR>(r, p, block_token<kPaged>(p, it, k0), ko_full);
+          k_load<W, BR>(r, p, tok, ko_full);
         else  // the item's partial last block: clamp to its last key
-          k_load<W, BR>(r, p, block_token<kPaged>(p, it, k0), k_offs<W, BR>(min(g4, klast), min(g4 + 8, klast), t4));
+          k_load<W, BR>(r, p, tok, k_offs<W, BR>(min(g4, klast), min(g4 + 8, klast), t4));
       };
       R nx;
-      if (warp < it.nblk) kload(nx, warp);
+      if (warp < it.nblk) kload(nx, warp, kPaged ? block_page<kPaged>(p, it, warp) : 0);
+      int32_t pg_next = 0;  // (paged: the page of the block loaded next)
+      if constexpr (kPaged)
+        if (warp + kCW < it.nblk) pg_next = block_page<true>(p, it, warp + kCW);
       for (int j = warp; j < it.nblk; j += kCW) {
         // everything this block needs is taken out of the load buffer first,
         // then the next block is loaded into the same registers (no copies)
@@ -454,7 +478,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCThreads, 1)
           rq[2] = nx.ra[1] >> sh_r;
           rq[3] = nx.rb[1] >> sh_r;
         }
-        if (j + kCW < it.nblk) kload(nx, j + kCW);
+        if (j + kCW < it.nblk) {
+          kload(nx, j + kCW, pg_next);
+          if constexpr (kPaged)
+            if (j + 2 * kCW < it.nblk) pg_next = block_page<true>(p, it, j + 2 * kCW);
+        }
         float sc[4] = {0.f, 0.f, 0.f, 0.f};
         if constexpr (BR == 4) {
           const uint32_t ra0 = rq[0], ra1 = rq[1], rb0 = rq[2], rb1 = rq[3];
@@ -568,15 +596,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCThreads, 1)
       const uint32_t sh_i = ((uint32_t)g4 * 4u * W) & 31u, sh_r = ((uint32_t)g4 * 4u * BR) & 31u;
       const bool two = BR * 4 + (((uint32_t)g4 * 4u * BR) & 31u) > 32u;  // radius run spans 2 words
       const VOffs vo_full = v_offs<W, BR>(kBK - 1, g4, t4);
-      auto vload = [&](R& r, int jb) {
+      auto vload = [&](R& r, int jb, int32_t pg) {
         const int k0 = jb * kBK, klast = it.kend_rel - 1 - k0;
+        int64_t tok;
+        if constexpr (kPaged) tok = block_token_pg<true>(p, it, jb, pg);
+        else tok = block_token<false>(p, it, k0);
         if (klast >= kBK - 1)
-          v_load<W, BR>(r, p, block_token<kPaged>(p, it, k0), vo_full, two);
+          v_load<W, BR>(r, p, tok, vo_full, two);
         else
-          v_load<W, BR>(r, p, block_token<kPaged>(p, it, k0), v_offs<W, BR>(klast, g4, t4), two);
+          v_load<W, BR>(r, p, tok, v_offs<W, BR>(klast, g4, t4), two);
       };
       R nx;
-      if (warp < it.nblk) vload(nx, warp);
+      if (warp < it.nblk) vload(nx, warp, kPaged ? block_page<kPaged>(p, it, warp) : 0);
+      int32_t pg_next = 0;  // (paged: the page of the block loaded next)
+      if constexpr (kPaged)
+        if (warp + kCW < it.nblk) pg_next = block_page<true>(p, it, warp + kCW);
       for (int j = warp; j < it.nblk; j += kCW) {
         if (kPfDist > 0 && lane == 0 && j + kPfDist * kCW < it.nblk)
           prefetch_block<W, BR, kPaged>(p, own, it, (j + kPfDist * kCW) * kBK, false);
@@ -587,7 +621,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kCThreads, 1)
           ic[e].align(nx.iw[e], sh_i);
           rr[e] = __funnelshift_r(nx.rw[e][0], nx.rw[e][1], sh_r);  // 4 codes of this lane
         }
-        if (j + kCW < it.nblk) vload(nx, j + kCW);  // (into the registers just consumed)
+        if (j + kCW < it.nblk) {  // (into the registers just consumed)
+          vload(nx, j + kCW, pg_next);
+          if constexpr (kPaged)
+            if (j + 2 * kCW < it.nblk) pg_next = block_page<true>(p, it, j + 2 * kCW);
+        }
         mbar_wait(mbox, u & 1u);  // the K twin's message has landed (complete-tx)
         // P^T B fragment of row g4, keys 2t4, 2t4+1, 2t4+8, 2t4+9 (positions
         // 4 t4 .. 4 t4 + 3 hold keys 2t4, 2t4+8, 2t4+1, 2t4+9); rescale
