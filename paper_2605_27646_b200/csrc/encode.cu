@@ -860,6 +860,7 @@ __global__ void __launch_bounds__(256, 4) encode_prep_kernel(EncParams p) {
   const int64_t ntiles = ceil_div(p.T, kT);
   const int64_t stride = (int64_t)gridDim.x * 8;
   const InT* __restrict__ data = reinterpret_cast<const InT*>(p.data);
+  const uint32_t rw_k = (uint32_t)(BR * lane) >> 5, rw_s = (uint32_t)(BR * lane) & 31u;
   auto load_tile = [&](int64_t wt, uint2 (&raw)[kT]) {
 #pragma unroll
     for (int j = 0; j < kT; ++j) {
@@ -914,15 +915,17 @@ __global__ void __launch_bounds__(256, 4) encode_prep_kernel(EncParams p) {
         else q = exact_quantum(__dsqrt_rn(sq[j]), sw, top);
       }
       // the token's BR radius words: word k holds bits [32k, 32k+32) of the
-      // 32 x BR-bit run; lane l's code sits at bit BR*l
-      const uint32_t bit = (uint32_t)(BR * lane);
+      // 32 x BR-bit run; lane l's code sits at bit BR*l: in word rw_k at
+      // shift rw_s, its top bits in word rw_k + 1 when it straddles (the
+      // per-lane word / shift are loop invariants, so each word costs one
+      // select and one REDUX)
+      const uint32_t lo = q << rw_s, hi = rw_s + BR > 32 ? q >> (32 - rw_s) : 0u;
       uint32_t my = 0;
 #pragma unroll
       for (int k = 0; k < BR; ++k) {
-        const int d = (int)bit - 32 * k;  // code offset relative to word k
-        const uint32_t c = d >= 0 ? (d < 32 ? q << d : 0u) : (d > -BR ? q >> (-d) : 0u);
+        const uint32_t c = rw_k == (uint32_t)k ? lo : (rw_k + 1 == (uint32_t)k ? hi : 0u);
         const uint32_t word = __reduce_or_sync(0xffffffffu, c);
-        if (lane == k) my = word;
+        my = lane == k ? word : my;
       }
       if (lane < BR) p.radw[(tok0 + j) * BR + lane] = my;
     }
