@@ -874,8 +874,6 @@ __global__ void __launch_bounds__(256, 4) encode_prep_kernel(EncParams p) {
   uint2 raw[kT];
   load_tile(wt, raw);
   for (; wt < ntiles; wt += stride) {
-    uint2 nxt[kT];
-    load_tile(wt + stride, nxt);
     const int64_t t0 = wt * kT;
     const int ntok = (int)min((int64_t)kT, p.T - t0);
     const int64_t tok0 = row * p.T + t0;
@@ -894,22 +892,29 @@ __global__ void __launch_bounds__(256, 4) encode_prep_kernel(EncParams p) {
       const double m = warp_max_nonneg_f64(sq[j]);
       sig_l = lane == j ? m : sig_l;
     }
+    // the input is consumed: the next tile loads into the same registers
+    load_tile(wt + stride, raw);
     sig_l = __dsqrt_rn(lane < kT ? sig_l : 1.0);  // (lanes >= kT: off the slow path)
+    // lane j (< ntok): token j's fp16 scale, one coalesced store per tile
+    float sw_l;
+    {
+      const double sg = sig_l > 0.0 ? sig_l : 1.0;
+      const __half hs = __double2half(sg);
+      sw_l = __half2float(hs);
+      if (lane < ntok) {
+        p.scales[tok0 + lane] = __half_as_ushort(hs);
+        if (!(sw_l > 0.0f)) atomicOr(p.err, HQMQ_DEVERR_SIGMA_NONPOSITIVE);
+      }
+    }
 #pragma unroll
     for (int j = 0; j < kT; ++j) {
       if (j >= ntok) break;  // warp-uniform
-      double sg = __shfl_sync(0xffffffffu, sig_l, j);
-      if (!(sg > 0.0)) sg = 1.0;
-      const __half hs = __double2half(sg);
-      const double sw = (double)__half2float(hs);
-      if (lane == j) {
-        p.scales[tok0 + j] = __half_as_ushort(hs);
-        if (!(sw > 0.0)) atomicOr(p.err, HQMQ_DEVERR_SIGMA_NONPOSITIVE);
-      }
+      const float swf = __shfl_sync(0xffffffffu, sw_l, j);
+      const double sw = (double)swf;
       uint32_t q = 0;
       if (sq[j] > 0.0) {
         const float s32 = (float)sq[j];
-        const float vq = (s32 * rsqrtf(s32)) * __fdividef(ftop, (float)sw) + 0.5f;
+        const float vq = (s32 * rsqrtf(s32)) * __fdividef(ftop, swf) + 0.5f;
         const float fq = floorf(vq), fr = vq - fq;
         if (s32 > 1e-30f && fr >= qm && fr <= 1.0f - qm) q = (uint32_t)fminf(fmaxf(fq, 0.f), ftop);
         else q = exact_quantum(__dsqrt_rn(sq[j]), sw, top);
@@ -929,8 +934,6 @@ __global__ void __launch_bounds__(256, 4) encode_prep_kernel(EncParams p) {
       }
       if (lane < BR) p.radw[(tok0 + j) * BR + lane] = my;
     }
-#pragma unroll
-    for (int j = 0; j < kT; ++j) raw[j] = nxt[j];
   }
 }
 
