@@ -625,22 +625,32 @@ __global__ void __launch_bounds__(kWThreads, kMinB) encode_warp_kernel(EncParams
         sig_l = (lane % kWT) == j ? m : sig_l;
       }
       sig_l = __dsqrt_rn(lane < kWT ? sig_l : 1.0);  // (lanes >= kWT: off the slow path)
+      // lane j (< ntok): token j's fp16 scale and flag word, one coalesced
+      // store each per tile; the other lanes get the scale by a float shuffle
+      float sw_l;
+      {
+        const double sg = sig_l > 0.0 ? sig_l : 1.0;
+        const __half hs = __double2half(sg);
+        sw_l = __half2float(hs);
+        uint32_t myf = 0;
+  #pragma unroll
+        for (int j = 0; j < kWT; ++j) myf = lane == j ? fmask[j] : myf;
+        if (lane < ntok) {
+          p.scales[tok0 + lane] = __half_as_ushort(hs);
+          if (!(sw_l > 0.0f)) atomicOr(p.err, HQMQ_DEVERR_SIGMA_NONPOSITIVE);
+          if (ext) p.flagw[tok0 + lane] = myf;
+        }
+      }
   #pragma unroll
       for (int j = 0; j < kWT; ++j) {
         const bool valid = j < ntok;
         const bool fl = (fmask[j] >> lane) & 1u;
-        double sg = __shfl_sync(0xffffffffu, sig_l, j);
-        if (!(sg > 0.0)) sg = 1.0;
-        const __half hs = __double2half(sg);
-        const double sw = (double)__half2float(hs);
-        if (valid && lane == j) {
-          p.scales[tok0 + j] = __half_as_ushort(hs);
-          if (!(sw > 0.0)) atomicOr(p.err, HQMQ_DEVERR_SIGMA_NONPOSITIVE);
-        }
+        const float swf = __shfl_sync(0xffffffffu, sw_l, j);
+        const double sw = (double)swf;
         if (valid && !fl && sq[j] > 0.0) {
           const float s32 = (float)sq[j];
           uint32_t q;
-          const float vq = (s32 * rsqrtf(s32)) * __fdividef(ftop, (float)sw) + 0.5f;
+          const float vq = (s32 * rsqrtf(s32)) * __fdividef(ftop, swf) + 0.5f;
           const float fq = floorf(vq), fr = vq - fq;
           if (s32 > 1e-30f && fr >= qm && fr <= 1.0f - qm) q = (uint32_t)fminf(fmaxf(fq, 0.f), ftop);
           else q = exact_quantum(__dsqrt_rn(sq[j]), sw, top);
@@ -660,7 +670,6 @@ __global__ void __launch_bounds__(kWThreads, kMinB) encode_warp_kernel(EncParams
               reinterpret_cast<ushort4*>(p.payloads)[prow] = hv;
             }
           }
-          if (lane == j) p.flagw[tok0 + j] = fmask[j];
           coded_run += __popc(~fmask[j]);
         }
       }
