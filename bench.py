@@ -329,7 +329,11 @@ def run_ours(args, wl, world, rank, local):
     launches = {"n": 0}
     # set_counts + prep + search; with Med3x: radix_init, 3 histogram passes, radix_tail,
     # token counts, CUB scan (2), finalize_counts, prep, search
-    per_encode = 3 if wl["C"] is None else 11
+    # our kernels per call (memsets are not kernels): encode = prep + search;
+    # Med3x adds the median sample + two narrowing passes (+1 for groups over
+    # ~8.4M chunks) and the token-offset scan; decode = one kernel
+    n_group = wl["batch"] * wl["heads"] * wl["tokens"] * (wl["head_dim"] // 4)
+    per_encode = 2 if wl["C"] is None else (6 + (1 if n_group > 2048 * 1024 * 4 else 0))
     per_decode = 1
 
     def step(single=False):
