@@ -7,21 +7,25 @@
 // section streams (kvpack.py:66-76,134-146).
 //
 // Kernel pipeline for one (layer, role) call, all stream-ordered, no host sync:
-//   [extraction on]  norms_hist (pass 0)  -> radix_hist x4 (exact rank-(n-1)//2
-//                    select on the fp64 bit patterns; last block selects)
-//                    -> tile_count -> cub exclusive scan -> finalize_counts
-//   encode_tile: one CTA per tile of <=1024 chunks of one (batch, head) row.
-//     1. exact fp64 norms, outlier flags (ballot), per-token sigma -> fp16 scale
-//     2. fp32 search: for every secondary s (rotation table staged in smem),
-//        v = u (x) conj(q_s) with 8 FFMA2; coset score = max(max|v_i|, sum|v_i|/2)
-//        (closed form over the 24 elements of 2T); running top-2 per chunk
-//     3. certification: gap between best and runner-up (other cosets and the
-//        within-coset runner-up) > kDelta proves the fp64 reference picks the
-//        same (p, s); otherwise a warp re-scores all candidate cosets with the
-//        reference's exact fp64 arithmetic and lowest-flat-index tie-break
-//     4. pack indices / radius quanta / flag bits into the section streams
-//        (smem staging, plain stores for owned words, atomicOr on shared edge
-//        words), token offsets, fp16 payload rows.
+//   [Med3x]  median_sample_kernel (strided 512-key sample -> bracket) ->
+//            median_pass_kernel x2-3 (norms stored; narrowing histogram /
+//            compaction; exact rank-(n-1)//2 select on the fp64 bit patterns)
+//            -> token_offsets_kernel (flags, coded counts, one-pass look-back
+//            scan) [tile path: tile_count -> cub scan -> finalize_counts]
+//   [head_dim 128, 2-byte inputs: the warp path]
+//     prep: encode_prep_kernel (no extraction: exact norms, sigma -> fp16
+//           scale, quanta, radius words by REDUX) or encode_warp_kernel<..,1>
+//           (Med3x: + flags, payload rows, shifted radius runs)
+//     search: encode_tc_kernel (tcgen05: the S-loop's rotations as split-fp16
+//           MMAs into TMEM, closed-form coset scores on the CUDA cores) or
+//           encode_warp_kernel<..,2> (FFMA2 search when S is not a multiple of 16)
+//     both: certification of the fp32 winner against the runner-up with a
+//           proven margin, else the warp re-scores the candidate cosets with
+//           the reference's exact fp64 arithmetic and lowest-index tie-break;
+//           index stream packed into the serialized section
+//   [other shapes] encode_tile_kernel: one CTA per tile of <= 1024 chunks,
+//     all of the above in one pass (smem-staged bit streams, atomicOr on
+//     shared edge words).
 #include <cub/cub.cuh>
 
 #include <algorithm>
