@@ -11,7 +11,12 @@
 // packed streams (funnel shift across 32-bit words) and the token's fp16
 // scale, gathers the codeword from smem and writes the 4 reconstructed
 // elements.  Flagged chunks come from the fp16 payload rows, addressed through
-// the per-token coded offsets.
+// the per-token coded offsets.  The model shapes take the TMA-ring kernels:
+// decode_fast_kernel (no extraction: token-aligned streams, two tokens per
+// warp instruction) and decode_flag_tma_kernel (Med3x: a 64-token tile's
+// compact code runs, flag words, offsets, scales and payload rows per ring
+// stage, a chunk quad per lane); decode_f64_kernel is the bit-exact fp64 path;
+// expand_kernel / paged_append_kernel serve the paged cache.
 #include <cub/cub.cuh>
 
 #include <algorithm>
